@@ -1,0 +1,574 @@
+"""Pins for the CPU oracle.  No GPU.
+
+Every check compares the oracle with something other than itself: a known-answer vector, a library
+routine (torch avg_pool2d / conv), a closed form, brute force, or an invariant the paper's equations
+fix.  Together they are chosen so that a dropped term, a wrong sign or index, a transposed operand or
+a wrong summation/selection rule in the oracle fails at least one of them.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as TF
+
+import oracle as O
+from synth import constant_video, iid_frames, moving_texture, static_textured_video, textured_frame
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ------------------------------------------------------------------ independent numpy helpers (float64)
+def np_patch_dist_field(A, B, F, p):
+    """D for every target pixel of candidate field F, zero padding (D9), float64, plain definition."""
+    h, w, _ = A.shape
+    Ap = np.pad(A.astype(np.float64), ((p, p), (p, p), (0, 0)))
+    Bp = np.pad(B.astype(np.float64), ((p, p), (p, p), (0, 0)))
+    rr, cc = np.mgrid[0:h, 0:w]
+    D = np.zeros((h, w))
+    for dr in range(-p, p + 1):
+        for dc in range(-p, p + 1):
+            b = Bp[rr + dr + p, cc + dc + p]
+            a = Ap[F[..., 0] + dr + p, F[..., 1] + dc + p]
+            D += ((b - a) ** 2).sum(-1)
+    return D
+
+
+def np_remap_votes(S, F, p):
+    """The O(hwp^2) formulation of P:99-101: cut the source into patches, rearrange them by F,
+    average the overlapping parts.  Scatter form (each target pixel's matched patch votes onto its
+    (2p+1)^2 neighbourhood), valid votes only (D19).  float64."""
+    h, w, _ = S.shape
+    acc = np.zeros((h, w, 3))
+    cnt = np.zeros((h, w))
+    for x in range(h):
+        for y in range(w):
+            sx, sy = F[x, y]
+            for dx in range(-p, p + 1):
+                for dy in range(-p, p + 1):
+                    tx, ty, ux, uy = x + dx, y + dy, sx + dx, sy + dy
+                    if 0 <= tx < h and 0 <= ty < w and 0 <= ux < h and 0 <= uy < w:
+                        acc[tx, ty] += S[ux, uy]
+                        cnt[tx, ty] += 1
+    return acc / cnt[..., None]
+
+
+def brute_force_min(A, B, p):
+    """Exhaustive NNF under the base loss: min over every source position (float64)."""
+    h, w, _ = A.shape
+    best = np.full((h, w), np.inf)
+    arg = np.zeros((h, w, 2), np.int64)
+    nbest = np.zeros((h, w), np.int64)
+    for sr in range(h):
+        for sc in range(w):
+            F = np.empty((h, w, 2), np.int64)
+            F[..., 0], F[..., 1] = sr, sc
+            D = np_patch_dist_field(A, B, F, p)
+            better = D < best
+            tie = D == best
+            nbest[tie] += 1
+            nbest[better] = 1
+            arg[better] = (sr, sc)
+            best = np.minimum(best, D)
+    return best, arg, nbest
+
+
+# ------------------------------------------------------------------ P1 Philox
+def test_philox_known_answers():
+    rows = [l.split() for l in open(os.path.join(GOLDEN, "philox_kat.txt")) if l.strip() and not l.startswith("#")]
+    assert len(rows) == 3
+    for row in rows:
+        v = [int(x, 16) for x in row]
+        assert O.philox4x32_10(v[0:4], v[4:6]) == v[6:10]
+
+
+# ------------------------------------------------------------------ P2 pyramid
+def test_pyramid_equals_avg_pool():
+    rng = np.random.default_rng(0)
+    img = rng.integers(0, 256, size=(75, 101, 3)).astype(np.float32)
+    lv = 5
+    pyr = O.pyramid(img, lv)
+    ref = torch.from_numpy(img.astype(np.float64)).permute(2, 0, 1)[None]
+    for k in range(lv):
+        if k:
+            ref = TF.avg_pool2d(ref, 2)  # floor dims, 2x2 mean (D6)
+        assert pyr[k].shape == (75 >> k, 101 >> k, 3)
+        np.testing.assert_array_equal(pyr[k].astype(np.float64), ref[0].permute(1, 2, 0).numpy())
+
+
+def test_pyramid_constant():
+    img = np.full((64, 48, 3), 77.0, np.float32)
+    for lev in O.pyramid(img, 4):
+        assert np.all(lev == 77.0)
+
+
+@pytest.mark.parametrize("H,W,p,req,expect", [
+    (64, 64, 2, 0, 2), (512, 512, 2, 0, 5), (768, 768, 2, 0, 5), (1080, 1920, 3, 0, 6),
+    (16, 16, 2, 0, 1), (4, 4, 2, 0, -1), (64, 64, 2, 5, -1), (64, 64, 2, 3, 3), (40, 40, 9, 0, 1)])
+def test_level_count(H, W, p, req, expect):
+    assert O.level_count(H, W, p, req) == expect
+
+
+# ------------------------------------------------------------------ P3 patch distance
+def test_patch_dist_closed_forms():
+    z = np.zeros((9, 9, 3), np.float32)
+    o = np.ones((9, 9, 3), np.float32)
+    f = np.full((9, 9, 3), 255.0, np.float32)
+    assert O.patch_dist(z, o, 4, 4, 4, 4, 1) == 27.0
+    assert O.patch_dist(z, f, 4, 4, 4, 4, 1) == 27.0 * 65025.0
+    assert O.patch_dist(f, f, 3, 5, 3, 5, 2) == 0.0
+    # corners: taps outside read 0 on both sides (D9) -> only in-bounds source taps count
+    assert O.patch_dist(f, z, 0, 0, 0, 0, 1) == 4 * 3 * 65025.0
+    assert O.patch_dist(f, z, 0, 0, 0, 0, 2) == 9 * 3 * 65025.0
+    assert O.patch_dist(f, z, 8, 0, 8, 0, 2) == 9 * 3 * 65025.0
+    # source at a corner, target interior: the 16 target taps whose source tap falls outside read
+    # 0 - B = -255 ... here B = 0 so they vanish; the 9 inside count 255^2 each
+    assert O.patch_dist(f, z, 0, 0, 4, 4, 2) == 9 * 3 * 65025.0
+
+
+@pytest.mark.parametrize("shift", [(2, -3), (-1, 4), (0, 1)])
+def test_patch_dist_constant_shift_equals_library_box_filter(shift):
+    """For F(r,c) = (r+a, c+b): D = (2p+1)^2 * avg_pool2d(sq. diff, 2p+1, stride 1, pad p) in the
+    interior (library routine)."""
+    rng = np.random.default_rng(1)
+    A = rng.integers(0, 256, size=(23, 31, 3)).astype(np.float32)
+    B = rng.integers(0, 256, size=(23, 31, 3)).astype(np.float32)
+    p, (a, b) = 2, shift
+    h, w, _ = A.shape
+    Ash = np.zeros_like(A, dtype=np.float64)
+    r0, r1 = max(0, -a), min(h, h - a)
+    c0, c1 = max(0, -b), min(w, w - b)
+    Ash[r0:r1, c0:c1] = A[r0 + a:r1 + a, c0 + b:c1 + b]
+    Q = ((B.astype(np.float64) - Ash) ** 2).sum(-1)
+    box = TF.avg_pool2d(torch.from_numpy(Q)[None, None], 2 * p + 1, stride=1, padding=p,
+                        count_include_pad=True)[0, 0].numpy() * (2 * p + 1) ** 2
+    for r in range(p, h - p):
+        for c in range(p, w - p):
+            sr, sc = r + a, c + b
+            if 0 <= sr < h and 0 <= sc < w:
+                assert float(O.patch_dist(A, B, sr, sc, r, c, p)) == pytest.approx(box[r, c], rel=1e-12, abs=1e-6)
+
+
+def test_patch_dist_random_float_within_fp32_rounding():
+    rng = np.random.default_rng(2)
+    A = (rng.random((12, 14, 3)) * 255).astype(np.float32)
+    B = (rng.random((12, 14, 3)) * 255).astype(np.float32)
+    F = np.stack([rng.integers(0, 12, (12, 14)), rng.integers(0, 14, (12, 14))], -1)
+    ref = np_patch_dist_field(A, B, F, 3)
+    for r in range(12):
+        for c in range(14):
+            got = float(O.patch_dist(A, B, int(F[r, c, 0]), int(F[r, c, 1]), r, c, 3))
+            assert got == pytest.approx(ref[r, c], rel=2e-6)
+
+
+# ------------------------------------------------------------------ P4 remap
+def test_remap_identity_and_constant_exact():
+    S = textured_frame(20, 17).astype(np.float32)
+    rr, cc = np.mgrid[0:20, 0:17]
+    Fid = np.stack([rr, cc], -1).astype(np.int32)
+    np.testing.assert_array_equal(O.remap(S, Fid, 2), S)
+    rng = np.random.default_rng(3)
+    Fr = np.stack([rng.integers(0, 20, (20, 17)), rng.integers(0, 17, (20, 17))], -1).astype(np.int32)
+    K = np.full_like(S, 123.0)
+    np.testing.assert_array_equal(O.remap(K, Fr, 3), K)
+
+
+def test_remap_shift_equals_roll_in_interior():
+    S = textured_frame(24, 30).astype(np.float32)
+    a, b, p = 3, -2, 2
+    rr, cc = np.mgrid[0:24, 0:30]
+    F = np.stack([np.clip(rr + a, 0, 23), np.clip(cc + b, 0, 29)], -1).astype(np.int32)
+    out = O.remap(S, F, p)
+    ref = np.roll(S, (-a, -b), axis=(0, 1))
+    m = p + 5
+    np.testing.assert_array_equal(out[m:-m, m:-m], ref[m:-m, m:-m])
+
+
+def test_remap_equals_patch_vote_formulation():
+    rng = np.random.default_rng(4)
+    S = (rng.random((11, 13, 3)) * 255).astype(np.float32)
+    F = np.stack([rng.integers(0, 11, (11, 13)), rng.integers(0, 13, (11, 13))], -1).astype(np.int32)
+    for p in (1, 2, 3):
+        np.testing.assert_allclose(O.remap(S, F, p), np_remap_votes(S, F, p), rtol=2e-6)
+
+
+def test_remap_linearity():
+    """Eq. 5: remapping is linear in the image (up to FP32 rounding)."""
+    rng = np.random.default_rng(5)
+    S1 = (rng.random((16, 16, 3)) * 255).astype(np.float32)
+    S2 = (rng.random((16, 16, 3)) * 255).astype(np.float32)
+    F = np.stack([rng.integers(0, 16, (16, 16)), rng.integers(0, 16, (16, 16))], -1).astype(np.int32)
+    lhs = O.remap((0.25 * S1 + 0.75 * S2).astype(np.float32), F, 2)
+    rhs = 0.25 * O.remap(S1, F, 2) + 0.75 * O.remap(S2, F, 2)
+    np.testing.assert_allclose(lhs, rhs, rtol=1e-5, atol=1e-4)
+
+
+# ------------------------------------------------------------------ single fields of Alg. 1
+def _shifted_pair(h, w, a, b, seed=6):
+    rng = np.random.default_rng(seed)
+    S = rng.integers(0, 256, size=(h, w, 3)).astype(np.float32)
+    T = rng.integers(0, 256, size=(h, w, 3)).astype(np.float32)
+    rr, cc = np.mgrid[0:h, 0:w]
+    inside = (rr + a >= 0) & (rr + a < h) & (cc + b >= 0) & (cc + b < w)
+    T[inside] = S[(rr + a)[inside], (cc + b)[inside]]
+    Ftrue = np.stack([np.clip(rr + a, 0, h - 1), np.clip(cc + b, 0, w - 1)], -1).astype(np.int32)
+    return S, T, Ftrue
+
+
+@pytest.mark.parametrize("field", [0, 1, 2, 3])
+def test_propagation_field(field):
+    """F'(x,y) = F(x+dx, y+dy) - (dx,dy), Jacobi, strict-min select."""
+    h, w, p = 20, 22, 2
+    a, b = 1, -2
+    S, T, Ftrue = _shifted_pair(h, w, a, b)
+    cfg = O.Cfg(patch_radius=p, loss=O.BASE, levels=1)
+    rng = np.random.default_rng(10 + field)
+    bad = rng.random((h, w)) < 0.3
+    Fin = Ftrue.copy()
+    Fin[bad] = np.stack([rng.integers(0, h, bad.sum()), rng.integers(0, w, bad.sum())], -1)
+    _, Ein = O.field(cfg, S, T, Fin, np.zeros((h, w), np.float32), -1)
+    np.testing.assert_array_equal(Ein, np_patch_dist_field(S, T, Fin, p).astype(np.float32))
+    Fout, Eout = O.field(cfg, S, T, Fin, Ein, field)
+    dx, dy = [(-1, 0), (1, 0), (0, -1), (0, 1)][field]
+    assert np.all(Eout <= Ein)
+    changed = np.any(Fout != Fin, -1)
+    assert np.all(Eout[changed] < Ein[changed])
+    fixed_expected = 0
+    for r in range(h):
+        for c in range(w):
+            nr, nc = min(max(r + dx, 0), h - 1), min(max(c + dy, 0), w - 1)
+            cand = (min(max(Fin[nr, nc, 0] - dx, 0), h - 1), min(max(Fin[nr, nc, 1] - dy, 0), w - 1))
+            # Jacobi: the only admissible outcomes are the incumbent or the neighbour-derived candidate
+            assert tuple(Fout[r, c]) in (tuple(Fin[r, c]), cand)
+            interior = p <= r + a < h - p and p <= c + b < w - p and p <= r < h - p and p <= c < w - p
+            if bad[r, c] and not bad[nr, nc] and (nr, nc) != (r, c) and interior and Ein[r, c] > 0:
+                assert tuple(Fout[r, c]) == tuple(Ftrue[r, c]) and Eout[r, c] == 0
+                fixed_expected += 1
+    assert fixed_expected > 10
+
+
+def test_random_search_offsets_uniform():
+    """Random search draws F' = F + (dx,dy), dx,dy uniform integers in [-R, R] (D13), from a
+    stream keyed by (level, iteration, step, pixel, src, tgt, tag) (D21)."""
+    h, w = 64, 64
+    cfg = O.Cfg(patch_radius=1, loss=O.BASE, levels=1, rs_radius0=8)
+    img = np.zeros((h, w, 3), np.float32)
+    Fin = np.full((h, w, 2), 32, np.int32)
+    Einf = np.full((h, w), np.inf, np.float32)  # every candidate accepted -> F' is observable
+    offs = {}
+    for s, R in [(0, 8), (1, 4), (3, 1)]:
+        Fo, _ = O.field(cfg, img, img, Fin, Einf, 4 + s, k=0, it=0, src_id=3, tgt_id=4)
+        off = Fo - 32
+        assert off.min() >= -R and off.max() <= R
+        assert off[..., 0].min() == -R and off[..., 0].max() == R and off[..., 1].min() == -R
+        hist = np.bincount((off[..., 0] + R).ravel(), minlength=2 * R + 1)
+        exp = h * w / (2 * R + 1)
+        chi2 = ((hist - exp) ** 2 / exp).sum()
+        assert chi2 < 3 * (2 * R + 1) + 30
+        assert abs(np.corrcoef(off[..., 0].ravel(), off[..., 1].ravel())[0, 1]) < 0.08
+        offs[s] = off
+    base = O.field(cfg, img, img, Fin, Einf, 4, k=0, it=0, src_id=3, tgt_id=4)[0]
+    for kw in (dict(k=1), dict(it=1), dict(src_id=5), dict(tgt_id=5), dict(tag=2)):
+        args = dict(k=0, it=0, src_id=3, tgt_id=4)
+        args.update(kw)
+        other = O.field(cfg, img, img, Fin, Einf, 4, **args)[0]
+        assert np.mean(np.all(other == base, -1)) < 0.2
+
+
+def test_random_init_uniform_non_square():
+    """"Randomly initialize F": uniform over the source grid; rows < h, cols < w."""
+    h, w = 40, 96
+    g = iid_frames(2, h, w)
+    cfg = O.Cfg(patch_radius=2, levels=1, iters_per_level=0, loss=O.BASE)
+    F, _, _, ev = O.nnf(cfg, g.astype(np.float32), [dict(src_guide=0, tgt_guide=1, src_id=0, tgt_id=1)], want_x=False)
+    assert ev == 0
+    F = F[0]
+    assert F[..., 0].min() == 0 and F[..., 0].max() == h - 1
+    assert F[..., 1].min() == 0 and F[..., 1].max() == w - 1
+    assert abs(F[..., 0].mean() - (h - 1) / 2) < 1.5 and abs(F[..., 1].mean() - (w - 1) / 2) < 3
+
+
+# ------------------------------------------------------------------ P5 brute force
+@pytest.mark.parametrize("h,w,kind,seed", [(8, 8, "iid", 1), (12, 12, "iid", 3), (10, 12, "tex", 2)])
+def test_patchmatch_reaches_brute_force_minimum(h, w, kind, seed):
+    """Tiny frames, base loss, one level, many iterations: the PatchMatch error equals the exhaustive
+    minimum at every pixel and the coordinates equal the unique minimiser (D16 ties excluded)."""
+    if kind == "iid":
+        fr = iid_frames(2, h, w, seed=seed).astype(np.float32)
+    else:
+        fr = np.stack([textured_frame(h, w, seed=seed), textured_frame(h, w, seed=seed + 100)]).astype(np.float32)
+    p = 2
+    cfg = O.Cfg(patch_radius=p, levels=1, iters_per_level=300, loss=O.BASE, seed=seed)
+    F, E, _, _ = O.nnf(cfg, fr, [dict(src_guide=0, tgt_guide=1, src_id=0, tgt_id=1)], want_x=False)
+    best, arg, nbest = brute_force_min(fr[0], fr[1], p)
+    np.testing.assert_array_equal(E[0].astype(np.float64), best)
+    uniq = nbest == 1
+    np.testing.assert_array_equal(F[0][uniq], arg[uniq])
+
+
+@pytest.mark.parametrize("h,w,seed", [(16, 16, 1), (24, 20, 2)])
+def test_patchmatch_error_is_loss_of_field_and_bounded_by_brute_force(h, w, seed):
+    """E is exactly the loss of the returned F, never below the exhaustive minimum, and
+    equal to it on most pixels after a moderate number of iterations."""
+    fr = np.stack([textured_frame(h, w, seed=seed), textured_frame(h, w, seed=seed + 100)]).astype(np.float32)
+    p = 2
+    cfg = O.Cfg(patch_radius=p, levels=1, iters_per_level=40, loss=O.BASE, seed=seed)
+    F, E, _, _ = O.nnf(cfg, fr, [dict(src_guide=0, tgt_guide=1, src_id=0, tgt_id=1)], want_x=False)
+    best, _, _ = brute_force_min(fr[0], fr[1], p)
+    np.testing.assert_array_equal(E[0].astype(np.float64), np_patch_dist_field(fr[0], fr[1], F[0], p))
+    assert np.all(E[0] >= best)
+    assert np.mean(E[0] == best) >= 0.85
+
+
+# ------------------------------------------------------------------ P6 identity
+def test_identity_init_identical_frames_stays_identity():
+    g = textured_frame(48, 40)[None].repeat(2, 0)
+    frames = np.concatenate([g, g]).astype(np.float32)
+    for loss in (O.BASE, O.GUIDE_STYLE):
+        cfg = O.Cfg(patch_radius=2, iters_per_level=2, loss=loss, init=O.INIT_IDENTITY)
+        F, E, X, _ = O.nnf(cfg, frames, [dict(src_guide=0, tgt_guide=1, src_style=2, src_id=0, tgt_id=1)])
+        rr, cc = np.mgrid[0:48, 0:40]
+        assert np.all(F[0][..., 0] == rr) and np.all(F[0][..., 1] == cc)
+        assert np.all(E[0] == 0)
+        np.testing.assert_array_equal(X[0], frames[2])
+
+
+def test_random_init_identical_frames_converges_to_identity():
+    g = textured_frame(64, 64, seed=5)[None].astype(np.float32)
+    cfg = O.Cfg(patch_radius=2, iters_per_level=5, loss=O.BASE)
+    F, E, _, _ = O.nnf(cfg, np.concatenate([g, g]), [dict(src_guide=0, tgt_guide=1, src_id=0, tgt_id=1)])
+    rr, cc = np.mgrid[0:64, 0:64]
+    ident = (F[0][..., 0] == rr) & (F[0][..., 1] == cc)
+    assert ident.mean() == 1.0
+    assert np.all(E[0] == 0)
+
+
+# ------------------------------------------------------------------ P7 constant video
+def test_constant_video_every_schedule_exact():
+    g, s = constant_video(6, 32, 40)
+    cfg = O.Cfg(patch_radius=2, iters_per_level=2)
+    for fn, loss in ((O.blend_direct, O.GUIDE_STYLE), (O.blend_direct, O.MEAN_ALIGN), (O.blend_tree, O.GUIDE_STYLE)):
+        cfg.loss = loss
+        out, _, _ = fn(cfg, g, s, 2)
+        np.testing.assert_array_equal(out, s.astype(np.float32))
+    cfg.loss = O.GUIDE_STYLE
+    out, _, _ = O.interpolate(cfg, g, [1, 4], s[[1, 4]])
+    np.testing.assert_array_equal(out, s.astype(np.float32))
+
+
+# ------------------------------------------------------------------ P8 tree bookkeeping
+@pytest.mark.parametrize("N,M", [(8, 3), (13, 4), (9, 8), (5, 0), (1, 3), (12, 1)])
+def test_static_video_direct_and_tree_equal_exact_window_mean(N, M):
+    """Static textured guide + identity init: every NNF stays identity (E = 0 is never beaten), all
+    cells are exact dyadic means, so both schedules must equal the correctly rounded truncated-window
+    mean of the style frames bit for bit (Eq. 2 with D3/D4; Alg. 3-5 and Eq. 6 with D23-D26)."""
+    g, s = static_textured_video(N, 24, 28)
+    cfg = O.Cfg(patch_radius=2, iters_per_level=1, init=O.INIT_IDENTITY, loss=O.GUIDE_STYLE)
+    direct, pd, _ = O.blend_direct(cfg, g, s, M)
+    tree, pt, _ = O.blend_tree(cfg, g, s, M)
+    ref = np.empty_like(direct)
+    s64 = s.astype(np.int64)
+    for i in range(N):
+        lo, hi = max(0, i - M), min(N - 1, i + M)
+        ref[i] = (s64[lo:hi + 1].sum(0) / (hi - lo + 1)).astype(np.float32)
+    np.testing.assert_array_equal(direct, ref)
+    np.testing.assert_array_equal(tree, ref)
+
+
+# ------------------------------------------------------------------ P9 counts
+def test_tree_counts_and_query_structure():
+    assert len(O.tree_build_tasks(8, 3)) == 12          # S:295 (L_max = ceil(log2 8))
+    assert len(O.tree_build_tasks(2, 1)) == 1
+    assert O.tree_query_nodes(0, 6) == [(6, 0), (5, 1), (3, 2)]
+    for r in range(64):
+        for l in range(r + 1):
+            nodes = O.tree_query_nodes(l, r)
+            covered = []
+            for i, L in nodes:
+                covered += list(range(i - (1 << L) + 1, i + 1))
+                assert i & ((1 << L) - 1) == (1 << L) - 1   # BT(i,L) exists only for i with L low ones
+            assert sorted(covered) == list(range(l, r + 1))   # exact partition of [l, r]
+            assert len(nodes) <= 2 * math.log2(r - l + 2) + 1
+
+
+def test_pair_counts_per_config():
+    g, s = moving_texture(8, 64, 64)
+    cfg = O.Cfg(patch_radius=2, iters_per_level=2)
+    _, pairs, evals = O.blend_direct(cfg, g, s, 3)
+    assert pairs == 36 and evals == 36 * 120832 == 4349952
+    _, pairs, _ = O.blend_tree(cfg, g, s, 3)
+    assert pairs == 28
+    assert O.evals_per_task(O.Cfg(patch_radius=2, iters_per_level=5), 512, 512) == 25615360
+    assert O.evals_per_task(O.Cfg(patch_radius=2, iters_per_level=5), 768, 768) == 57634560
+    assert O.evals_per_task(O.Cfg(patch_radius=3, iters_per_level=5), 1080, 1920) == 216537300
+    # direct pair counts (sum over targets of |W_i| - 1)
+    for N, M, expect in ((200, 15, 5760), (1000, 15, 29760), (200, 30, 11070)):
+        assert sum(min(N - 1, i + M) - max(0, i - M) for i in range(N)) == expect
+
+
+# ------------------------------------------------------------------ P10 monotonicity / bounds
+def test_error_non_increasing_with_iterations_and_bounds():
+    fr = iid_frames(2, 32, 36, seed=9).astype(np.float32)
+    prev = None
+    for n in (1, 2, 3):
+        cfg = O.Cfg(patch_radius=2, levels=1, iters_per_level=n, loss=O.BASE)
+        F, E, _, _ = O.nnf(cfg, fr, [dict(src_guide=0, tgt_guide=1, src_id=0, tgt_id=1)], want_x=False)
+        assert F[..., 0].min() >= 0 and F[..., 0].max() < 32 and F[..., 1].min() >= 0 and F[..., 1].max() < 36
+        if prev is not None:
+            assert np.all(E <= prev)
+            assert np.any(E < prev)
+        prev = E
+
+
+# ------------------------------------------------------------------ P11 determinism
+def test_batch_and_thread_invariance():
+    g, s = moving_texture(4, 40, 48, seed=3)
+    frames = np.concatenate([g, s]).astype(np.float32)
+    cfg = O.Cfg(patch_radius=2, iters_per_level=2, loss=O.GUIDE_STYLE)
+    tasks = [dict(src_guide=j, tgt_guide=0, src_style=4 + j, src_id=j, tgt_id=0, tag=0) for j in (1, 2, 3)]
+    Fb, Eb, Xb, _ = O.nnf(cfg, frames, tasks)
+    for t, tk in enumerate(tasks):
+        F1, E1, X1, _ = O.nnf(cfg, frames, [tk])
+        np.testing.assert_array_equal(F1[0], Fb[t])
+        np.testing.assert_array_equal(E1[0], Eb[t])
+        np.testing.assert_array_equal(X1[0], Xb[t])
+    n0 = O.num_threads()
+    try:
+        O.set_threads(1)
+        F1, E1, _, _ = O.nnf(cfg, frames, tasks)
+    finally:
+        O.set_threads(n0)
+    np.testing.assert_array_equal(F1, Fb)
+    np.testing.assert_array_equal(E1, Eb)
+
+
+# ------------------------------------------------------------------ P12 convergence quality
+def test_shifted_texture_reconstruction_psnr():
+    """a 128^2 texture vs its (3,5) circular shift is reconstructed at >= 35 dB."""
+    S = textured_frame(128, 128, seed=21).astype(np.float32)
+    T = np.roll(S, (3, 5), axis=(0, 1))
+    cfg = O.Cfg(patch_radius=2, iters_per_level=5, loss=O.GUIDE_STYLE)
+    frames = np.stack([S, T, S])
+    F, E, X, _ = O.nnf(cfg, frames, [dict(src_guide=0, tgt_guide=1, src_style=2, src_id=0, tgt_id=1)])
+    m = 2 + 5
+    mse = np.mean((X[0][m:-m, m:-m].astype(np.float64) - T[m:-m, m:-m]) ** 2)
+    psnr = 10 * np.log10(255.0 ** 2 / max(mse, 1e-12))
+    assert psnr >= 35.0, psnr
+
+
+# ------------------------------------------------------------------ P13 interpolation
+def test_interpolation_keys_verbatim_and_convex_weights():
+    g, s = static_textured_video(9, 24, 24, flicker=False)
+    keys = [1, 6]
+    ks = np.empty((2, 24, 24, 3), np.uint8)
+    ks[0] = 40
+    ks[1] = 200
+    cfg = O.Cfg(patch_radius=2, iters_per_level=1, init=O.INIT_IDENTITY)
+    out, pairs, _ = O.interpolate(cfg, g, keys, ks)
+    assert pairs == 2 * 4 + 1 + 2
+    np.testing.assert_array_equal(out[1], ks[0].astype(np.float32))
+    np.testing.assert_array_equal(out[6], ks[1].astype(np.float32))
+    np.testing.assert_array_equal(out[0], ks[0].astype(np.float32))        # before the first key
+    np.testing.assert_array_equal(out[8], ks[1].astype(np.float32))        # after the last key
+    for m in range(2, 6):
+        wl, wr = (6 - m) / 5, (m - 1) / 5                                  # Eq. 9
+        np.testing.assert_allclose(out[m], wl * 40 + wr * 200, atol=1e-4)
+    # equal keys on a static guide reproduce the key (weights sum to ~1)
+    ks2 = np.stack([s[0], s[0]])
+    out2, _, _ = O.interpolate(cfg, g, keys, ks2)
+    for m in range(9):
+        np.testing.assert_allclose(out2[m], s[0].astype(np.float32), atol=1e-4)
+
+
+# ------------------------------------------------------------------ aux definitions (Eq. 3, Eq. 8)
+
+
+def test_guide_style_loss_uses_remap_at_iteration_start():
+    """Eq. 3: E = alpha*||G_j[F]-G_i||^2 + ||S_j[F]-S^_i||^2 with S^_i the remap of S_j under the F of
+    the beginning of the iteration (D17/D18).  Levels = 1, so the run with n-1 iterations
+    exposes that F."""
+    g, s = moving_texture(2, 24, 28, seed=12)
+    frames = np.concatenate([g, s]).astype(np.float32)
+    p, alpha = 2, 3.5
+    task = [dict(src_guide=0, tgt_guide=1, src_style=2, src_id=0, tgt_id=1)]
+    cfg = O.Cfg(patch_radius=p, levels=1, iters_per_level=3, loss=O.GUIDE_STYLE, alpha=alpha)
+    Fn, En, _, _ = O.nnf(cfg, frames, task, want_x=False)
+    cfg.iters_per_level = 2
+    Fp, _, _, _ = O.nnf(cfg, frames, task, want_x=False)
+    aux = np_remap_votes(frames[2], Fp[0], p)
+    ref = alpha * np_patch_dist_field(frames[0], frames[1], Fn[0], p) + np_patch_dist_field(frames[2], aux, Fn[0], p)
+    np.testing.assert_allclose(En[0], ref, rtol=2e-5, atol=1e-2)
+    # dropping the guide term or the style term must be detectable
+    assert np.abs(np_patch_dist_field(frames[2], aux, Fn[0], p) - En[0]).max() > 1.0
+
+
+def test_mean_align_loss_uses_window_mean():
+    """Eq. 8 with D27: E_j = alpha*||G_j[F]-G_i||^2 + ||S_j[F]-T-bar_i||^2, T-bar_i the ascending-j mean
+    over the window of the remaps plus S_i itself, refreshed at the start of every iteration."""
+    g, s = moving_texture(3, 24, 28, seed=13)
+    frames = np.concatenate([g, s]).astype(np.float32)
+    p, alpha = 2, 2.0
+    tasks = [dict(src_guide=j, tgt_guide=1, src_style=3 + j, tgt_style=4, group=0, src_id=j, tgt_id=1) for j in (0, 2)]
+    cfg = O.Cfg(patch_radius=p, levels=1, iters_per_level=3, loss=O.MEAN_ALIGN, alpha=alpha)
+    Fn, En, _, _ = O.nnf(cfg, frames, tasks, want_x=False)
+    cfg.iters_per_level = 2
+    Fp, _, _, _ = O.nnf(cfg, frames, tasks, want_x=False)
+    Y0 = np_remap_votes(frames[3], Fp[0], p)
+    Y2 = np_remap_votes(frames[5], Fp[1], p)
+    tbar = (Y0 + frames[4].astype(np.float64) + Y2) / 3.0
+    for t, j in enumerate((0, 2)):
+        ref = alpha * np_patch_dist_field(frames[j], frames[1], Fn[t], p) + \
+            np_patch_dist_field(frames[3 + j], tbar, Fn[t], p)
+        np.testing.assert_allclose(En[t], ref, rtol=2e-5, atol=1e-2)
+
+
+# ------------------------------------------------------------------ schedule composition
+def test_direct_blend_composes_eq2_from_nnf_results():
+    """Eq. 2 with D3/D4: out_i = (sum over j ascending in W_i of X_{j->i}) / |W_i|, X_{i->i} = S_i,
+    X_{j->i} = remap of S_j with NNF(G_j, G_i).  Recomposed here from per-pair oracle NNF runs."""
+    N, M = 5, 2
+    g, s = moving_texture(N, 32, 32, seed=14)
+    cfg = O.Cfg(patch_radius=2, iters_per_level=2, loss=O.GUIDE_STYLE)
+    out, _, _ = O.blend_direct(cfg, g, s, M, targets=[0, 3])
+    frames = np.concatenate([g, s]).astype(np.float32)
+    for q, i in enumerate((0, 3)):
+        lo, hi = max(0, i - M), min(N - 1, i + M)
+        acc = np.zeros((32, 32, 3), np.float32)
+        for j in range(lo, hi + 1):
+            if j == i:
+                acc = acc + frames[N + i]
+            else:
+                _, _, X, _ = O.nnf(cfg, frames, [dict(src_guide=j, tgt_guide=i, src_style=N + j, src_id=j,
+                                                      tgt_id=i, tag=O.TAG_DIRECT)])
+                acc = acc + X[0]
+        np.testing.assert_array_equal(out[q], acc / np.float32(hi - lo + 1))
+
+
+def test_targets_subset_equals_full_run():
+    N, M = 7, 2
+    g, s = moving_texture(N, 32, 32, seed=15)
+    cfg = O.Cfg(patch_radius=2, iters_per_level=1)
+    for fn, loss in ((O.blend_direct, O.MEAN_ALIGN), (O.blend_tree, O.GUIDE_STYLE)):
+        cfg.loss = loss
+        full, _, _ = fn(cfg, g, s, M)
+        sub, _, _ = fn(cfg, g, s, M, targets=[6, 2])
+        np.testing.assert_array_equal(sub[0], full[6])
+        np.testing.assert_array_equal(sub[1], full[2])
+
+
+@pytest.mark.parametrize("field", [0, 1, 2, 3, 4, 5])
+def test_ties_keep_the_incumbent(field):
+    """F(E'<E) <- F' is a strict comparison (D16): on a constant image every interior
+    candidate ties with the incumbent and nothing may move."""
+    h = w = 24
+    img = np.full((h, w, 3), 100.0, np.float32)
+    cfg = O.Cfg(patch_radius=1, loss=O.BASE, levels=1, rs_radius0=2)
+    rr, cc = np.mgrid[0:h, 0:w]
+    Fin = np.stack([np.clip(rr + 1, 0, h - 1), np.clip(cc - 1, 0, w - 1)], -1).astype(np.int32)
+    Fin[8:16, 8:16] = 12
+    _, Ein = O.field(cfg, img, img, Fin, np.zeros((h, w), np.float32), -1)
+    Fout, Eout = O.field(cfg, img, img, Fin, Ein, field)
+    inner = (slice(6, 18), slice(6, 18))
+    assert np.all(Ein[inner] == 0)
+    np.testing.assert_array_equal(Fout[inner], Fin[inner])
