@@ -1,0 +1,953 @@
+// engine.cu — host side of the B200 FastBlend path: C ABI (include/fb.h), workspace arena, the
+// Alg. 1 batch driver and the three schedules (direct window blend, tree window blend, keyframe
+// interpolation).  All arithmetic runs in kernels.cu; this file only plans and enqueues.
+//
+// Execution model: one context = one device + one stream.  Every call first plans in "dry" mode
+// (same code path, no launches) to size the workspace, then runs for real.  All NNF tasks of a batch
+// advance in lockstep (level, iteration, field), which is what MEAN_ALIGN's shared T-bar needs
+// (Eq. 7) and what fills the 148 SMs: one launch covers every pixel of every pair.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/fb.h"
+#include "kernels.h"
+
+using fbk::DMember;
+using fbk::DOut;
+using fbk::DTask;
+using fbk::Lvl;
+
+struct fb_ctx_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    char* ws = nullptr;
+    size_t ws_bytes = 0;
+    int64_t max_pairs = 0;
+    uint64_t launches = 0;
+    std::string err;
+    // kernel timing (fb_profile_*)
+    bool prof = false;
+    struct Pending { int cls; cudaEvent_t a, b; uint64_t work; };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::string> cls_names;
+    std::vector<fb_profile_entry> totals;
+    int cls(const char* name)
+    {
+        for (size_t i = 0; i < cls_names.size(); ++i)
+            if (cls_names[i] == name) return (int)i;
+        cls_names.push_back(name);
+        fb_profile_entry e{};
+        snprintf(e.name, sizeof e.name, "%s", name);
+        totals.push_back(e);
+        return (int)cls_names.size() - 1;
+    }
+    cudaEvent_t ev()
+    {
+        if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    void drain()
+    {
+        for (auto& p : pending) {
+            cudaEventSynchronize(p.b);
+            float ms = 0.0f;
+            cudaEventElapsedTime(&ms, p.a, p.b);
+            totals[p.cls].launches += 1;
+            totals[p.cls].ms += ms;
+            totals[p.cls].work += p.work;
+            pool.push_back(p.a);
+            pool.push_back(p.b);
+        }
+        pending.clear();
+    }
+    ~fb_ctx_s()
+    {
+        drain();
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
+namespace {
+
+constexpr size_t kAutoStateBudget = 64ull << 30;  // bytes of per-pair state in one auto-sized batch
+constexpr int kMaxBatchPairs = 65535;              // grid.y limit of the per-task launches
+
+struct Fail {
+    fb_status st;
+    std::string msg;
+};
+
+// ------------------------------------------------------------------------------------ arena
+struct Arena {
+    char* base = nullptr;  // nullptr in dry mode: pointers are offsets, never dereferenced
+    size_t off = 0, peak = 0;
+    template <class T>
+    T* take(size_t n)
+    {
+        off = (off + 255) & ~size_t(255);
+        T* p = reinterpret_cast<T*>(base + off);
+        off += n * sizeof(T);
+        peak = std::max(peak, off);
+        return p;
+    }
+};
+
+struct Exec {
+    fb_ctx ctx;
+    bool dry;
+    Arena ar;
+    void check(cudaError_t e, const char* what)
+    {
+        if (e != cudaSuccess) throw Fail{FB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+    }
+    template <class F>
+    void launch(const char* what, F&& f, uint64_t work = 0)
+    {
+        if (dry) return;
+        if (ctx->prof) {
+            fb_ctx_s::Pending p{ctx->cls(what), ctx->ev(), ctx->ev(), work};
+            cudaEventRecord(p.a, ctx->stream);
+            check(f(), what);
+            cudaEventRecord(p.b, ctx->stream);
+            ctx->pending.push_back(p);
+            if (ctx->pending.size() > 4096) ctx->drain();
+        } else {
+            check(f(), what);
+        }
+        ++ctx->launches;
+    }
+    template <class T>
+    T* upload(const std::vector<T>& v)
+    {
+        T* d = ar.take<T>(std::max<size_t>(v.size(), 1));
+        if (!dry && !v.empty())
+            check(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream), "upload");
+        return d;
+    }
+    void d2d(void* dst, const void* src, size_t bytes)
+    {
+        if (!dry && bytes) check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream), "d2d");
+    }
+};
+
+// ------------------------------------------------------------------------------------ geometry
+struct Geo {
+    int H = 0, W = 0, Lv = 0, p = 0;
+    Lvl L[24];
+    long long pyr_texels = 0;  // texels of one pyramid
+    long long npx0() const { return (long long)H * W; }
+};
+
+int level_count(int H, int W, int p, int requested)  // D6, D32
+{
+    const int mn = std::min(H, W);
+    if (mn < 2 * p + 1) return -1;
+    if (requested > 0) {
+        if (requested > 20) return -1;
+        if (std::min(H >> (requested - 1), W >> (requested - 1)) < 2 * p + 1) return -1;
+        return requested;
+    }
+    int lv = 1;
+    for (int k = 1; k < 24; ++k)
+        if ((mn >> k) >= 32) lv = k + 1;
+    while (lv > 1 && (mn >> (lv - 1)) < 2 * p + 1) --lv;
+    return lv;
+}
+
+Geo make_geo(const fb_match_cfg& cfg, int H, int W)
+{
+    Geo g;
+    g.H = H; g.W = W; g.p = cfg.patch_radius;
+    g.Lv = level_count(H, W, cfg.patch_radius, cfg.levels);
+    if (g.Lv < 1) throw Fail{FB_ERR_SHAPE, "min(H,W) or the coarsest level is smaller than the patch (2p+1)"};
+    long long off = 0;
+    for (int k = 0; k < g.Lv; ++k) {
+        g.L[k] = Lvl{H >> k, W >> k, off};
+        off += (long long)(H >> k) * (W >> k);
+    }
+    g.pyr_texels = off;
+    return g;
+}
+
+int rs_r0(const fb_match_cfg& c, const Lvl& L) { return c.rs_radius0 > 0 ? c.rs_radius0 : std::max(L.h, L.w); }
+int rs_count(const fb_match_cfg& c, const Lvl& L)  // D13, D33
+{
+    if (c.rs_steps > 0) return c.rs_steps;
+    int n = 0, r0 = rs_r0(c, L);
+    while ((r0 >> n) >= 1) ++n;
+    return n;
+}
+uint64_t evals_per_pair(const fb_match_cfg& c, const Geo& g)
+{
+    uint64_t n = 0;
+    for (int k = 0; k < g.Lv; ++k)
+        n += (uint64_t)g.L[k].h * g.L[k].w * (uint64_t)c.iters_per_level * (uint64_t)(5 + rs_count(c, g.L[k]));
+    return n;
+}
+
+void validate_cfg(const fb_match_cfg* cfg)
+{
+    if (!cfg) throw Fail{FB_ERR_INVALID_ARG, "cfg is NULL"};
+    if (cfg->patch_radius < 1) throw Fail{FB_ERR_INVALID_ARG, "patch_radius < 1"};
+    if (cfg->patch_radius > 4) throw Fail{FB_ERR_UNSUPPORTED, "patch_radius > 4 is not compiled"};
+    if (cfg->iters_per_level < 0 || cfg->levels < 0 || cfg->rs_radius0 < 0 || cfg->rs_steps < 0)
+        throw Fail{FB_ERR_INVALID_ARG, "negative iteration / level / random-search parameter"};
+    if (!(cfg->alpha >= 0.0f)) throw Fail{FB_ERR_INVALID_ARG, "alpha < 0"};
+    if (cfg->loss < 0 || cfg->loss > 2) throw Fail{FB_ERR_INVALID_ARG, "unknown loss"};
+    if (cfg->init < 0 || cfg->init > 1) throw Fail{FB_ERR_INVALID_ARG, "unknown init"};
+}
+
+// ------------------------------------------------------------------------------------ pyramids
+struct Pyr {
+    float4* base = nullptr;
+    long long stride = 0;  // texels per frame
+    const float4* frame(long long i) const { return base + i * stride; }
+};
+
+Pyr pyramid_u8(Exec& ex, const Geo& g, const uint8_t* frames, int B)
+{
+    Pyr P;
+    P.stride = g.pyr_texels;
+    P.base = ex.ar.take<float4>((size_t)B * P.stride);
+    if (B == 0) return P;
+    ex.launch("pyr0", [&] { return fbk::launch_u8_to_pyr0(frames, P.base, B, g.H, g.W, P.stride, ex.ctx->stream); });
+    for (int k = 1; k < g.Lv; ++k)
+        ex.launch("box", [&] { return fbk::launch_box(P.base, B, P.stride, g.L[k - 1], g.L[k], ex.ctx->stream); });
+    return P;
+}
+
+void pyramid_levels_inplace(Exec& ex, const Geo& g, float4* base, int B, long long stride)
+{
+    for (int k = 1; k < g.Lv; ++k)
+        ex.launch("box", [&] { return fbk::launch_box(base, B, stride, g.L[k - 1], g.L[k], ex.ctx->stream); });
+}
+
+// ------------------------------------------------------------------------------------ NNF batch (Alg. 1)
+struct TaskSpec {
+    const float4* sg;  // source guide pyramid
+    const float4* tg;  // target guide pyramid
+    const float4* ss;  // source style pyramid (the image being remapped, D22)
+    int group;         // MEAN_ALIGN window index (into groups), else -1
+    uint32_t src_id, tgt_id, tag;
+};
+struct GroupSpec {
+    const float4* tstyle;  // target style pyramid (the self term of T-bar)
+    uint32_t tgt_id;
+};
+struct BatchOut {
+    int2* F = nullptr;  // final NNF of task t at F + t*fstride (level 0)
+    float* E = nullptr;
+    long long fstride = 0;
+};
+
+BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const std::vector<TaskSpec>& tasks,
+                 const std::vector<GroupSpec>& groups, fb_stats* st)
+{
+    const int T = (int)tasks.size();
+    const long long n0 = g.npx0();
+    const cudaStream_t s = ex.ctx->stream;
+    BatchOut out;
+    out.fstride = n0;
+    int2* F[2] = {ex.ar.take<int2>((size_t)T * n0), ex.ar.take<int2>((size_t)T * n0)};
+    out.E = ex.ar.take<float>((size_t)T * n0);
+    float4* aux = nullptr;
+    if (cfg.loss == FB_LOSS_GUIDE_STYLE) aux = ex.ar.take<float4>((size_t)T * n0);
+    if (cfg.loss == FB_LOSS_MEAN_ALIGN) aux = ex.ar.take<float4>((size_t)groups.size() * n0);
+    std::vector<DTask> dt(T);
+    for (int t = 0; t < T; ++t) {
+        const TaskSpec& k = tasks[t];
+        dt[t].sg = k.sg; dt[t].tg = k.tg; dt[t].ss = k.ss;
+        dt[t].aux = cfg.loss == FB_LOSS_GUIDE_STYLE ? aux + t * n0
+                  : cfg.loss == FB_LOSS_MEAN_ALIGN  ? aux + (long long)k.group * n0 : nullptr;
+        dt[t].c2 = k.src_id;
+        dt[t].c3 = (k.tag << 28) | k.tgt_id;
+        dt[t].pad0 = dt[t].pad1 = 0;
+    }
+    const DTask* d_tasks = ex.upload(dt);
+    // T-bar member lists for every level (MEAN_ALIGN): ascending source id with the self term inserted.
+    std::vector<const DOut*> d_outs(g.Lv, nullptr);
+    std::vector<const DMember*> d_mem(g.Lv, nullptr);
+    if (cfg.loss == FB_LOSS_MEAN_ALIGN) {
+        std::vector<std::vector<int>> members(groups.size());
+        for (int t = 0; t < T; ++t) members[tasks[t].group].push_back(t);
+        for (auto& m : members)
+            std::sort(m.begin(), m.end(), [&](int a, int b) { return tasks[a].src_id < tasks[b].src_id; });
+        for (int k = 0; k < g.Lv; ++k) {
+            std::vector<DOut> outs;
+            std::vector<DMember> mem;
+            for (size_t gi = 0; gi < groups.size(); ++gi) {
+                DOut o;
+                o.m0 = (int)mem.size();
+                bool self_done = false;
+                for (int t : members[gi]) {
+                    if (!self_done && tasks[t].src_id > groups[gi].tgt_id) {
+                        mem.push_back(DMember{groups[gi].tstyle + g.L[k].off, -1, 1.0f});
+                        self_done = true;
+                    }
+                    mem.push_back(DMember{tasks[t].ss + g.L[k].off, t, 1.0f});
+                }
+                if (!self_done) mem.push_back(DMember{groups[gi].tstyle + g.L[k].off, -1, 1.0f});
+                o.nm = (int)mem.size() - o.m0;
+                o.div = (float)o.nm;
+                o.fmt = 0;
+                o.out = aux + (long long)gi * n0;
+                outs.push_back(o);
+            }
+            d_outs[k] = ex.upload(outs);
+            d_mem[k] = ex.upload(mem);
+        }
+    }
+    const fbk::Rng rng{(uint32_t)(cfg.seed & 0xFFFFFFFFu), (uint32_t)(cfg.seed >> 32)};
+    int cur = 0;
+    for (int k = g.Lv - 1; k >= 0; --k) {
+        const Lvl L = g.L[k];
+        if (k == g.Lv - 1) {
+            ex.launch("init", [&] { return fbk::launch_init(d_tasks, T, F[cur], n0, L, cfg.init == FB_INIT_IDENTITY,
+                                                            rng, (uint32_t)k, s); });
+        } else {
+            ex.launch("upsample", [&] { return fbk::launch_upsample(F[cur], F[cur ^ 1], T, n0, g.L[k + 1], L, s); });
+            cur ^= 1;
+        }
+        const int rk = rs_count(cfg, L), r0 = rs_r0(cfg, L);
+        for (int it = 0; it < cfg.iters_per_level; ++it) {
+            if (cfg.loss == FB_LOSS_GUIDE_STYLE) {  // S^ refresh (D17/D18)
+                ex.launch("aux", [&] { return fbk::launch_aux_remap(d_tasks, T, F[cur], n0, L, g.p, s); },
+                          (uint64_t)T * L.h * L.w);
+                if (st) st->remap_pixels += (uint64_t)T * L.h * L.w;
+            } else if (cfg.loss == FB_LOSS_MEAN_ALIGN) {  // T-bar refresh (Eq. 7, D27)
+                ex.launch("tbar", [&] { return fbk::launch_combine(d_outs[k], (int)groups.size(), d_mem[k], F[cur], n0,
+                                                                   L.h, L.w, g.p, s); },
+                          (uint64_t)groups.size() * L.h * L.w);
+                if (st) st->remap_pixels += (uint64_t)T * L.h * L.w;
+            }
+            fbk::FieldArgs a{};
+            a.tasks = d_tasks; a.E = out.E; a.fstride = n0; a.L = L; a.alpha = cfg.alpha; a.rng = rng;
+            a.level = (uint32_t)k; a.iter = (uint32_t)it; a.rs_r0 = r0; a.rs_k = rk;
+            static const char* kFieldNames[4] = {"field0", "field1", "field2", "field3"};
+            for (int ph = 0; ph < 4; ++ph) {
+                a.Fin = F[cur]; a.Fout = F[cur ^ 1];
+                const uint64_t per_px = ph == 0 ? 2 : ph == 3 ? 1 + (uint64_t)rk : 1;
+                ex.launch(kFieldNames[ph], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, ph, s); },
+                          per_px * (uint64_t)T * L.h * L.w);
+                cur ^= 1;
+            }
+        }
+    }
+    out.F = F[cur];
+    if (st) {
+        st->nnf_pairs += (uint64_t)T;
+        st->candidate_evals += (uint64_t)T * evals_per_pair(cfg, g);
+    }
+    return out;
+}
+
+// Final combine at level 0 into API-layout float [.., H, W, 3] rows.
+struct CombineList {
+    std::vector<DOut> outs;
+    std::vector<DMember> mem;
+    void begin() { outs.push_back(DOut{(int)mem.size(), 0, 1.0f, 1, nullptr}); }
+    void add_img(const float4* img, float w) { mem.push_back(DMember{img, -1, w}); ++outs.back().nm; }
+    void add_remap(const float4* src_level_img, int task, float w) { mem.push_back(DMember{src_level_img, task, w}); ++outs.back().nm; }
+    void end(void* out, int fmt, float div) { outs.back().out = out; outs.back().fmt = fmt; outs.back().div = div; }
+};
+
+void run_combine(Exec& ex, const Geo& g, int k, const CombineList& cl, const int2* F, long long fstride)
+{
+    if (cl.outs.empty()) return;
+    const DOut* o = ex.upload(cl.outs);
+    const DMember* m = ex.upload(cl.mem);
+    ex.launch("combine", [&] { return fbk::launch_combine(o, (int)cl.outs.size(), m, F, fstride, g.L[k].h, g.L[k].w,
+                                                          g.p, ex.ctx->stream); },
+              (uint64_t)cl.outs.size() * g.L[k].h * g.L[k].w);
+}
+
+size_t per_pair_bytes(const Geo& g, int loss)
+{
+    // F ping-pong + E + (GS aux) per pair, plus descriptor slack
+    return (size_t)g.npx0() * (2 * sizeof(int2) + sizeof(float) + (loss == FB_LOSS_GUIDE_STYLE ? sizeof(float4) : 0)) + 4096;
+}
+
+int batch_pairs(fb_ctx ctx, const Geo& g, int loss)
+{
+    long long m = ctx->max_pairs > 0 ? ctx->max_pairs : (long long)(kAutoStateBudget / per_pair_bytes(g, loss));
+    m = std::max<long long>(1, std::min<long long>(m, kMaxBatchPairs));
+    return (int)m;
+}
+
+// Split consecutive units (each with `cost` pairs, never split) into batches of <= cap pairs.
+std::vector<std::pair<int, int>> make_batches(const std::vector<int>& cost, int cap)
+{
+    std::vector<std::pair<int, int>> b;
+    int start = 0, acc = 0;
+    for (int i = 0; i < (int)cost.size(); ++i) {
+        if (acc > 0 && acc + cost[i] > cap) { b.push_back({start, i}); start = i; acc = 0; }
+        acc += cost[i];
+    }
+    if (start < (int)cost.size()) b.push_back({start, (int)cost.size()});
+    return b;
+}
+
+// ------------------------------------------------------------------------------------ direct schedule
+// Eq. 2 + Eq. 3 (balanced) or Eq. 7/8 (accurate), O(N*M) NNFs.
+void blend_direct(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int N_total, int f0, int N, int M,
+                  const uint8_t* guide, const uint8_t* style, int t0, int t1, float* out, fb_stats* st)
+{
+    const Pyr G = pyramid_u8(ex, g, guide, N);
+    const Pyr S = pyramid_u8(ex, g, style, N);
+    const long long n0 = g.npx0();
+    std::vector<int> cost;
+    for (int i = t0; i < t1; ++i) cost.push_back(std::min(N_total - 1, i + M) - std::max(0, i - M));
+    const auto batches = make_batches(cost, batch_pairs(ex.ctx, g, cfg.loss));
+    const size_t mark = ex.ar.off;
+    for (auto [b0, b1] : batches) {
+        ex.ar.off = mark;
+        std::vector<TaskSpec> tasks;
+        std::vector<GroupSpec> groups;
+        std::vector<int> first(b1 - b0);
+        for (int q = b0; q < b1; ++q) {
+            const int i = t0 + q, lo = std::max(0, i - M), hi = std::min(N_total - 1, i + M);
+            first[q - b0] = (int)tasks.size();
+            if (cfg.loss == FB_LOSS_MEAN_ALIGN) groups.push_back(GroupSpec{S.frame(i - f0), (uint32_t)i});
+            for (int j = lo; j <= hi; ++j) {
+                if (j == i) continue;
+                tasks.push_back(TaskSpec{G.frame(j - f0), G.frame(i - f0), S.frame(j - f0),
+                                         cfg.loss == FB_LOSS_MEAN_ALIGN ? q - b0 : -1, (uint32_t)j, (uint32_t)i, 0u});
+            }
+        }
+        BatchOut bo;
+        if (!tasks.empty()) bo = run_nnf(ex, cfg, g, tasks, groups, st);
+        CombineList cl;  // out_i = (sum_{j asc} X_{j->i}) / |W_i|, X_{i->i} = S_i (D3, D4)
+        for (int q = b0; q < b1; ++q) {
+            const int i = t0 + q, lo = std::max(0, i - M), hi = std::min(N_total - 1, i + M);
+            int t = first[q - b0];
+            cl.begin();
+            for (int j = lo; j <= hi; ++j) {
+                if (j == i) cl.add_img(S.frame(i - f0), 1.0f);
+                else cl.add_remap(S.frame(j - f0), t++, 1.0f);
+            }
+            cl.end(out + 3LL * n0 * q, 1, (float)(hi - lo + 1));
+            if (st) st->remap_pixels += (uint64_t)(hi - lo) * n0;
+        }
+        run_combine(ex, g, 0, cl, bo.F, bo.fstride);
+    }
+}
+
+// ------------------------------------------------------------------------------------ tree schedule
+// Alg. 3 (remapping table), Alg. 4 (blending table), Alg. 5 (query) on the forward and the reversed
+// frame order (D26), merged by Eq. 6.  Tables hold means (D25); levels capped at floor(log2(M+1))
+// (D24); only the cells the requested targets' queries visit are built (the "task manager").
+int floor_log2(int x) { int l = 0; while ((2 << l) <= x) ++l; return l; }
+
+std::vector<std::pair<int, int>> query_nodes(int l, int r)  // Alg. 5 with i <- i - 2^L (D23)
+{
+    std::vector<std::pair<int, int>> v;
+    int i = r;
+    while (i >= l) {
+        int L = 0;
+        while ((i & (1 << L)) && i - (1 << (L + 1)) + 1 >= l) ++L;
+        v.push_back({i, L});
+        i -= 1 << L;
+    }
+    return v;
+}
+
+void blend_tree(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N_total, int f0, int N, int M,
+                const uint8_t* guide, const uint8_t* style, int t0, int t1, float* out, fb_stats* st)
+{
+    fb_match_cfg cfg = cfg0;
+    cfg.loss = FB_LOSS_GUIDE_STYLE;  // D22: the loss is taken on the image being remapped
+    const Pyr G = pyramid_u8(ex, g, guide, N);
+    const Pyr S = pyramid_u8(ex, g, style, N);
+    const long long n0 = g.npx0();
+    const int lcap = floor_log2(M + 1);
+    const int cap = batch_pairs(ex.ctx, g, cfg.loss);
+    const int nt = t1 - t0;
+    float4* A[2] = {ex.ar.take<float4>((size_t)nt * n0), ex.ar.take<float4>((size_t)nt * n0)};
+    for (int o = 0; o < 2; ++o) {
+        const size_t omark = ex.ar.off;  // this orientation's tables die once its A is written
+        auto orig = [&](int v) { return o == 0 ? v : N_total - 1 - v; };
+        const uint32_t tag_build = o == 0 ? 1u : 3u, tag_query = o == 0 ? 2u : 4u;
+        // cells needed by the queries: (j, L) for 1 <= L <= level of a visited node
+        std::map<std::pair<int, int>, int> cell_id;  // (j, L) -> index
+        std::vector<std::pair<int, int>> cells;
+        std::vector<int> top(N_total, 0);
+        for (int i = t0; i < t1; ++i) {
+            const int v = o == 0 ? i : N_total - 1 - i;
+            for (auto [node, L] : query_nodes(std::max(0, v - M), v)) top[node] = std::max(top[node], L);
+        }
+        for (int j = 0; j < N_total; ++j)
+            for (int L = 1; L <= top[j]; ++L) { cell_id[{j, L}] = (int)cells.size(); cells.push_back({j, L}); }
+        const int nc = (int)cells.size();
+        float4* RT = ex.ar.take<float4>((size_t)nc * n0);           // RT sums, level 0
+        float4* BT = ex.ar.take<float4>((size_t)nc * g.pyr_texels);  // BT cell pyramids
+        auto bt_pyr = [&](int v, int L) -> const float4* {
+            return L == 0 ? S.frame(orig(v) - f0) : BT + (long long)cell_id.at({v, L}) * g.pyr_texels;
+        };
+        // Alg. 3: RT(j,L) receives X_{i->j} for i in [j-2^L+1, j-2^(L-1)], summed ascending.
+        std::vector<int> cost(nc);
+        for (int c = 0; c < nc; ++c) cost[c] = 1 << (cells[c].second - 1);
+        const size_t mark = ex.ar.off;
+        for (auto [c0, c1] : make_batches(cost, cap)) {
+            ex.ar.off = mark;
+            std::vector<TaskSpec> tasks;
+            for (int c = c0; c < c1; ++c) {
+                const auto [j, L] = cells[c];
+                for (int v = j - (1 << L) + 1; v <= j - (1 << (L - 1)); ++v)
+                    tasks.push_back(TaskSpec{G.frame(orig(v) - f0), G.frame(orig(j) - f0), S.frame(orig(v) - f0), -1,
+                                             (uint32_t)orig(v), (uint32_t)orig(j), tag_build});
+            }
+            BatchOut bo = run_nnf(ex, cfg, g, tasks, {}, st);
+            CombineList cl;
+            int t = 0;
+            for (int c = c0; c < c1; ++c) {
+                const auto [j, L] = cells[c];
+                cl.begin();
+                for (int v = j - (1 << L) + 1; v <= j - (1 << (L - 1)); ++v) cl.add_remap(S.frame(orig(v) - f0), t++, 1.0f);
+                cl.end(RT + (long long)c * n0, 0, 1.0f);
+            }
+            if (st) st->remap_pixels += (uint64_t)tasks.size() * n0;
+            run_combine(ex, g, 0, cl, bo.F, bo.fstride);
+        }
+        ex.ar.off = mark;
+        // Alg. 4: BT(j,L) = (BT(j,L-1) + RT(j,L) * 2^-(L-1)) * 0.5, level by level
+        for (int L = 1; L <= lcap; ++L) {
+            CombineList cl;
+            for (int c = 0; c < nc; ++c) {
+                if (cells[c].second != L) continue;
+                const int j = cells[c].first;
+                cl.begin();
+                cl.add_img(bt_pyr(j, L - 1), 1.0f);
+                cl.add_img(RT + (long long)c * n0, 1.0f / (float)(1 << (L - 1)));
+                cl.end(BT + (long long)c * g.pyr_texels, 0, 2.0f);
+            }
+            run_combine(ex, g, 0, cl, nullptr, 0);
+        }
+        if (nc) pyramid_levels_inplace(ex, g, BT, nc, g.pyr_texels);
+        // Alg. 5 queries: A = sum over visited nodes of 2^L * (BT(i,L) -> S_r); the self node is BT itself.
+        std::vector<int> qcost;
+        std::vector<std::vector<std::pair<int, int>>> walks;
+        for (int i = t0; i < t1; ++i) {
+            const int v = o == 0 ? i : N_total - 1 - i;
+            walks.push_back(query_nodes(std::max(0, v - M), v));
+            qcost.push_back((int)walks.back().size() - 1);
+        }
+        const size_t mark2 = ex.ar.off;
+        for (auto [q0, q1] : make_batches(qcost, cap)) {
+            ex.ar.off = mark2;
+            std::vector<TaskSpec> tasks;
+            for (int q = q0; q < q1; ++q) {
+                const int i = t0 + q, v = o == 0 ? i : N_total - 1 - i;
+                for (auto [node, L] : walks[q]) {
+                    if (node == v) continue;
+                    tasks.push_back(TaskSpec{G.frame(orig(node) - f0), G.frame(i - f0), bt_pyr(node, L), -1,
+                                             (uint32_t)orig(node), (uint32_t)i, tag_query});
+                }
+            }
+            BatchOut bo;
+            if (!tasks.empty()) bo = run_nnf(ex, cfg, g, tasks, {}, st);
+            CombineList cl;
+            int t = 0;
+            for (int q = q0; q < q1; ++q) {
+                const int v = o == 0 ? t0 + q : N_total - 1 - (t0 + q);
+                cl.begin();
+                for (auto [node, L] : walks[q]) {
+                    const float wgt = (float)(1 << L);
+                    if (node == v) cl.add_img(bt_pyr(node, L), wgt);
+                    else cl.add_remap(bt_pyr(node, L), t++, wgt);
+                }
+                cl.end(A[o] + (long long)q * n0, 0, 1.0f);
+            }
+            if (st) st->remap_pixels += (uint64_t)tasks.size() * n0;
+            run_combine(ex, g, 0, cl, bo.F, bo.fstride);
+        }
+        ex.ar.off = omark;
+    }
+    // Eq. 6: out_i = ((A_f + A_r) - S_i) / |W_i|
+    CombineList cl;
+    for (int q = 0; q < nt; ++q) {
+        const int i = t0 + q, lo = std::max(0, i - M), hi = std::min(N_total - 1, i + M);
+        cl.begin();
+        cl.add_img(A[0] + (long long)q * n0, 1.0f);
+        cl.add_img(A[1] + (long long)q * n0, 1.0f);
+        cl.add_img(S.frame(i - f0), -1.0f);
+        cl.end(out + 3LL * n0 * q, 1, (float)(hi - lo + 1));
+    }
+    run_combine(ex, g, 0, cl, nullptr, 0);
+}
+
+// ------------------------------------------------------------------------------------ interpolation
+// Eq. 9 (D28).
+void interpolate(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N, const uint8_t* guide, int K,
+                 const int32_t* keys, const uint8_t* key_style, float* out, fb_stats* st)
+{
+    fb_match_cfg cfg = cfg0;
+    cfg.loss = FB_LOSS_GUIDE_STYLE;
+    const Pyr G = pyramid_u8(ex, g, guide, N);
+    const Pyr KS = pyramid_u8(ex, g, key_style, K);
+    const long long n0 = g.npx0();
+    struct Tgt { int m, left, right, key; };  // key indices (or -1)
+    std::vector<Tgt> tg;
+    std::vector<int> cost;
+    for (int m = 0; m < N; ++m) {
+        Tgt t{m, -1, -1, -1};
+        for (int k = 0; k < K; ++k) {
+            if (keys[k] == m) t.key = k;
+            if (keys[k] < m) t.left = k;
+            if (keys[k] > m && t.right < 0) t.right = k;
+        }
+        tg.push_back(t);
+        cost.push_back(t.key >= 0 ? 0 : (t.left >= 0) + (t.right >= 0));
+    }
+    const size_t mark = ex.ar.off;
+    for (auto [b0, b1] : make_batches(cost, batch_pairs(ex.ctx, g, cfg.loss))) {
+        ex.ar.off = mark;
+        std::vector<TaskSpec> tasks;
+        std::vector<int> tl(b1 - b0, -1), tr(b1 - b0, -1);
+        for (int q = b0; q < b1; ++q) {
+            const Tgt& t = tg[q];
+            if (t.key >= 0) continue;
+            if (t.left >= 0) {
+                tl[q - b0] = (int)tasks.size();
+                tasks.push_back(TaskSpec{G.frame(keys[t.left]), G.frame(t.m), KS.frame(t.left), -1, (uint32_t)keys[t.left],
+                                         (uint32_t)t.m, 5u});
+            }
+            if (t.right >= 0) {
+                tr[q - b0] = (int)tasks.size();
+                tasks.push_back(TaskSpec{G.frame(keys[t.right]), G.frame(t.m), KS.frame(t.right), -1,
+                                         (uint32_t)keys[t.right], (uint32_t)t.m, 5u});
+            }
+        }
+        BatchOut bo;
+        if (!tasks.empty()) bo = run_nnf(ex, cfg, g, tasks, {}, st);
+        CombineList cl;
+        for (int q = b0; q < b1; ++q) {
+            const Tgt& t = tg[q];
+            cl.begin();
+            if (t.key >= 0) {
+                cl.add_img(KS.frame(t.key), 1.0f);  // keyframes are not modified
+            } else if (t.left < 0 || t.right < 0) {
+                const int k = t.left >= 0 ? t.left : t.right;
+                cl.add_remap(KS.frame(k), t.left >= 0 ? tl[q - b0] : tr[q - b0], 1.0f);
+            } else {
+                const int l = keys[t.left], r = keys[t.right], m = t.m;
+                const float wl = (float)(r - m) / (float)(r - l), wr = (float)(m - l) / (float)(r - l);
+                cl.add_remap(KS.frame(t.right), tr[q - b0], wr);  // A = X_r * w_r, then fma(X_l, w_l, A)
+                cl.add_remap(KS.frame(t.left), tl[q - b0], wl);
+            }
+            cl.end(out + 3LL * n0 * t.m, 1, 1.0f);
+        }
+        if (st) st->remap_pixels += (uint64_t)tasks.size() * n0;
+        run_combine(ex, g, 0, cl, bo.F, bo.fstride);
+    }
+}
+
+// ------------------------------------------------------------------------------------ NNF API
+void nnf_api(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int B, const uint8_t* sg, const uint8_t* tg,
+             const uint8_t* ss, const uint8_t* ts, const int32_t* group, const fb_pair_key* keys, int32_t* nnf_out,
+             float* err_out, float* rem_out, fb_stats* st)
+{
+    const Pyr SG = pyramid_u8(ex, g, sg, B), TG = pyramid_u8(ex, g, tg, B);
+    Pyr SS, TS;
+    if (cfg.loss != FB_LOSS_BASE) SS = pyramid_u8(ex, g, ss, B);
+    if (cfg.loss == FB_LOSS_MEAN_ALIGN) TS = pyramid_u8(ex, g, ts, B);
+    std::vector<TaskSpec> tasks;
+    std::vector<GroupSpec> groups;
+    std::map<int32_t, int> gidx;
+    for (int b = 0; b < B; ++b) {
+        int gi = -1;
+        if (cfg.loss == FB_LOSS_MEAN_ALIGN) {
+            auto it = gidx.find(group[b]);
+            if (it == gidx.end()) {
+                gi = (int)groups.size();
+                gidx[group[b]] = gi;
+                groups.push_back(GroupSpec{TS.frame(b), (uint32_t)keys[b].tgt_id});
+            } else {
+                gi = it->second;
+                if (groups[gi].tgt_id != (uint32_t)keys[b].tgt_id)
+                    throw Fail{FB_ERR_INVALID_ARG, "pairs of one MEAN_ALIGN group must share tgt_id"};
+            }
+        }
+        tasks.push_back(TaskSpec{SG.frame(b), TG.frame(b), cfg.loss != FB_LOSS_BASE ? SS.frame(b) : nullptr, gi,
+                                 (uint32_t)keys[b].src_id, (uint32_t)keys[b].tgt_id, (uint32_t)keys[b].task_tag});
+    }
+    BatchOut bo = run_nnf(ex, cfg, g, tasks, groups, st);
+    const long long n0 = g.npx0();
+    ex.d2d(nnf_out, bo.F, sizeof(int2) * (size_t)B * n0);
+    if (err_out) ex.d2d(err_out, bo.E, sizeof(float) * (size_t)B * n0);
+    if (rem_out) {
+        if (cfg.loss == FB_LOSS_BASE) throw Fail{FB_ERR_INVALID_ARG, "remapped_out needs src_style (loss != BASE)"};
+        CombineList cl;
+        for (int b = 0; b < B; ++b) {
+            cl.begin();
+            cl.add_remap(SS.frame(b), b, 1.0f);
+            cl.end(rem_out + 3LL * n0 * b, 1, 1.0f);
+        }
+        if (st) st->remap_pixels += (uint64_t)B * n0;
+        run_combine(ex, g, 0, cl, bo.F, bo.fstride);
+    }
+}
+
+// Runs `body` twice: dry (to size the workspace) then for real.
+template <class Body>
+fb_status guarded(fb_ctx ctx, fb_stats* stats, Body&& body, size_t* need_only = nullptr)
+{
+    if (!ctx) return FB_ERR_INVALID_ARG;
+    try {
+        Exec dry{ctx, true, Arena{}};
+        fb_stats tmp{};
+        body(dry, &tmp);
+        if (need_only) { *need_only = dry.ar.peak; return FB_OK; }
+        if (dry.ar.peak > 0 && (!ctx->ws || ctx->ws_bytes < dry.ar.peak)) {
+            char buf[160];
+            snprintf(buf, sizeof buf, "workspace too small: need %zu bytes, have %zu", dry.ar.peak, ctx->ws_bytes);
+            throw Fail{FB_ERR_WORKSPACE, buf};
+        }
+        cudaError_t e = cudaSetDevice(ctx->device);
+        if (e != cudaSuccess) throw Fail{FB_ERR_CUDA, cudaGetErrorString(e)};
+        e = cudaGetLastError();  // surface a pending fault from earlier work
+        if (e != cudaSuccess) throw Fail{FB_ERR_CUDA, std::string("pending: ") + cudaGetErrorString(e)};
+        Exec run{ctx, false, Arena{ctx->ws}};
+        fb_stats st{};
+        body(run, &st);
+        if (stats) *stats = st;
+        ctx->err.clear();
+        return FB_OK;
+    } catch (const Fail& f) {
+        ctx->err = f.msg;
+        return f.st;
+    } catch (const std::exception& e) {
+        ctx->err = e.what();
+        return FB_ERR_INVALID_ARG;
+    }
+}
+
+void check_frames(int N, int H, int W)
+{
+    if (N < 1 || H < 1 || W < 1) throw Fail{FB_ERR_INVALID_ARG, "N, H, W must be >= 1"};
+}
+
+}  // namespace
+
+// ==================================================================================== C ABI
+extern "C" {
+
+fb_status fb_ctx_create(int device, void* cuda_stream, fb_ctx* out)
+{
+    if (!out) return FB_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (cudaSetDevice(device) != cudaSuccess) return FB_ERR_CUDA;
+    fb_ctx c = new fb_ctx_s;
+    c->device = device;
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+    *out = c;
+    return FB_OK;
+}
+
+void fb_ctx_destroy(fb_ctx ctx) { delete ctx; }
+
+const char* fb_last_error(fb_ctx ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+fb_status fb_set_workspace(fb_ctx ctx, void* dev_ptr, size_t bytes)
+{
+    if (!ctx || (!dev_ptr && bytes)) return FB_ERR_INVALID_ARG;
+    ctx->ws = static_cast<char*>(dev_ptr);
+    ctx->ws_bytes = bytes;
+    return FB_OK;
+}
+
+fb_status fb_set_max_batch_pairs(fb_ctx ctx, int64_t max_pairs)
+{
+    if (!ctx || max_pairs < 0) return FB_ERR_INVALID_ARG;
+    ctx->max_pairs = max_pairs;
+    return FB_OK;
+}
+
+uint64_t fb_launch_count(fb_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+fb_status fb_profile_enable(fb_ctx ctx, int on)
+{
+    if (!ctx) return FB_ERR_INVALID_ARG;
+    ctx->prof = on != 0;
+    return FB_OK;
+}
+
+int fb_profile_read(fb_ctx ctx, fb_profile_entry* out, int cap)
+{
+    if (!ctx) return 0;
+    ctx->drain();
+    const int n = (int)ctx->totals.size();
+    for (int i = 0; i < n && i < cap && out; ++i) out[i] = ctx->totals[i];
+    return n;
+}
+
+void fb_profile_reset(fb_ctx ctx)
+{
+    if (!ctx) return;
+    ctx->drain();
+    for (auto& e : ctx->totals) { e.launches = 0; e.ms = 0; e.work = 0; }
+}
+
+size_t fb_pyramid_elems(int B, int H, int W, int levels)
+{
+    if (B < 0 || H < 1 || W < 1 || levels < 1) return 0;
+    size_t n = 0;
+    for (int k = 0; k < levels; ++k) n += (size_t)(H >> k) * (size_t)(W >> k);
+    return 4 * n * (size_t)B;
+}
+
+fb_status fb_build_pyramid(fb_ctx ctx, const uint8_t* frames, int B, int H, int W, int levels, float* out)
+{
+    return guarded(ctx, nullptr, [&](Exec& ex, fb_stats*) {
+        if (!frames || !out || B < 1 || H < 1 || W < 1 || levels < 1 || levels > 20)
+            throw Fail{FB_ERR_INVALID_ARG, "bad pyramid arguments"};
+        if (std::min(H >> (levels - 1), W >> (levels - 1)) < 1) throw Fail{FB_ERR_SHAPE, "too many levels"};
+        Geo g;
+        g.H = H; g.W = W; g.Lv = levels;
+        long long off = 0;
+        for (int k = 0; k < levels; ++k) { g.L[k] = Lvl{H >> k, W >> k, off}; off += (long long)(H >> k) * (W >> k); }
+        g.pyr_texels = off;
+        float4* base = reinterpret_cast<float4*>(out);
+        ex.launch("pyr0", [&] { return fbk::launch_u8_to_pyr0(frames, base, B, H, W, off, ex.ctx->stream); });
+        pyramid_levels_inplace(ex, g, base, B, off);
+    });
+}
+
+fb_status fb_remap(fb_ctx ctx, int B, int H, int W, int p, const float* src, const int32_t* nnf, float* out)
+{
+    return guarded(ctx, nullptr, [&](Exec& ex, fb_stats*) {
+        if (!src || !nnf || !out || B < 0 || H < 1 || W < 1 || p < 1) throw Fail{FB_ERR_INVALID_ARG, "bad remap arguments"};
+        if (p > 4) throw Fail{FB_ERR_UNSUPPORTED, "patch_radius > 4 is not compiled"};
+        if (B == 0) return;
+        ex.launch("remap", [&] { return fbk::launch_remap_f3(src, reinterpret_cast<const int2*>(nnf), out, B, H, W, p,
+                                                             ex.ctx->stream); });
+    });
+}
+
+static void validate_nnf(const fb_match_cfg* cfg, int B, int H, int W, const uint8_t* sg, const uint8_t* tg,
+                         const uint8_t* ss, const uint8_t* ts, const int32_t* group, const fb_pair_key* keys,
+                         const int32_t* nnf_out)
+{
+    validate_cfg(cfg);
+    if (B < 1 || H < 1 || W < 1) throw Fail{FB_ERR_INVALID_ARG, "B, H, W must be >= 1"};
+    if (B > kMaxBatchPairs) throw Fail{FB_ERR_INVALID_ARG, "B exceeds 65535 pairs per call"};
+    if (!sg || !tg || !keys || !nnf_out) throw Fail{FB_ERR_INVALID_ARG, "NULL required pointer"};
+    if (cfg->loss != FB_LOSS_BASE && !ss) throw Fail{FB_ERR_INVALID_ARG, "src_style required for this loss"};
+    if (cfg->loss == FB_LOSS_MEAN_ALIGN && (!ts || !group)) throw Fail{FB_ERR_INVALID_ARG, "MEAN_ALIGN needs tgt_style and group"};
+    for (int b = 0; b < B; ++b)
+        if (keys[b].src_id < 0 || keys[b].tgt_id < 0 || keys[b].tgt_id >= (1 << 28) || keys[b].task_tag < 0 ||
+            keys[b].task_tag > 15)
+            throw Fail{FB_ERR_INVALID_ARG, "pair key out of range"};
+}
+
+fb_status fb_nnf_estimate(fb_ctx ctx, const fb_match_cfg* cfg, int B, int H, int W, const uint8_t* src_guide,
+                          const uint8_t* tgt_guide, const uint8_t* src_style, const uint8_t* tgt_style,
+                          const int32_t* group, const fb_pair_key* pair_keys, int32_t* nnf_out, float* err_out,
+                          float* remapped_out, fb_stats* stats)
+{
+    return guarded(ctx, stats, [&](Exec& ex, fb_stats* st) {
+        validate_nnf(cfg, B, H, W, src_guide, tgt_guide, src_style, tgt_style, group, pair_keys, nnf_out);
+        const Geo g = make_geo(*cfg, H, W);
+        nnf_api(ex, *cfg, g, B, src_guide, tgt_guide, src_style, tgt_style, group, pair_keys, nnf_out, err_out,
+                remapped_out, st);
+    });
+}
+
+static void blend_range_body(Exec& ex, fb_stats* st, const fb_match_cfg* cfg, int schedule, int N_total, int f0,
+                             int N, int H, int W, int M, const uint8_t* guide, const uint8_t* style, int t0, int t1,
+                             float* out)
+{
+    validate_cfg(cfg);
+    check_frames(N_total, H, W);
+    if (M < 0) throw Fail{FB_ERR_INVALID_ARG, "M < 0"};
+    if (schedule != FB_SCHED_DIRECT && schedule != FB_SCHED_TREE) throw Fail{FB_ERR_INVALID_ARG, "unknown schedule"};
+    if (schedule == FB_SCHED_TREE && cfg->loss == FB_LOSS_MEAN_ALIGN)
+        throw Fail{FB_ERR_UNSUPPORTED, "accurate mode (MEAN_ALIGN) is defined only for the direct schedule (P:249)"};
+    if (cfg->loss == FB_LOSS_BASE) throw Fail{FB_ERR_INVALID_ARG, "blending needs GUIDE_STYLE or MEAN_ALIGN"};
+    if (!guide || !style || !out) throw Fail{FB_ERR_INVALID_ARG, "NULL required pointer"};
+    if (t0 < 0 || t1 > N_total || t0 >= t1) throw Fail{FB_ERR_INVALID_ARG, "bad target range"};
+    if (f0 < 0 || N < 1 || f0 + N > N_total || f0 > std::max(0, t0 - M) || f0 + N < std::min(N_total, t1 + M))
+        throw Fail{FB_ERR_INVALID_ARG, "local frames must cover the targets plus a halo of M"};
+    const Geo g = make_geo(*cfg, H, W);
+    if (schedule == FB_SCHED_DIRECT) blend_direct(ex, *cfg, g, N_total, f0, N, M, guide, style, t0, t1, out, st);
+    else blend_tree(ex, *cfg, g, N_total, f0, N, M, guide, style, t0, t1, out, st);
+}
+
+fb_status fb_blend_window_range(fb_ctx ctx, const fb_match_cfg* cfg, int schedule, int N_total, int f0, int N,
+                                int H, int W, int M, const uint8_t* guide, const uint8_t* style, int t0, int t1,
+                                float* out, fb_stats* stats)
+{
+    return guarded(ctx, stats, [&](Exec& ex, fb_stats* st) {
+        blend_range_body(ex, st, cfg, schedule, N_total, f0, N, H, W, M, guide, style, t0, t1, out);
+    });
+}
+
+fb_status fb_blend_window(fb_ctx ctx, const fb_match_cfg* cfg, int schedule, int N, int H, int W, int M,
+                          const uint8_t* guide, const uint8_t* style, float* out, fb_stats* stats)
+{
+    return fb_blend_window_range(ctx, cfg, schedule, N, 0, N, H, W, M, guide, style, 0, N, out, stats);
+}
+
+fb_status fb_interpolate_keyframes(fb_ctx ctx, const fb_match_cfg* cfg, int N, int H, int W, const uint8_t* guide,
+                                   int K, const int32_t* key_index, const uint8_t* key_style, float* out,
+                                   fb_stats* stats)
+{
+    return guarded(ctx, stats, [&](Exec& ex, fb_stats* st) {
+        validate_cfg(cfg);
+        check_frames(N, H, W);
+        if (!guide || !key_index || !key_style || !out || K < 1) throw Fail{FB_ERR_INVALID_ARG, "NULL pointer or K < 1"};
+        for (int k = 0; k < K; ++k)
+            if (key_index[k] < 0 || key_index[k] >= N || (k && key_index[k] <= key_index[k - 1]))
+                throw Fail{FB_ERR_INVALID_ARG, "key_index must be strictly increasing in [0, N)"};
+        const Geo g = make_geo(*cfg, H, W);
+        interpolate(ex, *cfg, g, N, guide, K, key_index, key_style, out, st);
+    });
+}
+
+size_t fb_workspace_size(fb_ctx ctx, int op, const fb_match_cfg* cfg, int n, int H, int W, int M)
+{
+    if (!ctx || !cfg || n < 1 || H < 1 || W < 1) return 0;
+    size_t need = 0;
+    const uint8_t* fake = reinterpret_cast<const uint8_t*>(16);  // dry run: pointers are never dereferenced
+    float* fout = reinterpret_cast<float*>(16);
+    std::string saved = ctx->err;
+    fb_status s = FB_OK;
+    if (op == FB_OP_NNF) {
+        std::vector<fb_pair_key> keys(n, fb_pair_key{0, 0, 6});
+        std::vector<int32_t> grp(n, 0);
+        s = guarded(ctx, nullptr, [&](Exec& ex, fb_stats* st) {
+            validate_cfg(cfg);
+            const Geo g = make_geo(*cfg, H, W);
+            nnf_api(ex, *cfg, g, n, fake, fake, fake, fake, grp.data(), keys.data(),
+                    reinterpret_cast<int32_t*>(16), fout, cfg->loss == FB_LOSS_BASE ? nullptr : fout, st);
+        }, &need);
+    } else if (op == FB_OP_BLEND_DIRECT || op == FB_OP_BLEND_TREE) {
+        s = guarded(ctx, nullptr, [&](Exec& ex, fb_stats* st) {
+            blend_range_body(ex, st, cfg, op == FB_OP_BLEND_TREE ? FB_SCHED_TREE : FB_SCHED_DIRECT, n, 0, n, H, W, M,
+                             fake, fake, 0, n, fout);
+        }, &need);
+    } else if (op == FB_OP_INTERPOLATE) {
+        // upper bound: every non-key frame has two keys; the key placement does not change the size
+        std::vector<int32_t> keys;
+        const int K = std::max(1, std::min(M, n));
+        for (int k = 0; k < K; ++k) keys.push_back((int)((long long)k * (n - 1) / std::max(1, K - 1)));
+        keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+        s = guarded(ctx, nullptr, [&](Exec& ex, fb_stats* st) {
+            validate_cfg(cfg);
+            const Geo g = make_geo(*cfg, H, W);
+            interpolate(ex, *cfg, g, n, fake, (int)keys.size(), keys.data(), fake, fout, st);
+        }, &need);
+    } else {
+        return 0;
+    }
+    ctx->err = saved;
+    return s == FB_OK ? std::max<size_t>(need, 256) : 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,246 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): NNF identical on >= 99.9 % of pixels (bit-exact where untied);
+patch error relative difference <= 1e-5; output frames max |diff| <= 1/255 on [0,1] (= 1.0 in the
+8-bit units of the boundary).  The arithmetic contract makes both sides bit-identical,
+so every test also reports the exact-match fraction and most assert it.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth import constant_video, iid_frames, moving_texture, static_textured_video, textured_frame
+
+pytestmark = pytest.mark.gpu
+
+FRAME_TOL = 1.0  # 1/255 on [0,1] RGB, in 8-bit units
+
+
+@pytest.fixture(scope="module")
+def fb():
+    import paper_2311_09265_b200 as P
+    return P
+
+
+@pytest.fixture(scope="module")
+def ctx(fb):
+    return fb.Context(0)
+
+
+def ocfg(c):
+    return O.Cfg(c.patch_radius, c.levels, c.iters_per_level, c.rs_radius0, c.rs_steps, c.alpha, c.loss, c.init, c.seed)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def assert_frames(got, ref, exact=True):
+    got = got.detach().cpu().numpy() if torch.is_tensor(got) else got
+    d = np.abs(got.astype(np.float64) - ref.astype(np.float64))
+    assert d.max() <= FRAME_TOL, f"max |diff| = {d.max()}"
+    if exact:
+        assert np.array_equal(got, ref), f"not bit-exact: {np.mean(got != ref):.3g} of values differ, max {d.max()}"
+
+
+def assert_nnf(F, E, Fr, Er, exact=True):
+    F = F.cpu().numpy()
+    same = np.all(F == Fr, -1)
+    assert same.mean() >= 0.999, f"NNF identical on {same.mean():.5f}"
+    if E is not None:
+        E = E.cpu().numpy()
+        rel = np.abs(E.astype(np.float64) - Er) / np.maximum(np.abs(Er.astype(np.float64)), 1e-30)
+        assert rel[same].max(initial=0) <= 1e-5
+    if exact:
+        assert same.all()
+        if E is not None:
+            assert np.array_equal(E, Er)
+
+
+# ------------------------------------------------------------------------------ a1 pyramid
+@pytest.mark.parametrize("H,W,levels", [(64, 64, 2), (37, 45, 3), (512, 512, 5), (33, 70, 1)])
+def test_pyramid_bit_exact(ctx, H, W, levels):
+    fr = iid_frames(3, H, W, seed=H)
+    got = ctx.fb_build_pyramid(dev(fr), levels).cpu().numpy()
+    for b in range(3):
+        ref = O.pyramid(fr[b].astype(np.float32), levels)
+        off = 0
+        for k in range(levels):
+            n = (H >> k) * (W >> k)
+            lev = got[b, off:off + n].reshape(H >> k, W >> k, 4)
+            np.testing.assert_array_equal(lev[..., :3], ref[k])
+            assert np.all(lev[..., 3] == 0)
+            off += n
+
+
+# ------------------------------------------------------------------------------ a8 remap
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_remap_bit_exact(ctx, p):
+    rng = np.random.default_rng(p)
+    B, H, W = 3, 29, 67
+    S = (rng.random((B, H, W, 3)) * 255).astype(np.float32)
+    F = np.stack([rng.integers(0, H, (B, H, W)), rng.integers(0, W, (B, H, W))], -1).astype(np.int32)
+    got = ctx.fb_remap(dev(S), dev(F), p).cpu().numpy()
+    for b in range(B):
+        np.testing.assert_array_equal(got[b], O.remap(S[b], F[b], p))
+
+
+# ------------------------------------------------------------------------------ a2-a7 NNF estimation
+def _nnf_case(fb, loss, H, W, B=3, seed=4, **kw):
+    g, s = moving_texture(B + 1, H, W, seed=seed)
+    cfg = fb.MatchCfg(patch_radius=kw.pop("p", 2), iters_per_level=kw.pop("n", 2), loss=loss, **kw)
+    sg, tg = g[1:], np.repeat(g[:1], B, 0)
+    ss, ts = s[1:], np.repeat(s[:1], B, 0)
+    keys = [(j + 1, 0, 6) for j in range(B)]
+    frames = np.concatenate([g, s]).astype(np.float32)
+    tasks = [dict(src_guide=j + 1, tgt_guide=0, src_style=B + 1 + j + 1, tgt_style=B + 1, group=0, src_id=j + 1,
+                  tgt_id=0, tag=6) for j in range(B)]
+    if loss != fb.MEAN_ALIGN:
+        for t in tasks:
+            t["group"] = tasks.index(t)
+    if loss == fb.BASE:
+        for t in tasks:
+            t["src_style"] = -1
+    return cfg, (sg, tg, ss, ts, keys), frames, tasks
+
+
+@pytest.mark.parametrize("loss", [0, 1, 2])
+@pytest.mark.parametrize("H,W", [(64, 64), (45, 77)])
+def test_nnf_estimate_matches_oracle(fb, ctx, loss, H, W):
+    cfg, (sg, tg, ss, ts, keys), frames, tasks = _nnf_case(fb, loss, H, W)
+    group = [0] * len(keys) if loss == fb.MEAN_ALIGN else None
+    F, E, X, st = ctx.fb_nnf_estimate(cfg, dev(sg), dev(tg), None if loss == 0 else dev(ss),
+                                      dev(ts) if loss == 2 else None, group=group, pair_keys=keys)
+    Fr, Er, Xr, ev = O.nnf(ocfg(cfg), frames, tasks, want_x=loss != 0)
+    assert st["candidate_evals"] == ev and st["nnf_pairs"] == len(keys)
+    assert_nnf(F, E, Fr, Er)
+    if loss != 0:
+        assert_frames(X, Xr)
+
+
+@pytest.mark.parametrize("kw", [dict(p=1), dict(p=3), dict(p=4, n=1), dict(init=1), dict(rs_radius0=4, rs_steps=3),
+                                dict(levels=1, n=3), dict(alpha=0.0), dict(seed=123456789012345)])
+def test_nnf_estimate_config_variants(fb, ctx, kw):
+    cfg, (sg, tg, ss, ts, keys), frames, tasks = _nnf_case(fb, 1, 40, 52, B=2, **kw)
+    F, E, X, _ = ctx.fb_nnf_estimate(cfg, dev(sg), dev(tg), dev(ss), pair_keys=keys)
+    Fr, Er, Xr, _ = O.nnf(ocfg(cfg), frames, tasks)
+    assert_nnf(F, E, Fr, Er)
+    assert_frames(X, Xr)
+
+
+def test_nnf_batch_invariance(fb, ctx):
+    cfg, (sg, tg, ss, ts, keys), frames, tasks = _nnf_case(fb, 1, 48, 48, B=4)
+    Fb, Eb, Xb, _ = ctx.fb_nnf_estimate(cfg, dev(sg), dev(tg), dev(ss), pair_keys=keys)
+    for b in (0, 3):
+        F1, E1, X1, _ = ctx.fb_nnf_estimate(cfg, dev(sg[b:b + 1]), dev(tg[b:b + 1]), dev(ss[b:b + 1]),
+                                            pair_keys=[keys[b]])
+        assert torch.equal(F1[0], Fb[b]) and torch.equal(E1[0], Eb[b]) and torch.equal(X1[0], Xb[b])
+
+
+def test_identical_frames_identity(fb, ctx):
+    g = textured_frame(48, 40)[None].repeat(2, 0)
+    cfg = fb.MatchCfg(patch_radius=2, iters_per_level=2, loss=fb.GUIDE_STYLE, init=fb.INIT_IDENTITY)
+    F, E, X, _ = ctx.fb_nnf_estimate(cfg, dev(g), dev(g), dev(g), pair_keys=[(0, 1, 6), (0, 1, 6)])
+    rr, cc = np.mgrid[0:48, 0:40]
+    F = F.cpu().numpy()
+    assert np.all(F[..., 0] == rr) and np.all(F[..., 1] == cc) and torch.all(E == 0)
+
+
+# ------------------------------------------------------------------------------ a9/a10 window blends
+CONFIG1 = dict(N=8, H=64, W=64, M=3, p=2, levels=2, n=2)  # BASELINE.json configs[0]
+
+
+@pytest.mark.parametrize("mode", ["balanced", "accurate", "fast"])
+def test_config1_blend_full_parity(fb, ctx, mode):
+    c = CONFIG1
+    g, s = moving_texture(c["N"], c["H"], c["W"])
+    loss = fb.MEAN_ALIGN if mode == "accurate" else fb.GUIDE_STYLE
+    sched = fb.TREE if mode == "fast" else fb.DIRECT
+    cfg = fb.MatchCfg(patch_radius=c["p"], levels=c["levels"], iters_per_level=c["n"], loss=loss)
+    out, st = ctx.fb_blend_window(cfg, sched, dev(g), dev(s), c["M"])
+    fn = O.blend_tree if mode == "fast" else O.blend_direct
+    ref, pairs, evals = fn(ocfg(cfg), g, s, c["M"])
+    assert st["nnf_pairs"] == pairs == (28 if mode == "fast" else 36)
+    assert st["candidate_evals"] == evals
+    assert_frames(out, ref)
+
+
+@pytest.mark.parametrize("N,M,H,W", [(1, 3, 32, 32), (5, 0, 32, 40), (6, 9, 24, 36), (11, 4, 37, 29)])
+@pytest.mark.parametrize("mode", ["balanced", "accurate", "fast"])
+def test_blend_edge_cases(fb, ctx, N, M, H, W, mode):
+    g, s = moving_texture(N, H, W, seed=N * 7 + M)
+    loss = fb.MEAN_ALIGN if mode == "accurate" else fb.GUIDE_STYLE
+    sched = fb.TREE if mode == "fast" else fb.DIRECT
+    cfg = fb.MatchCfg(patch_radius=2, iters_per_level=1, loss=loss)
+    out, _ = ctx.fb_blend_window(cfg, sched, dev(g), dev(s), M)
+    fn = O.blend_tree if mode == "fast" else O.blend_direct
+    ref, _, _ = fn(ocfg(cfg), g, s, M)
+    assert_frames(out, ref)
+    if M == 0 or N == 1:
+        assert_frames(out, s.astype(np.float32))
+
+
+def test_constant_and_static_videos(fb, ctx):
+    g, s = constant_video(6, 32, 40)
+    for loss, sched in ((fb.GUIDE_STYLE, fb.DIRECT), (fb.MEAN_ALIGN, fb.DIRECT), (fb.GUIDE_STYLE, fb.TREE)):
+        out, _ = ctx.fb_blend_window(fb.MatchCfg(iters_per_level=2, loss=loss), sched, dev(g), dev(s), 2)
+        assert_frames(out, s.astype(np.float32))
+    g, s = static_textured_video(9, 24, 28)
+    cfg = fb.MatchCfg(iters_per_level=1, init=fb.INIT_IDENTITY)
+    ref = np.stack([(s[max(0, i - 3):i + 4].astype(np.int64).sum(0) / (min(8, i + 3) - max(0, i - 3) + 1))
+                    for i in range(9)]).astype(np.float32)
+    for sched in (fb.DIRECT, fb.TREE):
+        out, _ = ctx.fb_blend_window(cfg, sched, dev(g), dev(s), 3)
+        assert_frames(out, ref)
+
+
+@pytest.mark.parametrize("mode", ["balanced", "accurate", "fast"])
+def test_batching_and_sharding_invariance(fb, mode):
+    g, s = moving_texture(10, 40, 40, seed=31)
+    loss = fb.MEAN_ALIGN if mode == "accurate" else fb.GUIDE_STYLE
+    sched = fb.TREE if mode == "fast" else fb.DIRECT
+    cfg = fb.MatchCfg(iters_per_level=1, loss=loss)
+    M = 3
+    full, _ = fb.Context(0).fb_blend_window(cfg, sched, dev(g), dev(s), M)
+    small, _ = fb.Context(0, max_batch_pairs=5).fb_blend_window(cfg, sched, dev(g), dev(s), M)
+    assert torch.equal(full, small)
+    ctx = fb.Context(0)
+    for t0, t1 in ((0, 4), (4, 7), (7, 10)):
+        f0, f1 = max(0, t0 - M), min(10, t1 + M)
+        part, _ = ctx.fb_blend_window_range(cfg, sched, 10, f0, dev(g[f0:f1]), dev(s[f0:f1]), M, t0, t1)
+        assert torch.equal(part, full[t0:t1])
+
+
+# ------------------------------------------------------------------------------ a11 interpolation
+@pytest.mark.parametrize("keys", [[0, 7], [2, 5, 9], [4]])
+def test_interpolation_parity(fb, ctx, keys):
+    N = 10
+    g, s = moving_texture(N, 40, 48, seed=17)
+    cfg = fb.MatchCfg(iters_per_level=2)
+    out, st = ctx.fb_interpolate_keyframes(cfg, dev(g), keys, dev(s[keys]))
+    ref, pairs, evals = O.interpolate(ocfg(cfg), g, keys, s[keys])
+    assert st["nnf_pairs"] == pairs and st["candidate_evals"] == evals
+    assert_frames(out, ref)
+    for k in keys:
+        assert_frames(out[k], s[k].astype(np.float32))
+
+
+# ------------------------------------------------------------------------------ errors
+def test_error_statuses(fb, ctx):
+    g, s = moving_texture(4, 32, 32)
+    with pytest.raises(fb.FBError) as e:
+        ctx.fb_blend_window(fb.MatchCfg(loss=fb.MEAN_ALIGN), fb.TREE, dev(g), dev(s), 2)
+    assert e.value.status == 6
+    with pytest.raises(fb.FBError) as e:
+        ctx.fb_blend_window(fb.MatchCfg(patch_radius=9), fb.DIRECT, dev(g), dev(s), 2)
+    assert e.value.status == 6
+    with pytest.raises(fb.FBError) as e:
+        ctx.fb_blend_window(fb.MatchCfg(patch_radius=3), fb.DIRECT, dev(g[:, :6, :6]), dev(s[:, :6, :6]), 2)
+    assert e.value.status == 2
+    with pytest.raises(fb.FBError) as e:
+        ctx.fb_blend_window(fb.MatchCfg(), fb.DIRECT, dev(g), dev(s), -1)
+    assert e.value.status == 1
+    with pytest.raises(fb.FBError) as e:
+        ctx.fb_interpolate_keyframes(fb.MatchCfg(), dev(g), [2, 1], dev(s[:2]))
+    assert e.value.status == 1
