@@ -161,6 +161,7 @@ float orc_patch_dist(const float* A, const float* B, int h, int w, int sr, int s
  * ---------------------------------------------------------------------------------------------- */
 void orc_remap(const float* S, int h, int w, const int32_t* F, int p, float* out)
 {
+#pragma omp parallel for schedule(static)
     for (int r = 0; r < h; ++r)
         for (int c = 0; c < w; ++c) {
             float acc[3] = { 0.0f, 0.0f, 0.0f };
@@ -259,6 +260,7 @@ static void level_field(const orc_level_ctx* L, const orc_cfg* cfg, int field, i
     int h = L->h, w = L->w;
     size_t n = (size_t)h * w;
     if (field < 0) {
+#pragma omp parallel for schedule(static)
         for (int r = 0; r < h; ++r)
             for (int c = 0; c < w; ++c) {
                 size_t i = (size_t)r * w + c;
@@ -268,6 +270,7 @@ static void level_field(const orc_level_ctx* L, const orc_cfg* cfg, int field, i
     }
     if (field < 4) {
         int dx = PROP_DIRS[field][0], dy = PROP_DIRS[field][1];
+#pragma omp parallel for schedule(static)
         for (int r = 0; r < h; ++r)
             for (int c = 0; c < w; ++c) {
                 size_t i = (size_t)r * w + c;
@@ -283,6 +286,7 @@ static void level_field(const orc_level_ctx* L, const orc_cfg* cfg, int field, i
         return;
     }
     int s = field - 4, R = rs_radius(cfg, h, w, s);
+#pragma omp parallel for schedule(static)
     for (int r = 0; r < h; ++r)
         for (int c = 0; c < w; ++c) {
             size_t i = (size_t)r * w + c;
@@ -333,14 +337,12 @@ static void refresh_aux(orc_state* st, int k)
     size_t npx = (size_t)h * w;
     if (cfg->loss == ORC_GUIDE_STYLE) {
         /* S^_i = remap of the task's source style with the current F at this level (D18) */
-#pragma omp parallel for schedule(static)
         for (int t = 0; t < st->T; ++t)
             orc_remap(st->pyr_ss[t] + 3 * st->L[k].off, h, w, st->F[t], p, st->aux[t]);
     } else if (cfg->loss == ORC_MEAN_ALIGN) {
         /* T-bar_i = (sum over j in W_i ascending of Y_j) / |W_i|, Y_i = S_i, Y_j = (S_j -> T)
          * (Eq. 7; D27).  Pairs sharing a group id form one window. */
         float** rem = (float**)malloc(sizeof(float*) * st->T);
-#pragma omp parallel for schedule(static)
         for (int t = 0; t < st->T; ++t) {
             rem[t] = (float*)malloc(sizeof(float) * 3 * npx);
             orc_remap(st->pyr_ss[t] + 3 * st->L[k].off, h, w, st->F[t], p, rem[t]);
@@ -460,12 +462,10 @@ int orc_nnf(const orc_cfg* cfg, int T, int H, int W, const float* frames, const 
         for (int it = 0; it < cfg->iters_per_level; ++it) {
             refresh_aux(&st, k);
             uint64_t ev = 0;
-#pragma omp parallel for schedule(dynamic, 1) reduction(+ : ev)
-            for (int t = 0; t < T; ++t) iterate_task(&st, t, k, it, &ev);
+            for (int t = 0; t < T; ++t) iterate_task(&st, t, k, it, &ev); /* rows run in parallel inside */
             evals += ev;
         }
     }
-#pragma omp parallel for schedule(static)
     for (int t = 0; t < T; ++t) {
         if (F_out) memcpy(F_out + 2 * npx0 * t, st.F[t], sizeof(int32_t) * 2 * npx0);
         if (E_out) memcpy(E_out + npx0 * t, st.E[t], sizeof(float) * npx0);
