@@ -141,9 +141,16 @@ struct Exec {
 struct Geo {
     int H = 0, W = 0, Lv = 0, p = 0;
     Lvl L[24];
+    fbk::PLvl PL[24];          // padded geometry of the packed PatchMatch operands
     long long pyr_texels = 0;  // texels of one pyramid
     long long npx0() const { return (long long)H * W; }
 };
+
+fbk::PLvl padded(int h, int w)
+{
+    const int pitch = ((w + 2 * fbk::kBorder) + 3) & ~3;  // even (texel pairs are 16-byte aligned)
+    return fbk::PLvl{h, w, pitch, h + 2 * fbk::kBorder};
+}
 
 int level_count(int H, int W, int p, int requested)  // D6, D32
 {
@@ -170,6 +177,7 @@ Geo make_geo(const fb_match_cfg& cfg, int H, int W)
     long long off = 0;
     for (int k = 0; k < g.Lv; ++k) {
         g.L[k] = Lvl{H >> k, W >> k, off};
+        g.PL[k] = padded(H >> k, W >> k);
         off += (long long)(H >> k) * (W >> k);
     }
     g.pyr_texels = off;
@@ -229,16 +237,64 @@ void pyramid_levels_inplace(Exec& ex, const Geo& g, float4* base, int B, long lo
         ex.launch("box", [&] { return fbk::launch_box(base, B, stride, g.L[k - 1], g.L[k], ex.ctx->stream); });
 }
 
+// ------------------------------------------------------------------------------------ packed sources
+// A source slot = (source guide, source style): the frame pair an NNF task matches from.  Slots are
+// packed once per call (zero border) and shared by every task that reads them.
+struct SlotSpec {
+    const uint8_t* g8;  // uint8 [H,W,3] guide (SF8 level 0)
+    const uint8_t* s8;  // uint8 [H,W,3] style (SF8 level 0; NULL = zeros, BASE loss)
+    const float4* gp;   // guide float4 pyramid
+    const float4* sp;   // style float4 pyramid (NULL = zeros, BASE loss)
+};
+struct Slots {
+    char* base = nullptr;
+    size_t stride = 0;  // bytes per slot
+    size_t off[24] = {};
+    int fmt0 = fbk::SF8;
+    const char* slot(long long i) const { return base + (size_t)i * stride; }
+};
+
+Slots pack_sources(Exec& ex, const Geo& g, int fmt0, const std::vector<SlotSpec>& specs)
+{
+    Slots S;
+    if (g.p > 2) fmt0 = fbk::SF32;  // the register-resident fast kernel is compiled for p <= 2 only
+    S.fmt0 = fmt0;
+    size_t off = 0;
+    for (int k = 0; k < g.Lv; ++k) {
+        S.off[k] = off;
+        const size_t tb = (k == 0 && fmt0 == fbk::SF8) ? 8 : 32;
+        off = (off + (size_t)g.PL[k].rows * g.PL[k].pitch * tb + 255) & ~size_t(255);
+    }
+    S.stride = off;
+    const int n = (int)specs.size();
+    S.base = ex.ar.take<char>(std::max<size_t>(1, S.stride * (size_t)n));
+    if (n == 0) return S;
+    for (int k = 0; k < g.Lv; ++k) {
+        std::vector<fbk::PackSrc> jobs(n);
+        for (int i = 0; i < n; ++i) {
+            const SlotSpec& sp = specs[i];
+            jobs[i] = fbk::PackSrc{sp.g8, sp.s8, sp.gp ? sp.gp + g.L[k].off : nullptr,
+                                   sp.sp ? sp.sp + g.L[k].off : nullptr, S.base + (size_t)i * S.stride + S.off[k]};
+        }
+        const fbk::PackSrc* dj = ex.upload(jobs);
+        const int fmt = (k == 0 && fmt0 == fbk::SF8) ? fbk::SF8 : fbk::SF32;
+        ex.launch("pack_src", [&] { return fbk::launch_pack_src(dj, n, fmt, g.PL[k], ex.ctx->stream); },
+                  (uint64_t)n * g.PL[k].rows * g.PL[k].pitch);
+    }
+    return S;
+}
+
 // ------------------------------------------------------------------------------------ NNF batch (Alg. 1)
 struct TaskSpec {
-    const float4* sg;  // source guide pyramid
-    const float4* tg;  // target guide pyramid
+    const char* src;   // packed source slot
     const float4* ss;  // source style pyramid (the image being remapped, D22)
+    const float4* tg;  // target guide pyramid
     int group;         // MEAN_ALIGN window index (into groups), else -1
     uint32_t src_id, tgt_id, tag;
 };
 struct GroupSpec {
     const float4* tstyle;  // target style pyramid (the self term of T-bar)
+    const float4* tguide;  // target guide pyramid (the guide half of the packed target)
     uint32_t tgt_id;
 };
 struct BatchOut {
@@ -247,34 +303,38 @@ struct BatchOut {
     long long fstride = 0;
 };
 
-BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const std::vector<TaskSpec>& tasks,
-                 const std::vector<GroupSpec>& groups, fb_stats* st)
+BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& slots,
+                 const std::vector<TaskSpec>& tasks, const std::vector<GroupSpec>& groups, fb_stats* st)
 {
     const int T = (int)tasks.size();
     const long long n0 = g.npx0();
     const cudaStream_t s = ex.ctx->stream;
+    const bool fast0 = slots.fmt0 == fbk::SF8 && g.p <= 2;  // level-0 fast operands (SF8 / TF16)
     BatchOut out;
     out.fstride = n0;
     int2* F[2] = {ex.ar.take<int2>((size_t)T * n0), ex.ar.take<int2>((size_t)T * n0)};
     out.E = ex.ar.take<float>((size_t)T * n0);
-    float4* aux = nullptr;
-    if (cfg.loss == FB_LOSS_GUIDE_STYLE) aux = ex.ar.take<float4>((size_t)T * n0);
-    if (cfg.loss == FB_LOSS_MEAN_ALIGN) aux = ex.ar.take<float4>((size_t)groups.size() * n0);
+    size_t tbytes = 0;  // one packed target operand, largest level
+    for (int k = 0; k < g.Lv; ++k)
+        tbytes = std::max(tbytes, (size_t)g.PL[k].rows * g.PL[k].pitch * ((k == 0 && fast0) ? 16 : 32));
+    tbytes = (tbytes + 255) & ~size_t(255);
+    const bool per_group = cfg.loss == FB_LOSS_MEAN_ALIGN;
+    char* tgt = ex.ar.take<char>(tbytes * (per_group ? groups.size() : (size_t)T));
     std::vector<DTask> dt(T);
     for (int t = 0; t < T; ++t) {
         const TaskSpec& k = tasks[t];
-        dt[t].sg = k.sg; dt[t].tg = k.tg; dt[t].ss = k.ss;
-        dt[t].aux = cfg.loss == FB_LOSS_GUIDE_STYLE ? aux + t * n0
-                  : cfg.loss == FB_LOSS_MEAN_ALIGN  ? aux + (long long)k.group * n0 : nullptr;
+        dt[t].src = k.src;
+        dt[t].tgt = tgt + tbytes * (per_group ? (size_t)k.group : (size_t)t);
+        dt[t].ss = k.ss;
+        dt[t].tg = k.tg;
         dt[t].c2 = k.src_id;
         dt[t].c3 = (k.tag << 28) | k.tgt_id;
-        dt[t].pad0 = dt[t].pad1 = 0;
     }
     const DTask* d_tasks = ex.upload(dt);
     // T-bar member lists for every level (MEAN_ALIGN): ascending source id with the self term inserted.
     std::vector<const DOut*> d_outs(g.Lv, nullptr);
     std::vector<const DMember*> d_mem(g.Lv, nullptr);
-    if (cfg.loss == FB_LOSS_MEAN_ALIGN) {
+    if (per_group) {
         std::vector<std::vector<int>> members(groups.size());
         for (int t = 0; t < T; ++t) members[tasks[t].group].push_back(t);
         for (auto& m : members)
@@ -296,8 +356,9 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const std::vec
                 if (!self_done) mem.push_back(DMember{groups[gi].tstyle + g.L[k].off, -1, 1.0f});
                 o.nm = (int)mem.size() - o.m0;
                 o.div = (float)o.nm;
-                o.fmt = 0;
-                o.out = aux + (long long)gi * n0;
+                o.fmt = (k == 0 && fast0) ? 2 : 3;
+                o.out = tgt + tbytes * gi;
+                o.guide = groups[gi].tguide + g.L[k].off;
                 outs.push_back(o);
             }
             d_outs[k] = ex.upload(outs);
@@ -308,6 +369,9 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const std::vec
     int cur = 0;
     for (int k = g.Lv - 1; k >= 0; --k) {
         const Lvl L = g.L[k];
+        const fbk::PLvl PL = g.PL[k];
+        const bool fast = k == 0 && fast0;
+        const int tfmt = fast ? fbk::TF16 : fbk::TF32;
         if (k == g.Lv - 1) {
             ex.launch("init", [&] { return fbk::launch_init(d_tasks, T, F[cur], n0, L, cfg.init == FB_INIT_IDENTITY,
                                                             rng, (uint32_t)k, s); });
@@ -315,26 +379,28 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const std::vec
             ex.launch("upsample", [&] { return fbk::launch_upsample(F[cur], F[cur ^ 1], T, n0, g.L[k + 1], L, s); });
             cur ^= 1;
         }
+        if (cfg.loss == FB_LOSS_BASE)
+            ex.launch("pack_tgt", [&] { return fbk::launch_pack_tgt_guide(d_tasks, T, L, PL, tfmt, s); });
         const int rk = rs_count(cfg, L), r0 = rs_r0(cfg, L);
         for (int it = 0; it < cfg.iters_per_level; ++it) {
             if (cfg.loss == FB_LOSS_GUIDE_STYLE) {  // S^ refresh (D17/D18)
-                ex.launch("aux", [&] { return fbk::launch_aux_remap(d_tasks, T, F[cur], n0, L, g.p, s); },
+                ex.launch("aux", [&] { return fbk::launch_aux_remap(d_tasks, T, F[cur], n0, L, PL, g.p, tfmt, s); },
                           (uint64_t)T * L.h * L.w);
                 if (st) st->remap_pixels += (uint64_t)T * L.h * L.w;
-            } else if (cfg.loss == FB_LOSS_MEAN_ALIGN) {  // T-bar refresh (Eq. 7, D27)
+            } else if (per_group) {  // T-bar refresh (Eq. 7, D27)
                 ex.launch("tbar", [&] { return fbk::launch_combine(d_outs[k], (int)groups.size(), d_mem[k], F[cur], n0,
-                                                                   L.h, L.w, g.p, s); },
-                          (uint64_t)groups.size() * L.h * L.w);
+                                                                   L.h, L.w, g.p, fast ? 2 : 3, PL, s); },
+                          (uint64_t)T * L.h * L.w);
                 if (st) st->remap_pixels += (uint64_t)T * L.h * L.w;
             }
             fbk::FieldArgs a{};
-            a.tasks = d_tasks; a.E = out.E; a.fstride = n0; a.L = L; a.alpha = cfg.alpha; a.rng = rng;
-            a.level = (uint32_t)k; a.iter = (uint32_t)it; a.rs_r0 = r0; a.rs_k = rk;
+            a.tasks = d_tasks; a.E = out.E; a.fstride = n0; a.L = PL; a.src_off = (long long)slots.off[k];
+            a.alpha = cfg.alpha; a.rng = rng; a.level = (uint32_t)k; a.iter = (uint32_t)it; a.rs_r0 = r0; a.rs_k = rk;
             static const char* kFieldNames[4] = {"field0", "field1", "field2", "field3"};
             for (int ph = 0; ph < 4; ++ph) {
                 a.Fin = F[cur]; a.Fout = F[cur ^ 1];
                 const uint64_t per_px = ph == 0 ? 2 : ph == 3 ? 1 + (uint64_t)rk : 1;
-                ex.launch(kFieldNames[ph], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, ph, s); },
+                ex.launch(kFieldNames[ph], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, ph, fast, s); },
                           per_px * (uint64_t)T * L.h * L.w);
                 cur ^= 1;
             }
@@ -352,7 +418,7 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const std::vec
 struct CombineList {
     std::vector<DOut> outs;
     std::vector<DMember> mem;
-    void begin() { outs.push_back(DOut{(int)mem.size(), 0, 1.0f, 1, nullptr}); }
+    void begin() { outs.push_back(DOut{(int)mem.size(), 0, 1.0f, 1, nullptr, nullptr}); }
     void add_img(const float4* img, float w) { mem.push_back(DMember{img, -1, w}); ++outs.back().nm; }
     void add_remap(const float4* src_level_img, int task, float w) { mem.push_back(DMember{src_level_img, task, w}); ++outs.back().nm; }
     void end(void* out, int fmt, float div) { outs.back().out = out; outs.back().fmt = fmt; outs.back().div = div; }
@@ -363,15 +429,17 @@ void run_combine(Exec& ex, const Geo& g, int k, const CombineList& cl, const int
     if (cl.outs.empty()) return;
     const DOut* o = ex.upload(cl.outs);
     const DMember* m = ex.upload(cl.mem);
+    const int fmt = cl.outs[0].fmt;
     ex.launch("combine", [&] { return fbk::launch_combine(o, (int)cl.outs.size(), m, F, fstride, g.L[k].h, g.L[k].w,
-                                                          g.p, ex.ctx->stream); },
+                                                          g.p, fmt, g.PL[k], ex.ctx->stream); },
               (uint64_t)cl.outs.size() * g.L[k].h * g.L[k].w);
 }
 
 size_t per_pair_bytes(const Geo& g, int loss)
 {
     // F ping-pong + E + (GS aux) per pair, plus descriptor slack
-    return (size_t)g.npx0() * (2 * sizeof(int2) + sizeof(float) + (loss == FB_LOSS_GUIDE_STYLE ? sizeof(float4) : 0)) + 4096;
+    const size_t tgt = (size_t)g.PL[0].rows * g.PL[0].pitch * 32;
+    return (size_t)g.npx0() * (2 * sizeof(int2) + sizeof(float)) + (loss == FB_LOSS_MEAN_ALIGN ? 0 : tgt) + 4096;
 }
 
 int batch_pairs(fb_ctx ctx, const Geo& g, int loss)
@@ -402,6 +470,9 @@ void blend_direct(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int N_total, 
     const Pyr G = pyramid_u8(ex, g, guide, N);
     const Pyr S = pyramid_u8(ex, g, style, N);
     const long long n0 = g.npx0();
+    std::vector<SlotSpec> specs;
+    for (int j = 0; j < N; ++j) specs.push_back(SlotSpec{guide + 3 * n0 * j, style + 3 * n0 * j, G.frame(j), S.frame(j)});
+    const Slots FR = pack_sources(ex, g, fbk::SF8, specs);
     std::vector<int> cost;
     for (int i = t0; i < t1; ++i) cost.push_back(std::min(N_total - 1, i + M) - std::max(0, i - M));
     const auto batches = make_batches(cost, batch_pairs(ex.ctx, g, cfg.loss));
@@ -414,15 +485,15 @@ void blend_direct(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int N_total, 
         for (int q = b0; q < b1; ++q) {
             const int i = t0 + q, lo = std::max(0, i - M), hi = std::min(N_total - 1, i + M);
             first[q - b0] = (int)tasks.size();
-            if (cfg.loss == FB_LOSS_MEAN_ALIGN) groups.push_back(GroupSpec{S.frame(i - f0), (uint32_t)i});
+            if (cfg.loss == FB_LOSS_MEAN_ALIGN) groups.push_back(GroupSpec{S.frame(i - f0), G.frame(i - f0), (uint32_t)i});
             for (int j = lo; j <= hi; ++j) {
                 if (j == i) continue;
-                tasks.push_back(TaskSpec{G.frame(j - f0), G.frame(i - f0), S.frame(j - f0),
+                tasks.push_back(TaskSpec{FR.slot(j - f0), S.frame(j - f0), G.frame(i - f0),
                                          cfg.loss == FB_LOSS_MEAN_ALIGN ? q - b0 : -1, (uint32_t)j, (uint32_t)i, 0u});
             }
         }
         BatchOut bo;
-        if (!tasks.empty()) bo = run_nnf(ex, cfg, g, tasks, groups, st);
+        if (!tasks.empty()) bo = run_nnf(ex, cfg, g, FR, tasks, groups, st);
         CombineList cl;  // out_i = (sum_{j asc} X_{j->i}) / |W_i|, X_{i->i} = S_i (D3, D4)
         for (int q = b0; q < b1; ++q) {
             const int i = t0 + q, lo = std::max(0, i - M), hi = std::min(N_total - 1, i + M);
@@ -466,6 +537,9 @@ void blend_tree(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N_total, i
     const Pyr G = pyramid_u8(ex, g, guide, N);
     const Pyr S = pyramid_u8(ex, g, style, N);
     const long long n0 = g.npx0();
+    std::vector<SlotSpec> specs;
+    for (int j = 0; j < N; ++j) specs.push_back(SlotSpec{guide + 3 * n0 * j, style + 3 * n0 * j, G.frame(j), S.frame(j)});
+    const Slots FR = pack_sources(ex, g, fbk::SF8, specs);
     const int lcap = floor_log2(M + 1);
     const int cap = batch_pairs(ex.ctx, g, cfg.loss);
     const int nt = t1 - t0;
@@ -500,10 +574,10 @@ void blend_tree(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N_total, i
             for (int c = c0; c < c1; ++c) {
                 const auto [j, L] = cells[c];
                 for (int v = j - (1 << L) + 1; v <= j - (1 << (L - 1)); ++v)
-                    tasks.push_back(TaskSpec{G.frame(orig(v) - f0), G.frame(orig(j) - f0), S.frame(orig(v) - f0), -1,
+                    tasks.push_back(TaskSpec{FR.slot(orig(v) - f0), S.frame(orig(v) - f0), G.frame(orig(j) - f0), -1,
                                              (uint32_t)orig(v), (uint32_t)orig(j), tag_build});
             }
-            BatchOut bo = run_nnf(ex, cfg, g, tasks, {}, st);
+            BatchOut bo = run_nnf(ex, cfg, g, FR, tasks, {}, st);
             CombineList cl;
             int t = 0;
             for (int c = c0; c < c1; ++c) {
@@ -542,16 +616,20 @@ void blend_tree(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N_total, i
         for (auto [q0, q1] : make_batches(qcost, cap)) {
             ex.ar.off = mark2;
             std::vector<TaskSpec> tasks;
+            std::vector<SlotSpec> qspecs;  // query sources: (G_i, BT(i,L)) packed as SF32 (float style)
             for (int q = q0; q < q1; ++q) {
                 const int i = t0 + q, v = o == 0 ? i : N_total - 1 - i;
                 for (auto [node, L] : walks[q]) {
                     if (node == v) continue;
-                    tasks.push_back(TaskSpec{G.frame(orig(node) - f0), G.frame(i - f0), bt_pyr(node, L), -1,
-                                             (uint32_t)orig(node), (uint32_t)i, tag_query});
+                    qspecs.push_back(SlotSpec{nullptr, nullptr, G.frame(orig(node) - f0), bt_pyr(node, L)});
+                    tasks.push_back(TaskSpec{nullptr, bt_pyr(node, L), G.frame(i - f0), -1, (uint32_t)orig(node),
+                                             (uint32_t)i, tag_query});
                 }
             }
+            const Slots QS = pack_sources(ex, g, fbk::SF32, qspecs);
+            for (size_t t = 0; t < tasks.size(); ++t) tasks[t].src = QS.slot((long long)t);
             BatchOut bo;
-            if (!tasks.empty()) bo = run_nnf(ex, cfg, g, tasks, {}, st);
+            if (!tasks.empty()) bo = run_nnf(ex, cfg, g, QS, tasks, {}, st);
             CombineList cl;
             int t = 0;
             for (int q = q0; q < q1; ++q) {
@@ -592,6 +670,10 @@ void interpolate(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N, const 
     const Pyr G = pyramid_u8(ex, g, guide, N);
     const Pyr KS = pyramid_u8(ex, g, key_style, K);
     const long long n0 = g.npx0();
+    std::vector<SlotSpec> specs;
+    for (int k = 0; k < K; ++k)
+        specs.push_back(SlotSpec{guide + 3 * n0 * keys[k], key_style + 3 * n0 * k, G.frame(keys[k]), KS.frame(k)});
+    const Slots KSl = pack_sources(ex, g, fbk::SF8, specs);
     struct Tgt { int m, left, right, key; };  // key indices (or -1)
     std::vector<Tgt> tg;
     std::vector<int> cost;
@@ -615,17 +697,17 @@ void interpolate(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N, const 
             if (t.key >= 0) continue;
             if (t.left >= 0) {
                 tl[q - b0] = (int)tasks.size();
-                tasks.push_back(TaskSpec{G.frame(keys[t.left]), G.frame(t.m), KS.frame(t.left), -1, (uint32_t)keys[t.left],
+                tasks.push_back(TaskSpec{KSl.slot(t.left), KS.frame(t.left), G.frame(t.m), -1, (uint32_t)keys[t.left],
                                          (uint32_t)t.m, 5u});
             }
             if (t.right >= 0) {
                 tr[q - b0] = (int)tasks.size();
-                tasks.push_back(TaskSpec{G.frame(keys[t.right]), G.frame(t.m), KS.frame(t.right), -1,
+                tasks.push_back(TaskSpec{KSl.slot(t.right), KS.frame(t.right), G.frame(t.m), -1,
                                          (uint32_t)keys[t.right], (uint32_t)t.m, 5u});
             }
         }
         BatchOut bo;
-        if (!tasks.empty()) bo = run_nnf(ex, cfg, g, tasks, {}, st);
+        if (!tasks.empty()) bo = run_nnf(ex, cfg, g, KSl, tasks, {}, st);
         CombineList cl;
         for (int q = b0; q < b1; ++q) {
             const Tgt& t = tg[q];
@@ -657,6 +739,12 @@ void nnf_api(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int B, const uint8
     Pyr SS, TS;
     if (cfg.loss != FB_LOSS_BASE) SS = pyramid_u8(ex, g, ss, B);
     if (cfg.loss == FB_LOSS_MEAN_ALIGN) TS = pyramid_u8(ex, g, ts, B);
+    const long long np = g.npx0();
+    std::vector<SlotSpec> specs;
+    for (int b = 0; b < B; ++b)
+        specs.push_back(SlotSpec{sg + 3 * np * b, cfg.loss != FB_LOSS_BASE ? ss + 3 * np * b : nullptr, SG.frame(b),
+                                 cfg.loss != FB_LOSS_BASE ? SS.frame(b) : nullptr});
+    const Slots SL = pack_sources(ex, g, fbk::SF8, specs);
     std::vector<TaskSpec> tasks;
     std::vector<GroupSpec> groups;
     std::map<int32_t, int> gidx;
@@ -667,17 +755,17 @@ void nnf_api(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int B, const uint8
             if (it == gidx.end()) {
                 gi = (int)groups.size();
                 gidx[group[b]] = gi;
-                groups.push_back(GroupSpec{TS.frame(b), (uint32_t)keys[b].tgt_id});
+                groups.push_back(GroupSpec{TS.frame(b), TG.frame(b), (uint32_t)keys[b].tgt_id});
             } else {
                 gi = it->second;
                 if (groups[gi].tgt_id != (uint32_t)keys[b].tgt_id)
                     throw Fail{FB_ERR_INVALID_ARG, "pairs of one MEAN_ALIGN group must share tgt_id"};
             }
         }
-        tasks.push_back(TaskSpec{SG.frame(b), TG.frame(b), cfg.loss != FB_LOSS_BASE ? SS.frame(b) : nullptr, gi,
+        tasks.push_back(TaskSpec{SL.slot(b), cfg.loss != FB_LOSS_BASE ? SS.frame(b) : nullptr, TG.frame(b), gi,
                                  (uint32_t)keys[b].src_id, (uint32_t)keys[b].tgt_id, (uint32_t)keys[b].task_tag});
     }
-    BatchOut bo = run_nnf(ex, cfg, g, tasks, groups, st);
+    BatchOut bo = run_nnf(ex, cfg, g, SL, tasks, groups, st);
     const long long n0 = g.npx0();
     ex.d2d(nnf_out, bo.F, sizeof(int2) * (size_t)B * n0);
     if (err_out) ex.d2d(err_out, bo.E, sizeof(float) * (size_t)B * n0);

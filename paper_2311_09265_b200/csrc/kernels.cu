@@ -1,7 +1,11 @@
 // kernels.cu — sm_100a kernels of the FastBlend hot path (arXiv 2311.09265).
 //
 // No tensor cores: the method has no dense contraction (patch distances are gathers of data-dependent
-// patches).  The bound resources are the L1/LSU gather path and the FP32 pipe.
+// patches).  The bound resource is the L1/LSU gather path (ncu: l1tex wavefronts ~97 % of peak on the
+// random-search kernel); the design minimises load instructions and sectors per candidate evaluation
+// (DESIGN.md §6): 8-byte packed u8 source texels at level 0, a zero border instead of per-tap bounds
+// checks, the target patch held in registers across a pixel's candidates, and an exact integer guide
+// term (dp4a) where the contract proves it equal to the FP32 sum.
 //
 // Every floating-point operation that decides a result is written with an explicit IEEE intrinsic
 // (__fadd_rn, __fsub_rn, __fmaf_rn, __fdiv_rn) in the order DESIGN.md §3 fixes (D20), so the kernels
@@ -11,6 +15,7 @@
 namespace fbk {
 
 static constexpr int TILE_X = 32, TILE_Y = 8;  // 256-thread 2D tiles: a warp is one row segment
+static constexpr int B = kBorder;
 
 // ------------------------------------------------------------------------------------ Philox4x32-10
 // Salmon et al. (SC'11).  Counter layout of D21: c0 = pixel, c1 = purpose<<28 | level<<22 | iter<<12 |
@@ -28,6 +33,16 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
 }
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
+
+// u8 channel `ch` of a packed rgb word as an exact float: 0x4B0000xx is 2^23 + xx.
+__device__ __forceinline__ float u8f(uint32_t word, int ch)
+{
+    return __fsub_rn(__uint_as_float(__byte_perm(word, 0x4B000000u, 0x7440u + (uint32_t)ch)), 8388608.0f);
+}
+__device__ __forceinline__ uint32_t pack_rgb(float r, float g, float b)  // exact for integer 0..255
+{
+    return (uint32_t)r | ((uint32_t)g << 8) | ((uint32_t)b << 16);
+}
 
 // ------------------------------------------------------------------------------------ pyramid (D6)
 __global__ void k_u8_to_pyr0(const uint8_t* __restrict__ frames, float4* __restrict__ pyr, int npx,
@@ -55,6 +70,68 @@ __global__ void k_box(float4* __restrict__ pyr, long long pyr_stride, Lvl prev, 
         o.z = __fmul_rn(__fadd_rn(__fadd_rn(a.z, bb.z), __fadd_rn(d.z, e.z)), 0.25f);
         o.w = 0.0f;
         base[cur.off + i] = o;
+    }
+}
+
+// ------------------------------------------------------------------------------------ operand packing
+// Source operands: the whole padded block is written (zeros in the border).
+__global__ void k_pack_src(const PackSrc* __restrict__ jobs, int fmt, PLvl L)
+{
+    const PackSrc J = jobs[blockIdx.y];
+    const int n = L.rows * L.pitch;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int pr = i / L.pitch, pc = i - pr * L.pitch;
+        const int r = pr - B, c = pc - B;
+        const bool in = (unsigned)r < (unsigned)L.h && (unsigned)c < (unsigned)L.w;
+        if (fmt == SF8) {
+            uint2 v = make_uint2(0u, 0u);
+            if (in) {
+                const uint8_t* g = J.g8 + 3LL * (r * L.w + c);
+                v.x = g[0] | (g[1] << 8) | (g[2] << 16);
+                if (J.s8) {
+                    const uint8_t* s = J.s8 + 3LL * (r * L.w + c);
+                    v.y = s[0] | (s[1] << 8) | (s[2] << 16);
+                }
+            }
+            reinterpret_cast<uint2*>(J.out)[i] = v;
+        } else {
+            float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+            if (in) {
+                const float4 g = J.gp[r * L.w + c];
+                const float4 s = J.sp ? J.sp[r * L.w + c] : make_float4(0.f, 0.f, 0.f, 0.f);
+                a = make_float4(g.x, g.y, g.z, s.x);
+                b = make_float4(s.y, s.z, 0.0f, 0.0f);
+            }
+            reinterpret_cast<float4*>(J.out)[2 * i] = a;
+            reinterpret_cast<float4*>(J.out)[2 * i + 1] = b;
+        }
+    }
+}
+
+__device__ __forceinline__ void store_tgt(char* out, int tfmt, int i, bool in, float4 g, float ar, float ag, float ab)
+{
+    if (tfmt == TF16) {
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (in) v = make_uint4(pack_rgb(g.x, g.y, g.z), __float_as_uint(ar), __float_as_uint(ag), __float_as_uint(ab));
+        reinterpret_cast<uint4*>(out)[i] = v;
+    } else {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+        if (in) { a = make_float4(g.x, g.y, g.z, ar); b = make_float4(ag, ab, 0.0f, 0.0f); }
+        reinterpret_cast<float4*>(out)[2 * i] = a;
+        reinterpret_cast<float4*>(out)[2 * i + 1] = b;
+    }
+}
+
+// BASE loss: the target operand is the target guide alone.
+__global__ void k_pack_tgt_guide(const DTask* __restrict__ tasks, Lvl L, PLvl P, int tfmt)
+{
+    const DTask T = tasks[blockIdx.y];
+    const int n = P.rows * P.pitch;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int r = i / P.pitch - B, c = i % P.pitch - B;
+        const bool in = (unsigned)r < (unsigned)P.h && (unsigned)c < (unsigned)P.w;
+        const float4 g = in ? T.tg[L.off + r * P.w + c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        store_tgt(T.tgt, tfmt, i, in, g, 0.0f, 0.0f, 0.0f);
     }
 }
 
@@ -123,51 +200,69 @@ __device__ __forceinline__ float3 remap_px(const float4* __restrict__ S, const i
     return make_float3(__fdiv_rn(ax, fn), __fdiv_rn(ay, fn), __fdiv_rn(az, fn));
 }
 
+// S^ refresh (GUIDE_STYLE, D17/D18): packed target = {G_tgt, remap(S_src, F)} over the padded grid.
 template <int P>
-__global__ void k_aux_remap(const DTask* __restrict__ tasks, const int2* __restrict__ F, long long fstride, Lvl L)
+__global__ void k_aux_remap(const DTask* __restrict__ tasks, const int2* __restrict__ F, long long fstride, Lvl L,
+                            PLvl PL, int tfmt)
 {
     const int t = blockIdx.y;
-    const int n = L.h * L.w;
     const DTask T = tasks[t];
     const float4* S = T.ss + L.off;
     const int2* Ft = F + t * fstride;
+    const int n = PL.rows * PL.pitch;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int r = i / L.w, c = i - r * L.w;
-        const float3 v = remap_px<P>(S, Ft, L.h, L.w, r, c);
-        T.aux[i] = make_float4(v.x, v.y, v.z, 0.0f);
+        const int r = i / PL.pitch - B, c = i % PL.pitch - B;
+        const bool in = (unsigned)r < (unsigned)L.h && (unsigned)c < (unsigned)L.w;
+        float3 v = make_float3(0.f, 0.f, 0.f);
+        float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (in) {
+            v = remap_px<P>(S, Ft, L.h, L.w, r, c);
+            g = __ldg(&T.tg[L.off + r * L.w + c]);
+        }
+        store_tgt(T.tgt, tfmt, i, in, g, v.x, v.y, v.z);
     }
 }
 
-template <int P>
+template <int P, int FMT>
 __global__ void k_combine(const DOut* __restrict__ outs, const DMember* __restrict__ mem, const int2* __restrict__ F,
-                          long long fstride, int h, int w)
+                          long long fstride, int h, int w, PLvl PL)
 {
     const DOut o = outs[blockIdx.y];
-    const int n = h * w;
+    const bool padded = FMT >= 2;
+    const int n = padded ? PL.rows * PL.pitch : h * w;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int r = i / w, c = i - r * w;
+        int r, c;
+        if (padded) { r = i / PL.pitch - B; c = i % PL.pitch - B; }
+        else { r = i / w; c = i - r * w; }
+        const bool in = (unsigned)r < (unsigned)h && (unsigned)c < (unsigned)w;
         float ax = 0.0f, ay = 0.0f, az = 0.0f;
-        for (int m = 0; m < o.nm; ++m) {
-            const DMember mb = mem[o.m0 + m];
-            float3 y;
-            if (mb.task < 0) {
-                const float4 v = __ldg(&mb.img[i]);
-                y = make_float3(v.x, v.y, v.z);
-            } else {
-                y = remap_px<P>(mb.img, F + mb.task * fstride, h, w, r, c);
+        if (in) {
+            const int j = r * w + c;
+            for (int m = 0; m < o.nm; ++m) {
+                const DMember mb = mem[o.m0 + m];
+                float3 y;
+                if (mb.task < 0) {
+                    const float4 v = __ldg(&mb.img[j]);
+                    y = make_float3(v.x, v.y, v.z);
+                } else {
+                    y = remap_px<P>(mb.img, F + mb.task * fstride, h, w, r, c);
+                }
+                ax = __fmaf_rn(mb.w, y.x, ax);
+                ay = __fmaf_rn(mb.w, y.y, ay);
+                az = __fmaf_rn(mb.w, y.z, az);
             }
-            ax = __fmaf_rn(mb.w, y.x, ax);
-            ay = __fmaf_rn(mb.w, y.y, ay);
-            az = __fmaf_rn(mb.w, y.z, az);
+            ax = __fdiv_rn(ax, o.div);
+            ay = __fdiv_rn(ay, o.div);
+            az = __fdiv_rn(az, o.div);
         }
-        ax = __fdiv_rn(ax, o.div);
-        ay = __fdiv_rn(ay, o.div);
-        az = __fdiv_rn(az, o.div);
-        if (o.fmt == 0) {
+        if (FMT == 0) {
             static_cast<float4*>(o.out)[i] = make_float4(ax, ay, az, 0.0f);
-        } else {
+        } else if (FMT == 1) {
             float* d = static_cast<float*>(o.out) + 3LL * i;
             d[0] = ax; d[1] = ay; d[2] = az;
+        } else {
+            const float4 g = in ? __ldg(&o.guide[r * w + c]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            store_tgt(static_cast<char*>(o.out), FMT == 2 ? TF16 : TF32, i, in, g, ax, ay, az);
         }
     }
 }
@@ -208,89 +303,92 @@ __global__ void k_remap_f3(const float* __restrict__ src, const int2* __restrict
     }
 }
 
-__global__ void k_f4_to_f3(const float4* __restrict__ in, long long in_stride, float* __restrict__ out, int npx)
-{
-    const int b = blockIdx.y;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npx; i += gridDim.x * blockDim.x) {
-        const float4 v = in[(long long)b * in_stride + i];
-        float* d = out + 3LL * ((long long)b * npx + i);
-        d[0] = v.x; d[1] = v.y; d[2] = v.z;
-    }
-}
-
-// ------------------------------------------------------------------------------------ patch loss
-// D(A,(sr,sc),B,(r,c)) = sum_dr ( rho_dr ), rho_dr = fma chain over dc then channel of (B - A)^2, zero
-// outside the image (Eq. 1, D9, D20).  GS = two-term loss fma(alpha, D_guide, D_style) (Eq. 3 / Eq. 8).
-template <int P, bool GS>
-__device__ __forceinline__ float patch_loss(const float4* __restrict__ sg, const float4* __restrict__ ss,
-                                            const float4* __restrict__ tg, const float4* __restrict__ ax, int h,
-                                            int w, int r, int c, int sr, int sc, float alpha)
-{
-    float dg = 0.0f, ds = 0.0f;
-    const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-#pragma unroll
-    for (int dr = -P; dr <= P; ++dr) {
-        const int tr = r + dr, ur = sr + dr;
-        const bool tin_r = (unsigned)tr < (unsigned)h, sin_r = (unsigned)ur < (unsigned)h;
-        float rg = 0.0f, rs = 0.0f;
-#pragma unroll
-        for (int dc = -P; dc <= P; ++dc) {
-            const int tc = c + dc, uc = sc + dc;
-            const bool tin = tin_r && (unsigned)tc < (unsigned)w;
-            const bool sin = sin_r && (unsigned)uc < (unsigned)w;
-            const int ti = tr * w + tc, si = ur * w + uc;
-            const float4 b = tin ? __ldg(&tg[ti]) : z;
-            const float4 a = sin ? __ldg(&sg[si]) : z;
-            float d;
-            d = __fsub_rn(b.x, a.x); rg = __fmaf_rn(d, d, rg);
-            d = __fsub_rn(b.y, a.y); rg = __fmaf_rn(d, d, rg);
-            d = __fsub_rn(b.z, a.z); rg = __fmaf_rn(d, d, rg);
-            if (GS) {
-                const float4 bb = tin ? __ldg(&ax[ti]) : z;
-                const float4 aa = sin ? __ldg(&ss[si]) : z;
-                d = __fsub_rn(bb.x, aa.x); rs = __fmaf_rn(d, d, rs);
-                d = __fsub_rn(bb.y, aa.y); rs = __fmaf_rn(d, d, rs);
-                d = __fsub_rn(bb.z, aa.z); rs = __fmaf_rn(d, d, rs);
-            }
-        }
-        dg = __fadd_rn(dg, rg);
-        if (GS) ds = __fadd_rn(ds, rs);
-    }
-    return GS ? __fmaf_rn(alpha, dg, ds) : dg;
-}
-
+// ------------------------------------------------------------------------------------ the field kernels
 // One element of Alg. 1's updating sequence per launch, Jacobi over pixels:
 //   PHASE 0: E <- L(F), then propagation (-1,0); 1: (+1,0); 2: (0,-1);
 //   PHASE 3: propagation (0,+1), then the K random-search fields, pointwise in registers.
 // Each candidate F' = clamp(.) is kept iff L(F') < E (strict, D16).
-template <int P, bool GS, int PHASE>
-__global__ void __launch_bounds__(TILE_X* TILE_Y) k_field(FieldArgs a)
+//
+// Loss (Eq. 1 / Eq. 3 / Eq. 8): D = sum over rows dr of rho_dr, rho_dr = fma chain over dc then
+// channel of (target - source)^2 (D20); two-term losses return fma(alpha, D_guide, D_style).
+
+// ---- fast variant: SF8 source, TF16 target, target patch in registers (P <= 2) -------------------
+// Guide term: at level 0 every guide value is an integer 0..255, every partial sum of the FP32 chain
+// is an integer below 2^24 (p <= 4), so the chain is exact and equals the integer SSD computed with
+// byte-wise |a-b| and dp4a; it is converted once, exactly.  Style term: the FP32 chain of D20 with the
+// u8 source channel converted exactly (u8f).
+template <int P, bool TWO, int PHASE>
+__global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_fast(FieldArgs a)
 {
+    constexpr int D = 2 * P + 1;
+    constexpr int NCH = (D + 2) / 2;  // 16-byte chunks (texel pairs) covering D texels at either parity
     const int t = blockIdx.x / a.tiles_per_task;
     const int tile = blockIdx.x - t * a.tiles_per_task;
     const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
     const int c = tx * TILE_X + (threadIdx.x & (TILE_X - 1));
     const int r = ty * TILE_Y + (threadIdx.x / TILE_X);
-    const int h = a.L.h, w = a.L.w;
+    const int h = a.L.h, w = a.L.w, pitch = a.L.pitch;
     if (r >= h || c >= w) return;
     const DTask T = a.tasks[t];
-    const float4* sg = T.sg + a.L.off;
-    const float4* tg = T.tg + a.L.off;
-    const float4* ss = GS ? T.ss + a.L.off : nullptr;
-    const float4* ax = GS ? T.aux : nullptr;
+    const uint2* S = reinterpret_cast<const uint2*>(T.src + a.src_off);
+    const uint4* Tt = reinterpret_cast<const uint4*>(T.tgt);
+    uint32_t tgG[D][D];
+    float tgA[D][D][3];
+#pragma unroll
+    for (int dr = 0; dr < D; ++dr)
+#pragma unroll
+        for (int dc = 0; dc < D; ++dc) {
+            const uint4 v = __ldg(&Tt[(r + dr - P + B) * pitch + (c + dc - P + B)]);
+            tgG[dr][dc] = v.x;
+            tgA[dr][dc][0] = __uint_as_float(v.y);
+            tgA[dr][dc][1] = __uint_as_float(v.z);
+            tgA[dr][dc][2] = __uint_as_float(v.w);
+        }
+    auto loss = [&](int sr, int sc) -> float {
+        uint32_t dg = 0u;
+        float ds = 0.0f;
+#pragma unroll
+        for (int dr = 0; dr < D; ++dr) {
+            const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
+            const int o = idx & 1;
+            const uint4* cp = reinterpret_cast<const uint4*>(S + (idx - o));
+            uint32_t wd[4 * NCH];
+#pragma unroll
+            for (int k = 0; k < NCH; ++k) {
+                const uint4 v = __ldg(cp + k);
+                wd[4 * k] = v.x; wd[4 * k + 1] = v.y; wd[4 * k + 2] = v.z; wd[4 * k + 3] = v.w;
+            }
+            float rs = 0.0f;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const uint32_t g = o ? wd[2 * j + 2] : wd[2 * j];
+                const uint32_t d = __vabsdiffu4(g, tgG[dr][j]);
+                dg = __dp4a(d, d, dg);
+                if (TWO) {
+                    const uint32_t s = o ? wd[2 * j + 3] : wd[2 * j + 1];
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) {
+                        const float dl = __fsub_rn(tgA[dr][j][ch], u8f(s, ch));
+                        rs = __fmaf_rn(dl, dl, rs);
+                    }
+                }
+            }
+            if (TWO) ds = __fadd_rn(ds, rs);
+        }
+        const float fg = __uint2float_rn(dg);
+        return TWO ? __fmaf_rn(a.alpha, fg, ds) : fg;
+    };
     const int2* Fi = a.Fin + t * a.fstride;
     const int i = r * w + c;
     int2 f = Fi[i];
-    float e;
-    if (PHASE == 0) e = patch_loss<P, GS>(sg, ss, tg, ax, h, w, r, c, f.x, f.y, a.alpha);
-    else e = a.E[t * a.fstride + i];
+    float e = PHASE == 0 ? loss(f.x, f.y) : a.E[t * a.fstride + i];
     {
         constexpr int dx = PHASE == 0 ? -1 : (PHASE == 1 ? 1 : 0);
         constexpr int dy = PHASE == 2 ? -1 : (PHASE == 3 ? 1 : 0);
         const int nr = clampi(r + dx, 0, h - 1), nc = clampi(c + dy, 0, w - 1);  // D11
         const int2 fn = Fi[nr * w + nc];
         const int sr = clampi(fn.x - dx, 0, h - 1), sc = clampi(fn.y - dy, 0, w - 1);  // D10
-        const float e2 = patch_loss<P, GS>(sg, ss, tg, ax, h, w, r, c, sr, sc, a.alpha);
+        const float e2 = loss(sr, sc);
         if (e2 < e) { f = make_int2(sr, sc); e = e2; }
     }
     if (PHASE == 3) {
@@ -302,7 +400,95 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field(FieldArgs a)
             const uint32_t span = 2u * (uint32_t)R + 1u;
             const int ox = (int)__umulhi(u.x, span) - R, oy = (int)__umulhi(u.y, span) - R;
             const int sr = clampi(f.x + ox, 0, h - 1), sc = clampi(f.y + oy, 0, w - 1);
-            const float e2 = patch_loss<P, GS>(sg, ss, tg, ax, h, w, r, c, sr, sc, a.alpha);
+            const float e2 = loss(sr, sc);
+            if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+        }
+    }
+    a.Fout[t * a.fstride + i] = f;
+    a.E[t * a.fstride + i] = e;
+}
+
+// ---- general variant: SF32 source, TF32 target staged in shared memory (any level, P <= 4) -------
+template <int P, bool TWO, int PHASE>
+__global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
+{
+    constexpr int D = 2 * P + 1, SX = TILE_X + 2 * P, SY = TILE_Y + 2 * P;
+    __shared__ float4 t0[SY][SX];  // {G.r, G.g, G.b, aux.r}
+    __shared__ float2 t1[SY][SX];  // {aux.g, aux.b}
+    const int t = blockIdx.x / a.tiles_per_task;
+    const int tile = blockIdx.x - t * a.tiles_per_task;
+    const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+    const int h = a.L.h, w = a.L.w, pitch = a.L.pitch;
+    const DTask T = a.tasks[t];
+    {
+        const float4* Tt = reinterpret_cast<const float4*>(T.tgt);
+        for (int k = threadIdx.x; k < SX * SY; k += TILE_X * TILE_Y) {
+            const int yy = k / SX, xx = k - yy * SX;
+            const int pr = ty * TILE_Y + yy - P + B, pc = tx * TILE_X + xx - P + B;  // padded coords
+            float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+            if (pr < a.L.rows && pc < pitch) {
+                v0 = __ldg(&Tt[2 * (pr * pitch + pc)]);
+                v1 = __ldg(&Tt[2 * (pr * pitch + pc) + 1]);
+            }
+            t0[yy][xx] = v0;
+            t1[yy][xx] = make_float2(v1.x, v1.y);
+        }
+    }
+    __syncthreads();
+    const int lx = threadIdx.x & (TILE_X - 1), ly = threadIdx.x / TILE_X;
+    const int c = tx * TILE_X + lx, r = ty * TILE_Y + ly;
+    if (r >= h || c >= w) return;
+    const float4* S = reinterpret_cast<const float4*>(T.src + a.src_off);
+    auto loss = [&](int sr, int sc) -> float {
+        float dg = 0.0f, ds = 0.0f;
+#pragma unroll
+        for (int dr = 0; dr < D; ++dr) {
+            const int base = (sr + dr - P + B) * pitch + (sc - P + B);
+            float rg = 0.0f, rs = 0.0f;
+#pragma unroll
+            for (int dc = 0; dc < D; ++dc) {
+                const float4 s0 = __ldg(&S[2 * (base + dc)]);
+                const float4 q0 = t0[ly + dr][lx + dc];
+                float dl;
+                dl = __fsub_rn(q0.x, s0.x); rg = __fmaf_rn(dl, dl, rg);
+                dl = __fsub_rn(q0.y, s0.y); rg = __fmaf_rn(dl, dl, rg);
+                dl = __fsub_rn(q0.z, s0.z); rg = __fmaf_rn(dl, dl, rg);
+                if (TWO) {
+                    const float4 s1 = __ldg(&S[2 * (base + dc) + 1]);
+                    const float2 q1 = t1[ly + dr][lx + dc];
+                    dl = __fsub_rn(q0.w, s0.w); rs = __fmaf_rn(dl, dl, rs);
+                    dl = __fsub_rn(q1.x, s1.x); rs = __fmaf_rn(dl, dl, rs);
+                    dl = __fsub_rn(q1.y, s1.y); rs = __fmaf_rn(dl, dl, rs);
+                }
+            }
+            dg = __fadd_rn(dg, rg);
+            if (TWO) ds = __fadd_rn(ds, rs);
+        }
+        return TWO ? __fmaf_rn(a.alpha, dg, ds) : dg;
+    };
+    const int2* Fi = a.Fin + t * a.fstride;
+    const int i = r * w + c;
+    int2 f = Fi[i];
+    float e = PHASE == 0 ? loss(f.x, f.y) : a.E[t * a.fstride + i];
+    {
+        constexpr int dx = PHASE == 0 ? -1 : (PHASE == 1 ? 1 : 0);
+        constexpr int dy = PHASE == 2 ? -1 : (PHASE == 3 ? 1 : 0);
+        const int nr = clampi(r + dx, 0, h - 1), nc = clampi(c + dy, 0, w - 1);  // D11
+        const int2 fn = Fi[nr * w + nc];
+        const int sr = clampi(fn.x - dx, 0, h - 1), sc = clampi(fn.y - dy, 0, w - 1);  // D10
+        const float e2 = loss(sr, sc);
+        if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+    }
+    if (PHASE == 3) {
+        for (int s = 0; s < a.rs_k; ++s) {
+            const int R = max(a.rs_r0 >> s, 1);
+            const uint4 u = philox4x32_10(
+                make_uint4((uint32_t)i, (1u << 28) | (a.level << 22) | (a.iter << 12) | (uint32_t)s, T.c2, T.c3),
+                a.rng.k0, a.rng.k1);
+            const uint32_t span = 2u * (uint32_t)R + 1u;
+            const int ox = (int)__umulhi(u.x, span) - R, oy = (int)__umulhi(u.y, span) - R;
+            const int sr = clampi(f.x + ox, 0, h - 1), sc = clampi(f.y + oy, 0, w - 1);
+            const float e2 = loss(sr, sc);
             if (e2 < e) { f = make_int2(sr, sc); e = e2; }
         }
     }
@@ -319,16 +505,29 @@ static inline dim3 grid1d(long long n, int y, int threads = 256)
     return dim3((unsigned)b, (unsigned)y);
 }
 
-cudaError_t launch_u8_to_pyr0(const uint8_t* frames, float4* pyr, int B, int H, int W, long long pyr_stride,
+cudaError_t launch_u8_to_pyr0(const uint8_t* frames, float4* pyr, int Bn, int H, int W, long long pyr_stride,
                               cudaStream_t s)
 {
-    k_u8_to_pyr0<<<grid1d((long long)H * W, B), 256, 0, s>>>(frames, pyr, H * W, pyr_stride);
+    k_u8_to_pyr0<<<grid1d((long long)H * W, Bn), 256, 0, s>>>(frames, pyr, H * W, pyr_stride);
     return cudaGetLastError();
 }
 
-cudaError_t launch_box(float4* pyr, int B, long long pyr_stride, Lvl prev, Lvl cur, cudaStream_t s)
+cudaError_t launch_box(float4* pyr, int Bn, long long pyr_stride, Lvl prev, Lvl cur, cudaStream_t s)
 {
-    k_box<<<grid1d((long long)cur.h * cur.w, B), 256, 0, s>>>(pyr, pyr_stride, prev, cur);
+    k_box<<<grid1d((long long)cur.h * cur.w, Bn), 256, 0, s>>>(pyr, pyr_stride, prev, cur);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_src(const PackSrc* jobs, int n, int fmt, PLvl L, cudaStream_t s)
+{
+    if (n <= 0) return cudaSuccess;
+    k_pack_src<<<grid1d((long long)L.rows * L.pitch, n), 256, 0, s>>>(jobs, fmt, L);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_tgt_guide(const DTask* tasks, int T, Lvl L, PLvl P, int tfmt, cudaStream_t s)
+{
+    k_pack_tgt_guide<<<grid1d((long long)P.rows * P.pitch, T), 256, 0, s>>>(tasks, L, P, tfmt);
     return cudaGetLastError();
 }
 
@@ -354,55 +553,79 @@ cudaError_t launch_upsample(const int2* Fc, int2* Ff, int T, long long fstride, 
     default: return cudaErrorInvalidValue;          \
     }
 
-cudaError_t launch_aux_remap(const DTask* tasks, int T, const int2* F, long long fstride, Lvl L, int p,
-                             cudaStream_t s)
+cudaError_t launch_aux_remap(const DTask* tasks, int T, const int2* F, long long fstride, Lvl L, PLvl PL, int p,
+                             int tfmt, cudaStream_t s)
 {
-    FB_DISPATCH_P(p, (k_aux_remap<PP><<<grid1d((long long)L.h * L.w, T), 256, 0, s>>>(tasks, F, fstride, L)));
+    FB_DISPATCH_P(p, (k_aux_remap<PP><<<grid1d((long long)PL.rows * PL.pitch, T), 256, 0, s>>>(tasks, F, fstride, L,
+                                                                                               PL, tfmt)));
     return cudaGetLastError();
 }
 
-cudaError_t launch_combine(const DOut* outs, int n_outs, const DMember* mem, const int2* F, long long fstride,
-                           int h, int w, int p, cudaStream_t s)
+template <int P>
+static void launch_combine_t(const DOut* outs, int n_outs, const DMember* mem, const int2* F, long long fstride,
+                             int h, int w, int fmt, PLvl PL, cudaStream_t s)
 {
-    if (n_outs <= 0) return cudaSuccess;
-    FB_DISPATCH_P(p, (k_combine<PP><<<grid1d((long long)h * w, n_outs), 256, 0, s>>>(outs, mem, F, fstride, h, w)));
-    return cudaGetLastError();
-}
-
-cudaError_t launch_remap_f3(const float* src, const int2* F, float* out, int B, int H, int W, int p,
-                            cudaStream_t s)
-{
-    FB_DISPATCH_P(p, (k_remap_f3<PP><<<grid1d((long long)H * W, B), 256, 0, s>>>(src, F, out, H, W)));
-    return cudaGetLastError();
-}
-
-cudaError_t launch_f4_to_f3(const float4* in, long long in_stride, float* out, int B, int npx, cudaStream_t s)
-{
-    k_f4_to_f3<<<grid1d(npx, B), 256, 0, s>>>(in, in_stride, out, npx);
-    return cudaGetLastError();
-}
-
-template <int P, bool GS>
-static void launch_field_t(const FieldArgs& a, int T, int phase, cudaStream_t s)
-{
-    const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(TILE_X * TILE_Y);
-    switch (phase) {
-    case 0: k_field<P, GS, 0><<<grid, block, 0, s>>>(a); break;
-    case 1: k_field<P, GS, 1><<<grid, block, 0, s>>>(a); break;
-    case 2: k_field<P, GS, 2><<<grid, block, 0, s>>>(a); break;
-    default: k_field<P, GS, 3><<<grid, block, 0, s>>>(a); break;
+    const dim3 g = grid1d(fmt >= 2 ? (long long)PL.rows * PL.pitch : (long long)h * w, n_outs);
+    switch (fmt) {
+    case 0: k_combine<P, 0><<<g, 256, 0, s>>>(outs, mem, F, fstride, h, w, PL); break;
+    case 1: k_combine<P, 1><<<g, 256, 0, s>>>(outs, mem, F, fstride, h, w, PL); break;
+    case 2: k_combine<P, 2><<<g, 256, 0, s>>>(outs, mem, F, fstride, h, w, PL); break;
+    default: k_combine<P, 3><<<g, 256, 0, s>>>(outs, mem, F, fstride, h, w, PL); break;
     }
 }
 
-cudaError_t launch_field(const FieldArgs& a0, int T, int p, int loss, int phase, cudaStream_t s)
+cudaError_t launch_combine(const DOut* outs, int n_outs, const DMember* mem, const int2* F, long long fstride,
+                           int h, int w, int p, int fmt, PLvl PL, cudaStream_t s)
+{
+    if (n_outs <= 0) return cudaSuccess;
+    FB_DISPATCH_P(p, (launch_combine_t<PP>(outs, n_outs, mem, F, fstride, h, w, fmt, PL, s)));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_remap_f3(const float* src, const int2* F, float* out, int Bn, int H, int W, int p,
+                            cudaStream_t s)
+{
+    FB_DISPATCH_P(p, (k_remap_f3<PP><<<grid1d((long long)H * W, Bn), 256, 0, s>>>(src, F, out, H, W)));
+    return cudaGetLastError();
+}
+
+template <int P, bool TWO>
+static void launch_field_gen(const FieldArgs& a, int T, int phase, cudaStream_t s)
+{
+    const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(TILE_X * TILE_Y);
+    switch (phase) {
+    case 0: k_field_gen<P, TWO, 0><<<grid, block, 0, s>>>(a); break;
+    case 1: k_field_gen<P, TWO, 1><<<grid, block, 0, s>>>(a); break;
+    case 2: k_field_gen<P, TWO, 2><<<grid, block, 0, s>>>(a); break;
+    default: k_field_gen<P, TWO, 3><<<grid, block, 0, s>>>(a); break;
+    }
+}
+
+template <int P, bool TWO>
+static void launch_field_fast(const FieldArgs& a, int T, int phase, cudaStream_t s)
+{
+    const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(TILE_X * TILE_Y);
+    switch (phase) {
+    case 0: k_field_fast<P, TWO, 0><<<grid, block, 0, s>>>(a); break;
+    case 1: k_field_fast<P, TWO, 1><<<grid, block, 0, s>>>(a); break;
+    case 2: k_field_fast<P, TWO, 2><<<grid, block, 0, s>>>(a); break;
+    default: k_field_fast<P, TWO, 3><<<grid, block, 0, s>>>(a); break;
+    }
+}
+
+cudaError_t launch_field(const FieldArgs& a0, int T, int p, int loss, int phase, bool fast, cudaStream_t s)
 {
     FieldArgs a = a0;
     a.tiles_x = (a.L.w + TILE_X - 1) / TILE_X;
     a.tiles_per_task = a.tiles_x * ((a.L.h + TILE_Y - 1) / TILE_Y);
-    if (loss == 0) {
-        FB_DISPATCH_P(p, (launch_field_t<PP, false>(a, T, phase, s)));
+    if (fast) {
+        if (p == 1) { loss ? launch_field_fast<1, true>(a, T, phase, s) : launch_field_fast<1, false>(a, T, phase, s); }
+        else if (p == 2) { loss ? launch_field_fast<2, true>(a, T, phase, s) : launch_field_fast<2, false>(a, T, phase, s); }
+        else return cudaErrorInvalidValue;
+    } else if (loss == 0) {
+        FB_DISPATCH_P(p, (launch_field_gen<PP, false>(a, T, phase, s)));
     } else {
-        FB_DISPATCH_P(p, (launch_field_t<PP, true>(a, T, phase, s)));
+        FB_DISPATCH_P(p, (launch_field_gen<PP, true>(a, T, phase, s)));
     }
     return cudaGetLastError();
 }

@@ -3,27 +3,45 @@
 // Arithmetic contract shared with nothing but DESIGN.md §3: FP32 round-to-nearest-even, explicit
 // __fadd_rn/__fsub_rn/__fmaf_rn/__fdiv_rn in the orders written in DESIGN.md (D20), images in 8-bit
 // units (D5), zero padding (D9).  Compiled with -fmad=false so nothing else is ever contracted.
+//
+// Data layout:
+//  * float4 pyramids [slot][level-major texels] (RGB + 0) for remap inputs and packing;
+//  * packed PatchMatch operands with a zero border of kBorder texels on every side (so patch taps never
+//    need bounds checks: out-of-image taps read the border's zeros, reading D9) and an even pitch:
+//      source  SF8  (level 0, uint8 style): uint2 {G rgb u8, S rgb u8}                        8 B
+//              SF32 (otherwise):           float4 {G.r,G.g,G.b,S.r}, float4 {S.g,S.b,0,0}     32 B
+//      target  TF16 (with SF8):            uint4  {G rgb u8, aux.r, aux.g, aux.b (f32 bits)}  16 B
+//              TF32 (with SF32):           float4 {G.r,G.g,G.b,aux.r}, float4 {aux.g,aux.b,0,0} 32 B
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace fbk {
 
-// One NNF task (pair): pyramid base pointers (level 0; level k starts at +Lvl::off texels) and RNG key.
+constexpr int kBorder = 4;  // >= the largest compiled patch radius
+
+enum SrcFmt { SF8 = 0, SF32 = 1 };
+enum TgtFmt { TF16 = 0, TF32 = 1 };
+
+// One NNF task (pair).
 struct DTask {
-    const float4* sg;   // source guide pyramid  G_src
-    const float4* tg;   // target guide pyramid  G_tgt
-    const float4* ss;   // source style pyramid  S_src (nullptr for BASE)
-    float4* aux;        // aux image of this task at the current level (S^ or T-bar), h_k*w_k texels
-    uint32_t c2;        // Philox counter word 2: source frame id (D21)
-    uint32_t c3;        // Philox counter word 3: tag << 28 | target frame id (D21)
-    uint32_t pad0, pad1;
+    const char* src;   // packed source pyramid of the task's source slot (level k at +FieldArgs::src_off)
+    char* tgt;         // packed target operand of the current level (per task, or shared by a MEAN_ALIGN group)
+    const float4* ss;  // source style float4 pyramid (remap input of the S^ refresh)
+    const float4* tg;  // target guide float4 pyramid (guide half of the packed target)
+    uint32_t c2;       // Philox counter word 2: source frame id (D21)
+    uint32_t c3;       // Philox counter word 3: tag << 28 | target frame id (D21)
 };
 
-// Geometry of one pyramid level.
+// Geometry of one pyramid level (unpadded float4 pyramids).
 struct Lvl {
     int h, w;
-    long long off;  // texel offset of this level inside a pyramid
+    long long off;  // texel offset of this level inside a float4 pyramid
+};
+
+// Padded geometry of one level of the packed operands: texel (r,c) at (r+kBorder)*pitch + c+kBorder.
+struct PLvl {
+    int h, w, pitch, rows;  // rows = h + 2*kBorder
 };
 
 // Combine: out = (fma-accumulate over the ordered members of w_m * Y_m) / div, where Y_m is an image
@@ -34,46 +52,58 @@ struct DMember {
     float w;            // weight (exact powers of two, 1, -1, or the Eq. 9 weights)
 };
 struct DOut {
-    int m0, nm;   // member range
-    float div;    // IEEE divisor applied last (1 = none)
-    int fmt;      // 0: float4 [h*w] image; 1: float [h*w*3] (API layout)
+    int m0, nm;           // member range
+    float div;            // IEEE divisor applied last (1 = none)
+    int fmt;              // 0: float4 [h*w]; 1: float [h*w*3] (API layout); 2: packed TF16; 3: packed TF32
     void* out;
+    const float4* guide;  // fmt 2/3: target guide at this level (the G half of the packed target)
 };
 
 struct Rng {
     uint32_t k0, k1;  // Philox key = seed
 };
 
-// Field launch parameters.
 struct FieldArgs {
     const DTask* tasks;
     const int2* Fin;
     int2* Fout;
     float* E;
     long long fstride;  // elements per task in F/E buffers
-    Lvl L;
+    PLvl L;
+    long long src_off;  // byte offset of this level inside each packed source pyramid
     int tiles_x, tiles_per_task;
     float alpha;
     Rng rng;
     uint32_t level, iter;  // for the Philox counter (D21)
-    int rs_r0, rs_k;       // random search radius r0 and step count at this level (D13, D33)
+    int rs_r0, rs_k;       // random-search radius r0 and step count at this level (D13, D33)
+};
+
+// Packing jobs: one per (slot, level) for sources, one per task/group for BASE targets.
+struct PackSrc {
+    const uint8_t* g8;   // SF8: guide frame uint8 [H,W,3]
+    const uint8_t* s8;   // SF8: style frame uint8 [H,W,3]
+    const float4* gp;    // SF32: guide pyramid level pointer
+    const float4* sp;    // SF32: style pyramid level pointer
+    char* out;           // packed level block
 };
 
 // ---- launchers (return cudaGetLastError()) ---------------------------------------------------
 cudaError_t launch_u8_to_pyr0(const uint8_t* frames, float4* pyr, int B, int H, int W, long long pyr_stride,
                               cudaStream_t s);
 cudaError_t launch_box(float4* pyr, int B, long long pyr_stride, Lvl prev, Lvl cur, cudaStream_t s);
+cudaError_t launch_pack_src(const PackSrc* jobs, int n, int fmt, PLvl L, cudaStream_t s);
+cudaError_t launch_pack_tgt_guide(const DTask* tasks, int T, Lvl L, PLvl P, int tfmt, cudaStream_t s);
 cudaError_t launch_init(const DTask* tasks, int T, int2* F, long long fstride, Lvl L, int identity, Rng rng,
                         uint32_t level, cudaStream_t s);
 cudaError_t launch_upsample(const int2* Fc, int2* Ff, int T, long long fstride, Lvl Lc, Lvl Lf, cudaStream_t s);
-cudaError_t launch_aux_remap(const DTask* tasks, int T, const int2* F, long long fstride, Lvl L, int p,
-                             cudaStream_t s);
+cudaError_t launch_aux_remap(const DTask* tasks, int T, const int2* F, long long fstride, Lvl L, PLvl P, int p,
+                             int tfmt, cudaStream_t s);
 cudaError_t launch_combine(const DOut* outs, int n_outs, const DMember* mem, const int2* F, long long fstride,
-                           int h, int w, int p, cudaStream_t s);
+                           int h, int w, int p, int fmt, PLvl P, cudaStream_t s);
 // phase 0: E init + propagation (-1,0); 1: (+1,0); 2: (0,-1); 3: (0,+1) + all random-search steps.
-cudaError_t launch_field(const FieldArgs& a, int T, int p, int loss, int phase, cudaStream_t s);
+// fast = SF8/TF16 operands (target patch in registers); otherwise SF32/TF32 (target tile in smem).
+cudaError_t launch_field(const FieldArgs& a, int T, int p, int loss, int phase, bool fast, cudaStream_t s);
 cudaError_t launch_remap_f3(const float* src, const int2* F, float* out, int B, int H, int W, int p,
                             cudaStream_t s);
-cudaError_t launch_f4_to_f3(const float4* in, long long in_stride, float* out, int B, int npx, cudaStream_t s);
 
 }  // namespace fbk
