@@ -146,11 +146,20 @@ struct Geo {
     long long npx0() const { return (long long)H * W; }
 };
 
-fbk::PLvl padded(int h, int w)
+fbk::PLvl padded(int h, int w, int k)
 {
     const int pitch = ((w + 2 * fbk::kBorder) + 3) & ~3;  // even (texel pairs are 16-byte aligned)
-    return fbk::PLvl{h, w, pitch, h + 2 * fbk::kBorder};
+    return fbk::PLvl{h, w, pitch, h + 2 * fbk::kBorder, k};
 }
+
+// Packed source format of level k for a slot whose level-0 format is fmt0 (kernels.h): u8 styles use
+// SF8 at level 0 and the exact 16-bit integer form SF16 at levels 1..4 (values n / 4^k, n < 2^16).
+int src_fmt(int fmt0, int k)
+{
+    if (fmt0 != fbk::SF8) return fbk::SF32;
+    return k == 0 ? fbk::SF8 : (k <= 4 ? fbk::SF16 : fbk::SF32);
+}
+size_t src_bytes(int fmt) { return fmt == fbk::SF8 ? 8 : fmt == fbk::SF16 ? 16 : 32; }
 
 int level_count(int H, int W, int p, int requested)  // D6, D32
 {
@@ -177,7 +186,7 @@ Geo make_geo(const fb_match_cfg& cfg, int H, int W)
     long long off = 0;
     for (int k = 0; k < g.Lv; ++k) {
         g.L[k] = Lvl{H >> k, W >> k, off};
-        g.PL[k] = padded(H >> k, W >> k);
+        g.PL[k] = padded(H >> k, W >> k, k);
         off += (long long)(H >> k) * (W >> k);
     }
     g.pyr_texels = off;
@@ -262,7 +271,7 @@ Slots pack_sources(Exec& ex, const Geo& g, int fmt0, const std::vector<SlotSpec>
     size_t off = 0;
     for (int k = 0; k < g.Lv; ++k) {
         S.off[k] = off;
-        const size_t tb = (k == 0 && fmt0 == fbk::SF8) ? 8 : 32;
+        const size_t tb = src_bytes(src_fmt(fmt0, k));
         off = (off + (size_t)g.PL[k].rows * g.PL[k].pitch * tb + 255) & ~size_t(255);
     }
     S.stride = off;
@@ -277,7 +286,7 @@ Slots pack_sources(Exec& ex, const Geo& g, int fmt0, const std::vector<SlotSpec>
                                    sp.sp ? sp.sp + g.L[k].off : nullptr, S.base + (size_t)i * S.stride + S.off[k]};
         }
         const fbk::PackSrc* dj = ex.upload(jobs);
-        const int fmt = (k == 0 && fmt0 == fbk::SF8) ? fbk::SF8 : fbk::SF32;
+        const int fmt = src_fmt(fmt0, k);
         ex.launch("pack_src", [&] { return fbk::launch_pack_src(dj, n, fmt, g.PL[k], ex.ctx->stream); },
                   (uint64_t)n * g.PL[k].rows * g.PL[k].pitch);
     }
@@ -396,6 +405,7 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
             fbk::FieldArgs a{};
             a.tasks = d_tasks; a.E = out.E; a.fstride = n0; a.L = PL; a.src_off = (long long)slots.off[k];
             a.alpha = cfg.alpha; a.rng = rng; a.level = (uint32_t)k; a.iter = (uint32_t)it; a.rs_r0 = r0; a.rs_k = rk;
+            a.src_fmt = src_fmt(slots.fmt0, k);
             static const char* kFieldNames[4] = {"field0", "field1", "field2", "field3"};
             for (int ph = 0; ph < 4; ++ph) {
                 a.Fin = F[cur]; a.Fout = F[cur ^ 1];

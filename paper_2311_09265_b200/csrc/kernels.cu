@@ -15,6 +15,7 @@
 namespace fbk {
 
 static constexpr int TILE_X = 32, TILE_Y = 8;  // 256-thread 2D tiles: a warp is one row segment
+static constexpr int FAST_TY = 4;              // fast kernel: 128-thread tiles, 3 CTAs/SM at <= 168 regs
 static constexpr int B = kBorder;
 
 // ------------------------------------------------------------------------------------ Philox4x32-10
@@ -94,6 +95,19 @@ __global__ void k_pack_src(const PackSrc* __restrict__ jobs, int fmt, PLvl L)
                 }
             }
             reinterpret_cast<uint2*>(J.out)[i] = v;
+        } else if (fmt == SF16) {
+            // level k of a u8 pyramid: v = n / 4^k with n < 2^16 (k <= 4); store n
+            const float sc = (float)(1 << (2 * L.k));
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (in) {
+                const float4 g = J.gp[r * L.w + c];
+                const float4 s = J.sp ? J.sp[r * L.w + c] : make_float4(0.f, 0.f, 0.f, 0.f);
+                v.x = (uint32_t)(g.x * sc) | ((uint32_t)(g.y * sc) << 16);
+                v.y = (uint32_t)(g.z * sc);
+                v.z = (uint32_t)(s.x * sc) | ((uint32_t)(s.y * sc) << 16);
+                v.w = (uint32_t)(s.z * sc);
+            }
+            reinterpret_cast<uint4*>(J.out)[i] = v;
         } else {
             float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
             if (in) {
@@ -318,7 +332,7 @@ __global__ void k_remap_f3(const float* __restrict__ src, const int2* __restrict
 // byte-wise |a-b| and dp4a; it is converted once, exactly.  Style term: the FP32 chain of D20 with the
 // u8 source channel converted exactly (u8f).
 template <int P, bool TWO, int PHASE>
-__global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_fast(FieldArgs a)
+__global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
 {
     constexpr int D = 2 * P + 1;
     constexpr int NCH = (D + 2) / 2;  // 16-byte chunks (texel pairs) covering D texels at either parity
@@ -326,7 +340,7 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_fast(FieldArgs a)
     const int tile = blockIdx.x - t * a.tiles_per_task;
     const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
     const int c = tx * TILE_X + (threadIdx.x & (TILE_X - 1));
-    const int r = ty * TILE_Y + (threadIdx.x / TILE_X);
+    const int r = ty * FAST_TY + (threadIdx.x / TILE_X);
     const int h = a.L.h, w = a.L.w, pitch = a.L.pitch;
     if (r >= h || c >= w) return;
     const DTask T = a.tasks[t];
@@ -409,7 +423,14 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_fast(FieldArgs a)
 }
 
 // ---- general variant: SF32 source, TF32 target staged in shared memory (any level, P <= 4) -------
-template <int P, bool TWO, int PHASE>
+// SF16 channel: u16 lane `sel` (0x7410 low, 0x7432 high) of a word as the exact float n / 4^k, using
+// the magic 2^(23-2k) whose bit pattern is ex = (75-k) << 24: bits(ex | n) = 2^(23-2k) + n 4^-k.
+__device__ __forceinline__ float u16f(uint32_t word, uint32_t sel, uint32_t ex)
+{
+    return __fsub_rn(__uint_as_float(__byte_perm(word, ex, sel)), __uint_as_float(ex));
+}
+
+template <int P, bool TWO, int PHASE, int SFMT>
 __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
 {
     constexpr int D = 2 * P + 1, SX = TILE_X + 2 * P, SY = TILE_Y + 2 * P;
@@ -439,6 +460,8 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
     const int c = tx * TILE_X + lx, r = ty * TILE_Y + ly;
     if (r >= h || c >= w) return;
     const float4* S = reinterpret_cast<const float4*>(T.src + a.src_off);
+    const uint4* S16 = reinterpret_cast<const uint4*>(T.src + a.src_off);
+    const uint32_t ex = (uint32_t)(75 - a.L.k) << 24;
     auto loss = [&](int sr, int sc) -> float {
         float dg = 0.0f, ds = 0.0f;
 #pragma unroll
@@ -447,14 +470,22 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
             float rg = 0.0f, rs = 0.0f;
 #pragma unroll
             for (int dc = 0; dc < D; ++dc) {
-                const float4 s0 = __ldg(&S[2 * (base + dc)]);
+                float4 s0, s1;
+                if (SFMT == SF16) {
+                    const uint4 v = __ldg(&S16[base + dc]);
+                    s0 = make_float4(u16f(v.x, 0x7410u, ex), u16f(v.x, 0x7432u, ex), u16f(v.y, 0x7410u, ex),
+                                     TWO ? u16f(v.z, 0x7410u, ex) : 0.0f);
+                    s1 = TWO ? make_float4(u16f(v.z, 0x7432u, ex), u16f(v.w, 0x7410u, ex), 0.0f, 0.0f) : s0;
+                } else {
+                    s0 = __ldg(&S[2 * (base + dc)]);
+                    s1 = TWO ? __ldg(&S[2 * (base + dc) + 1]) : s0;
+                }
                 const float4 q0 = t0[ly + dr][lx + dc];
                 float dl;
                 dl = __fsub_rn(q0.x, s0.x); rg = __fmaf_rn(dl, dl, rg);
                 dl = __fsub_rn(q0.y, s0.y); rg = __fmaf_rn(dl, dl, rg);
                 dl = __fsub_rn(q0.z, s0.z); rg = __fmaf_rn(dl, dl, rg);
                 if (TWO) {
-                    const float4 s1 = __ldg(&S[2 * (base + dc) + 1]);
                     const float2 q1 = t1[ly + dr][lx + dc];
                     dl = __fsub_rn(q0.w, s0.w); rs = __fmaf_rn(dl, dl, rs);
                     dl = __fsub_rn(q1.x, s1.x); rs = __fmaf_rn(dl, dl, rs);
@@ -589,22 +620,22 @@ cudaError_t launch_remap_f3(const float* src, const int2* F, float* out, int Bn,
     return cudaGetLastError();
 }
 
-template <int P, bool TWO>
+template <int P, bool TWO, int SFMT>
 static void launch_field_gen(const FieldArgs& a, int T, int phase, cudaStream_t s)
 {
     const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(TILE_X * TILE_Y);
     switch (phase) {
-    case 0: k_field_gen<P, TWO, 0><<<grid, block, 0, s>>>(a); break;
-    case 1: k_field_gen<P, TWO, 1><<<grid, block, 0, s>>>(a); break;
-    case 2: k_field_gen<P, TWO, 2><<<grid, block, 0, s>>>(a); break;
-    default: k_field_gen<P, TWO, 3><<<grid, block, 0, s>>>(a); break;
+    case 0: k_field_gen<P, TWO, 0, SFMT><<<grid, block, 0, s>>>(a); break;
+    case 1: k_field_gen<P, TWO, 1, SFMT><<<grid, block, 0, s>>>(a); break;
+    case 2: k_field_gen<P, TWO, 2, SFMT><<<grid, block, 0, s>>>(a); break;
+    default: k_field_gen<P, TWO, 3, SFMT><<<grid, block, 0, s>>>(a); break;
     }
 }
 
 template <int P, bool TWO>
 static void launch_field_fast(const FieldArgs& a, int T, int phase, cudaStream_t s)
 {
-    const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(TILE_X * TILE_Y);
+    const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(TILE_X * FAST_TY);
     switch (phase) {
     case 0: k_field_fast<P, TWO, 0><<<grid, block, 0, s>>>(a); break;
     case 1: k_field_fast<P, TWO, 1><<<grid, block, 0, s>>>(a); break;
@@ -617,15 +648,19 @@ cudaError_t launch_field(const FieldArgs& a0, int T, int p, int loss, int phase,
 {
     FieldArgs a = a0;
     a.tiles_x = (a.L.w + TILE_X - 1) / TILE_X;
-    a.tiles_per_task = a.tiles_x * ((a.L.h + TILE_Y - 1) / TILE_Y);
+    a.tiles_per_task = a.tiles_x * ((a.L.h + (fast ? FAST_TY : TILE_Y) - 1) / (fast ? FAST_TY : TILE_Y));
     if (fast) {
         if (p == 1) { loss ? launch_field_fast<1, true>(a, T, phase, s) : launch_field_fast<1, false>(a, T, phase, s); }
         else if (p == 2) { loss ? launch_field_fast<2, true>(a, T, phase, s) : launch_field_fast<2, false>(a, T, phase, s); }
         else return cudaErrorInvalidValue;
+    } else if (a.src_fmt == SF16) {
+        if (p == 1) { loss ? launch_field_gen<1, true, SF16>(a, T, phase, s) : launch_field_gen<1, false, SF16>(a, T, phase, s); }
+        else if (p == 2) { loss ? launch_field_gen<2, true, SF16>(a, T, phase, s) : launch_field_gen<2, false, SF16>(a, T, phase, s); }
+        else return cudaErrorInvalidValue;
     } else if (loss == 0) {
-        FB_DISPATCH_P(p, (launch_field_gen<PP, false>(a, T, phase, s)));
+        FB_DISPATCH_P(p, (launch_field_gen<PP, false, SF32>(a, T, phase, s)));
     } else {
-        FB_DISPATCH_P(p, (launch_field_gen<PP, true>(a, T, phase, s)));
+        FB_DISPATCH_P(p, (launch_field_gen<PP, true, SF32>(a, T, phase, s)));
     }
     return cudaGetLastError();
 }

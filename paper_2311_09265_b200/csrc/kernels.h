@@ -9,6 +9,8 @@
 //  * packed PatchMatch operands with a zero border of kBorder texels on every side (so patch taps never
 //    need bounds checks: out-of-image taps read the border's zeros, reading D9) and an even pitch:
 //      source  SF8  (level 0, uint8 style): uint2 {G rgb u8, S rgb u8}                        8 B
+//              SF16 (levels 1..4, uint8 style): uint4 of u16 n = v * 4^k {G.r,G.g | G.b,0 |
+//                   S.r,S.g | S.b,0}; exact because level-k values are multiples of 4^-k (D6) 16 B
 //              SF32 (otherwise):           float4 {G.r,G.g,G.b,S.r}, float4 {S.g,S.b,0,0}     32 B
 //      target  TF16 (with SF8):            uint4  {G rgb u8, aux.r, aux.g, aux.b (f32 bits)}  16 B
 //              TF32 (with SF32):           float4 {G.r,G.g,G.b,aux.r}, float4 {aux.g,aux.b,0,0} 32 B
@@ -20,7 +22,7 @@ namespace fbk {
 
 constexpr int kBorder = 4;  // >= the largest compiled patch radius
 
-enum SrcFmt { SF8 = 0, SF32 = 1 };
+enum SrcFmt { SF8 = 0, SF32 = 1, SF16 = 2 };
 enum TgtFmt { TF16 = 0, TF32 = 1 };
 
 // One NNF task (pair).
@@ -42,6 +44,7 @@ struct Lvl {
 // Padded geometry of one level of the packed operands: texel (r,c) at (r+kBorder)*pitch + c+kBorder.
 struct PLvl {
     int h, w, pitch, rows;  // rows = h + 2*kBorder
+    int k;                  // pyramid level (selects the SF16 scale 4^k)
 };
 
 // Combine: out = (fma-accumulate over the ordered members of w_m * Y_m) / div, where Y_m is an image
@@ -76,6 +79,7 @@ struct FieldArgs {
     Rng rng;
     uint32_t level, iter;  // for the Philox counter (D21)
     int rs_r0, rs_k;       // random-search radius r0 and step count at this level (D13, D33)
+    int src_fmt;           // SF16 or SF32 for the general kernel
 };
 
 // Packing jobs: one per (slot, level) for sources, one per task/group for BASE targets.
