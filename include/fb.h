@@ -99,7 +99,7 @@ uint64_t fb_launch_count(fb_ctx ctx);
  * When enabled, every kernel launch of this context is bracketed by two CUDA events recorded on the
  * context stream.  fb_profile_read synchronises those events and writes up to `cap` per-kernel-class
  * entries (returns how many classes exist).  `work` is the class's algorithmic unit count summed over
- * launches: candidate evaluations for the PatchMatch field kernels ("field0".."field3"), output pixels
+ * launches: candidate evaluations for the PatchMatch field kernels ("field<phase>.L<level>"), output pixels
  * for the remap / combine kernels, texels for the pyramid kernels.  fb_profile_reset clears totals. */
 typedef struct {
     char name[32];

@@ -160,6 +160,7 @@ int src_fmt(int fmt0, int k)
     return k == 0 ? fbk::SF8 : (k <= 4 ? fbk::SF16 : fbk::SF32);
 }
 size_t src_bytes(int fmt) { return fmt == fbk::SF8 ? 8 : fmt == fbk::SF16 ? 16 : 32; }
+int src_copies(int fmt) { return fmt == fbk::SF8 ? fbk::kShift8 : fmt == fbk::SF16 ? fbk::kShift16 : 1; }
 
 int level_count(int H, int W, int p, int requested)  // D6, D32
 {
@@ -271,8 +272,8 @@ Slots pack_sources(Exec& ex, const Geo& g, int fmt0, const std::vector<SlotSpec>
     size_t off = 0;
     for (int k = 0; k < g.Lv; ++k) {
         S.off[k] = off;
-        const size_t tb = src_bytes(src_fmt(fmt0, k));
-        off = (off + (size_t)g.PL[k].rows * g.PL[k].pitch * tb + 255) & ~size_t(255);
+        const int f = src_fmt(fmt0, k);
+        off = (off + (size_t)src_copies(f) * g.PL[k].rows * g.PL[k].pitch * src_bytes(f) + 255) & ~size_t(255);
     }
     S.stride = off;
     const int n = (int)specs.size();
@@ -397,7 +398,7 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
                           (uint64_t)T * L.h * L.w);
                 if (st) st->remap_pixels += (uint64_t)T * L.h * L.w;
             } else if (per_group) {  // T-bar refresh (Eq. 7, D27)
-                ex.launch("tbar", [&] { return fbk::launch_combine(d_outs[k], (int)groups.size(), d_mem[k], F[cur], n0,
+                ex.launch(k == 0 ? "tbar.L0" : "tbar.L1+", [&] { return fbk::launch_combine(d_outs[k], (int)groups.size(), d_mem[k], F[cur], n0,
                                                                    L.h, L.w, g.p, fast ? 2 : 3, PL, s); },
                           (uint64_t)T * L.h * L.w);
                 if (st) st->remap_pixels += (uint64_t)T * L.h * L.w;
@@ -406,11 +407,12 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
             a.tasks = d_tasks; a.E = out.E; a.fstride = n0; a.L = PL; a.src_off = (long long)slots.off[k];
             a.alpha = cfg.alpha; a.rng = rng; a.level = (uint32_t)k; a.iter = (uint32_t)it; a.rs_r0 = r0; a.rs_k = rk;
             a.src_fmt = src_fmt(slots.fmt0, k);
-            static const char* kFieldNames[4] = {"field0", "field1", "field2", "field3"};
+            char names[4][32];
+            for (int ph = 0; ph < 4; ++ph) snprintf(names[ph], sizeof names[ph], "field%d.L%d", ph, k);
             for (int ph = 0; ph < 4; ++ph) {
                 a.Fin = F[cur]; a.Fout = F[cur ^ 1];
                 const uint64_t per_px = ph == 0 ? 2 : ph == 3 ? 1 + (uint64_t)rk : 1;
-                ex.launch(kFieldNames[ph], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, ph, fast, s); },
+                ex.launch(names[ph], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, ph, fast, s); },
                           per_px * (uint64_t)T * L.h * L.w);
                 cur ^= 1;
             }
