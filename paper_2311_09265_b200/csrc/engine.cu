@@ -160,7 +160,6 @@ int src_fmt(int fmt0, int k)
     return k == 0 ? fbk::SF8 : (k <= 4 ? fbk::SF16 : fbk::SF32);
 }
 size_t src_bytes(int fmt) { return fmt == fbk::SF8 ? 8 : fmt == fbk::SF16 ? 16 : 32; }
-int src_copies(int fmt) { return fmt == fbk::SF8 ? fbk::kShift8 : fmt == fbk::SF16 ? fbk::kShift16 : 1; }
 
 int level_count(int H, int W, int p, int requested)  // D6, D32
 {
@@ -273,7 +272,7 @@ Slots pack_sources(Exec& ex, const Geo& g, int fmt0, const std::vector<SlotSpec>
     for (int k = 0; k < g.Lv; ++k) {
         S.off[k] = off;
         const int f = src_fmt(fmt0, k);
-        off = (off + (size_t)src_copies(f) * g.PL[k].rows * g.PL[k].pitch * src_bytes(f) + 255) & ~size_t(255);
+        off = (off + (size_t)g.PL[k].rows * g.PL[k].pitch * src_bytes(f) + 255) & ~size_t(255);
     }
     S.stride = off;
     const int n = (int)specs.size();
