@@ -8,6 +8,7 @@
 // (Eq. 7) and what fills the 148 SMs: one launch covers every pixel of every pair.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -28,6 +29,7 @@ struct fb_ctx_s {
     size_t ws_bytes = 0;
     int64_t max_pairs = 0;
     uint64_t launches = 0;
+    bool fused = false;  // fused iteration kernel on the fast path (FB_FUSED=1; measured equal speed)
     std::string err;
     // kernel timing (fb_profile_*)
     bool prof = false;
@@ -408,6 +410,15 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
             a.src_fmt = src_fmt(slots.fmt0, k);
             char names[4][32];
             for (int ph = 0; ph < 4; ++ph) snprintf(names[ph], sizeof names[ph], "field%d.L%d", ph, k);
+            if (fast && ex.ctx->fused) {  // one fused launch per iteration
+                char nm[32];
+                snprintf(nm, sizeof nm, "iter.L%d", k);
+                a.Fin = F[cur]; a.Fout = F[cur ^ 1];
+                ex.launch(nm, [&] { return fbk::launch_iter_fast(a, T, g.p, cfg.loss, s); },
+                          (uint64_t)(5 + rk) * T * L.h * L.w);
+                cur ^= 1;
+                continue;
+            }
             for (int ph = 0; ph < 4; ++ph) {
                 a.Fin = F[cur]; a.Fout = F[cur ^ 1];
                 const uint64_t per_px = ph == 0 ? 2 : ph == 3 ? 1 + (uint64_t)rk : 1;
@@ -843,6 +854,8 @@ fb_status fb_ctx_create(int device, void* cuda_stream, fb_ctx* out)
     *out = nullptr;
     if (cudaSetDevice(device) != cudaSuccess) return FB_ERR_CUDA;
     fb_ctx c = new fb_ctx_s;
+    const char* fused = getenv("FB_FUSED");  // A/B knob: FB_FUSED=1 runs each level-0 iteration as one launch
+    if (fused && fused[0] == '1') c->fused = true;
     c->device = device;
     c->stream = static_cast<cudaStream_t>(cuda_stream);
     *out = c;

@@ -107,6 +107,9 @@ cudaError_t launch_combine(const DOut* outs, int n_outs, const DMember* mem, con
 // phase 0: E init + propagation (-1,0); 1: (+1,0); 2: (0,-1); 3: (0,+1) + all random-search steps.
 // fast = SF8/TF16 operands (target patch in registers); otherwise SF32/TF32 (target tile in smem).
 cudaError_t launch_field(const FieldArgs& a, int T, int p, int loss, int phase, bool fast, cudaStream_t s);
+// The whole updating sequence of one iteration (E init, four propagation fields, random search) in one
+// launch, fast operands only (SF8/TF16, p <= 2).  Fin -> Fout, E written.
+cudaError_t launch_iter_fast(const FieldArgs& a, int T, int p, int loss, cudaStream_t s);
 cudaError_t launch_remap_f3(const float* src, const int2* F, float* out, int B, int H, int W, int p,
                             cudaStream_t s);
 
