@@ -92,6 +92,9 @@ fb_status fb_set_max_batch_pairs(fb_ctx ctx, int64_t max_pairs);
 /* Workspace bytes an operation needs.  op = fb_op; n = B pairs (FB_OP_NNF) or N frames; M = window
  * half-width (blend) or number of keyframes K (interpolate).  Returns 0 on invalid arguments. */
 size_t fb_workspace_size(fb_ctx ctx, int op, const fb_match_cfg* cfg, int n, int H, int W, int M);
+/* Workspace bytes of one fb_blend_window_range call (same arguments; 0 on invalid arguments). */
+size_t fb_workspace_size_range(fb_ctx ctx, int schedule, const fb_match_cfg* cfg, int N_total, int f0, int N, int H,
+                               int W, int M, int t0, int t1);
 /* Number of kernels this context has launched so far (for launch accounting in bench.py). */
 uint64_t fb_launch_count(fb_ctx ctx);
 

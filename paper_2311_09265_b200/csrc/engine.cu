@@ -1022,6 +1022,21 @@ fb_status fb_interpolate_keyframes(fb_ctx ctx, const fb_match_cfg* cfg, int N, i
     });
 }
 
+size_t fb_workspace_size_range(fb_ctx ctx, int schedule, const fb_match_cfg* cfg, int N_total, int f0, int N, int H,
+                               int W, int M, int t0, int t1)
+{
+    if (!ctx || !cfg) return 0;
+    size_t need = 0;
+    const uint8_t* fake = reinterpret_cast<const uint8_t*>(16);  // dry run: pointers are never dereferenced
+    float* fout = reinterpret_cast<float*>(16);
+    std::string saved = ctx->err;
+    const fb_status s = guarded(ctx, nullptr, [&](Exec& ex, fb_stats* st) {
+        blend_range_body(ex, st, cfg, schedule, N_total, f0, N, H, W, M, fake, fake, t0, t1, fout);
+    }, &need);
+    ctx->err = saved;
+    return s == FB_OK ? std::max<size_t>(need, 256) : 0;
+}
+
 size_t fb_workspace_size(fb_ctx ctx, int op, const fb_match_cfg* cfg, int n, int H, int W, int M)
 {
     if (!ctx || !cfg || n < 1 || H < 1 || W < 1) return 0;

@@ -25,7 +25,7 @@ STATUS = {0: "FB_OK", 1: "FB_ERR_INVALID_ARG", 2: "FB_ERR_SHAPE", 3: "FB_ERR_CUD
           5: "FB_ERR_WORKSPACE", 6: "FB_ERR_UNSUPPORTED"}
 
 SYMBOLS = ["fb_ctx_create", "fb_ctx_destroy", "fb_last_error", "fb_set_workspace", "fb_set_max_batch_pairs",
-           "fb_workspace_size", "fb_launch_count", "fb_pyramid_elems", "fb_build_pyramid", "fb_nnf_estimate",
+           "fb_workspace_size", "fb_workspace_size_range", "fb_launch_count", "fb_pyramid_elems", "fb_build_pyramid", "fb_nnf_estimate",
            "fb_remap", "fb_blend_window", "fb_blend_window_range", "fb_interpolate_keyframes", "fb_profile_enable",
            "fb_profile_read", "fb_profile_reset"]
 
@@ -101,6 +101,8 @@ def load_library(build_if_missing: bool = True):
     lib.fb_set_max_batch_pairs.argtypes = [V, C.c_int64]
     lib.fb_workspace_size.argtypes = [V, C.c_int, P(_Cfg), C.c_int, C.c_int, C.c_int, C.c_int]
     lib.fb_workspace_size.restype = C.c_size_t
+    lib.fb_workspace_size_range.argtypes = [V, C.c_int, P(_Cfg)] + [C.c_int] * 8
+    lib.fb_workspace_size_range.restype = C.c_size_t
     lib.fb_launch_count.argtypes = [V]
     lib.fb_launch_count.restype = C.c_uint64
     lib.fb_pyramid_elems.argtypes = [C.c_int] * 4
@@ -262,9 +264,9 @@ class Context:
         g = _dev(guide, self.device, torch.uint8)
         s = _dev(style, self.device, torch.uint8)
         N, H, W, _ = g.shape
-        op = OP_BLEND_TREE if schedule == TREE else OP_BLEND_DIRECT
-        # the full-video plan bounds any shard's workspace
-        self.ensure_workspace(self.workspace_size(op, cfg, N_total, H, W, M))
+        c0 = cfg.c()
+        self.ensure_workspace(int(self.lib.fb_workspace_size_range(self.h, schedule, C.byref(c0), N_total, f0, N, H, W, M,
+                                                                   t0, t1)))
         if out is None:
             out = torch.empty((t1 - t0, H, W, 3), dtype=torch.float32, device=self.device)
         st = _Stats()

@@ -1,0 +1,80 @@
+"""Multi-GPU host logic on CPU: the pair-balanced shard plan and the halo exchange (gloo, world 2-3)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2311_09265_b200 import shard
+
+
+def direct_cost(N, M, a, b):
+    return sum(shard.direct_pairs(N, M, i) for i in range(a, b))
+
+
+@pytest.mark.parametrize("N,M,world", [(200, 15, 1), (200, 15, 2), (200, 15, 8), (1000, 15, 8), (200, 30, 8),
+                                       (7, 3, 8), (9, 0, 4), (1, 5, 2)])
+def test_plan_is_contiguous_covering_and_balanced(N, M, world):
+    plan = shard.plan_shards(N, M, world)
+    assert len(plan) == world
+    assert plan[0][0] == 0 and plan[-1][1] == N
+    for (a, b), (c, d) in zip(plan, plan[1:]):
+        assert b == c and a <= b
+    if N >= world:
+        assert all(b > a for a, b in plan)
+    if N >= 8 * world and M > 0:
+        costs = [direct_cost(N, M, a, b) for a, b in plan]
+        assert min(costs) / max(costs) >= 0.9, costs
+
+
+def test_halo_ranges_cover_every_window():
+    N, M = 50, 7
+    plan = shard.plan_shards(N, M, 4)
+    for t0, t1 in plan:
+        f0, f1 = shard.halo_range(N, M, t0, t1)
+        for i in range(t0, t1):
+            assert f0 <= max(0, i - M) and min(N, i + M + 1) <= f1
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, N, M, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(5)
+        full_g = torch.from_numpy(rng.integers(0, 256, size=(N, 6, 7, 3), dtype=np.uint8))
+        full_s = torch.from_numpy(rng.integers(0, 256, size=(N, 6, 7, 3), dtype=np.uint8))
+        plan = shard.plan_shards(N, M, world)
+        t0, t1 = plan[rank]
+        (g_loc, s_loc), f0 = shard.halo_exchange([full_g[t0:t1].clone(), full_s[t0:t1].clone()], plan, N, M, rank)
+        f1 = f0 + g_loc.shape[0]
+        ok = (f0, f1) == shard.halo_range(N, M, t0, t1) and torch.equal(g_loc, full_g[f0:f1]) and \
+            torch.equal(s_loc, full_s[f0:f1])
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,N,M", [(2, 20, 3), (3, 12, 6), (2, 5, 9)])
+def test_halo_exchange_gloo(world, N, M):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, N, M, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    res = dict(q.get(timeout=5) for _ in range(world))
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(res[r] for r in range(world)), res
