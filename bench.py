@@ -59,6 +59,16 @@ def flops_per_eval(p: int, loss: int) -> int:
     return terms * (2 * p + 1) ** 2 * 3 * 3
 
 
+L1_BYTES_PER_CLK = 128    # L1/shared data path per SM (B300_MICROARCH.md: smem crossbar 128 B/cyc/SM)
+
+
+def gathered_bytes_per_eval(p: int, loss: int) -> int:
+    """Algorithmic gathered source bytes of one evaluation: (2p+1)^2 taps x 3 channels x
+    4 B per source image read (guide, plus style for the two-term losses)."""
+    terms = 1 if loss == 0 else 2
+    return terms * (2 * p + 1) ** 2 * 3 * 4
+
+
 class ClockSampler:
     """Samples nvidia-smi clocks / throttle reasons every 200 ms while the timed region runs."""
     FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
@@ -288,13 +298,14 @@ def main():
 
     # ---- roofline of the dominant kernel class
     dom = max(prof, key=lambda k: prof[k]["ms"]) if prof else None
-    roof = None
+    roof = roof_l1 = None
     if dom:
         d = prof[dom]
         sec = d["ms"] / 1e3
         total_ms = sum(v["ms"] for v in prof.values())
-        if dom.startswith("field"):
+        if dom.startswith("field") or dom.startswith("iter"):
             fpe = flops_per_eval(wl["p"], cfg.loss)
+            bpe = gathered_bytes_per_eval(wl["p"], cfg.loss)
             achieved = d["work"] * fpe / sec / 1e12
             peak = SMS * FP32_LANES_PER_SM * 2 * SM_MAX_MHZ * 1e6 / 1e12
             roof = {"kernel": f"pm_{dom}", "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -302,6 +313,11 @@ def main():
                     "peak_basis": "FP32: 148 SMs x 128 lanes x 2 flop x 1965 MHz (guide unit counts, max clock)",
                     "flops_per_eval": fpe, "evals_per_launch": d["work"] / max(d["launches"], 1),
                     "avg_launch_ms": d["ms"] / max(d["launches"], 1), "share_of_kernel_time": d["ms"] / total_ms}
+            achieved_l1 = d["work"] * bpe / sec / 1e9
+            peak_l1 = SMS * L1_BYTES_PER_CLK * SM_MAX_MHZ * 1e6 / 1e9
+            roof_l1 = {"kernel": f"pm_{dom}", "bound": "l1", "achieved": achieved_l1, "peak": peak_l1, "unit": "GB/s",
+                       "frac": achieved_l1 / peak_l1, "bytes_per_eval": bpe,
+                       "peak_basis": "L1/shared data path: 148 SMs x 128 B/clk x 1965 MHz (SURVEY 8(d) binding ceiling)"}
         traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if roof and os.path.exists(traffic_file):
             try:
@@ -338,7 +354,7 @@ def main():
                    "nnf_pairs_per_step": pairs_step, "evals_per_step": evals_step,
                    "launches_per_step": launches / args.steps},
         "evals_per_s": evals_step / (ms / 1e3),
-        "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "roofline": roof, "roofline_l1": roof_l1, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
