@@ -326,6 +326,19 @@ __global__ void k_remap_f3(const float* __restrict__ src, const int2* __restrict
 // Loss (Eq. 1 / Eq. 3 / Eq. 8): D = sum over rows dr of rho_dr, rho_dr = fma chain over dc then
 // channel of (target - source)^2 (D20); two-term losses return fma(alpha, D_guide, D_style).
 
+// Partial-distance elimination stages: rows [0,S1) then a bound check, rows [S1,S2) and a second check
+// (skipped when S2 >= 2P+1), then the remaining rows.  Tuned on B200 (N=48 accurate proxy): the
+// register-target kernel is best with one check after the first row, the smem-target kernel with
+// checks after rows 1 and 3 (profiles/r01_pde_tuning.txt).
+#define PDE_FAST_S1(P) 1
+#define PDE_FAST_S2(P) (2 * (P) + 1)
+#define PDE_GEN_S1(P) 1
+#define PDE_GEN_S2(P) 3
+__device__ __forceinline__ float partial_loss(float alpha, float dg, float ds, bool two)
+{
+    return two ? __fmaf_rn(alpha, dg, ds) : dg;
+}
+
 // ---- fast variant: SF8 source, TF16 target, target patch in registers (P <= 2) -------------------
 // Guide term: at level 0 every guide value is an integer 0..255, every partial sum of the FP32 chain
 // is an integer below 2^24 (p <= 4), so the chain is exact and equals the integer SSD computed with
@@ -358,51 +371,66 @@ __global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
             tgA[dr][dc][1] = __uint_as_float(v.z);
             tgA[dr][dc][2] = __uint_as_float(v.w);
         }
-    auto loss = [&](int sr, int sc) -> float {
-        uint32_t dg = 0u;
-        float ds = 0.0f;
+    // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
+    auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
+        const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
+        const int o = idx & 1;
+        const uint4* cp = reinterpret_cast<const uint4*>(S + (idx - o));
+        uint32_t wd[4 * NCH];
 #pragma unroll
-        for (int dr = 0; dr < D; ++dr) {
-            const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
-            const int o = idx & 1;
-            const uint4* cp = reinterpret_cast<const uint4*>(S + (idx - o));
-            uint32_t wd[4 * NCH];
+        for (int k = 0; k < NCH; ++k) {
+            const uint4 v = __ldg(cp + k);
+            wd[4 * k] = v.x; wd[4 * k + 1] = v.y; wd[4 * k + 2] = v.z; wd[4 * k + 3] = v.w;
+        }
+        float rs = 0.0f;
 #pragma unroll
-            for (int k = 0; k < NCH; ++k) {
-                const uint4 v = __ldg(cp + k);
-                wd[4 * k] = v.x; wd[4 * k + 1] = v.y; wd[4 * k + 2] = v.z; wd[4 * k + 3] = v.w;
-            }
-            float rs = 0.0f;
+        for (int j = 0; j < D; ++j) {
+            const uint32_t g = o ? wd[2 * j + 2] : wd[2 * j];
+            const uint32_t d = __vabsdiffu4(g, tgG[dr][j]);
+            dg = __dp4a(d, d, dg);
+            if (TWO) {
+                const uint32_t s = o ? wd[2 * j + 3] : wd[2 * j + 1];
 #pragma unroll
-            for (int j = 0; j < D; ++j) {
-                const uint32_t g = o ? wd[2 * j + 2] : wd[2 * j];
-                const uint32_t d = __vabsdiffu4(g, tgG[dr][j]);
-                dg = __dp4a(d, d, dg);
-                if (TWO) {
-                    const uint32_t s = o ? wd[2 * j + 3] : wd[2 * j + 1];
-#pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) {
-                        const float dl = __fsub_rn(tgA[dr][j][ch], u8f(s, ch));
-                        rs = __fmaf_rn(dl, dl, rs);
-                    }
+                for (int ch = 0; ch < 3; ++ch) {
+                    const float dl = __fsub_rn(tgA[dr][j][ch], u8f(s, ch));
+                    rs = __fmaf_rn(dl, dl, rs);
                 }
             }
-            if (TWO) ds = __fadd_rn(ds, rs);
         }
+        if (TWO) ds = __fadd_rn(ds, rs);
+    };
+    // Loss with partial-distance elimination: every term is >= 0 and round-to-nearest sums are
+    // monotone, so once the partial loss after the first P rows is >= `bound` the full loss is too and
+    // the candidate cannot win the strict select (D16); its remaining rows are never loaded.  Results
+    // are unchanged: selected candidates are always evaluated in full, in the D20 order.
+    auto loss = [&](int sr, int sc, float bound) -> float {
+        uint32_t dg = 0u;
+        float ds = 0.0f;
+        constexpr int S1 = PDE_FAST_S1(P), S2 = PDE_FAST_S2(P);
+#pragma unroll
+        for (int dr = 0; dr < S1; ++dr) row(sr, sc, dr, dg, ds);
+        if (partial_loss(a.alpha, __uint2float_rn(dg), ds, TWO) >= bound) return __int_as_float(0x7f800000);
+        if (S2 < D) {
+#pragma unroll
+            for (int dr = S1; dr < S2; ++dr) row(sr, sc, dr, dg, ds);
+            if (partial_loss(a.alpha, __uint2float_rn(dg), ds, TWO) >= bound) return __int_as_float(0x7f800000);
+        }
+#pragma unroll
+        for (int dr = (S2 < D ? S2 : S1); dr < D; ++dr) row(sr, sc, dr, dg, ds);
         const float fg = __uint2float_rn(dg);
         return TWO ? __fmaf_rn(a.alpha, fg, ds) : fg;
     };
     const int2* Fi = a.Fin + t * a.fstride;
     const int i = r * w + c;
     int2 f = Fi[i];
-    float e = PHASE == 0 ? loss(f.x, f.y) : a.E[t * a.fstride + i];
+    float e = PHASE == 0 ? loss(f.x, f.y, __int_as_float(0x7f800000)) : a.E[t * a.fstride + i];
     {
         constexpr int dx = PHASE == 0 ? -1 : (PHASE == 1 ? 1 : 0);
         constexpr int dy = PHASE == 2 ? -1 : (PHASE == 3 ? 1 : 0);
         const int nr = clampi(r + dx, 0, h - 1), nc = clampi(c + dy, 0, w - 1);  // D11
         const int2 fn = Fi[nr * w + nc];
         const int sr = clampi(fn.x - dx, 0, h - 1), sc = clampi(fn.y - dy, 0, w - 1);  // D10
-        const float e2 = loss(sr, sc);
+        const float e2 = loss(sr, sc, e);
         if (e2 < e) { f = make_int2(sr, sc); e = e2; }
     }
     if (PHASE == 3) {
@@ -414,7 +442,7 @@ __global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
             const uint32_t span = 2u * (uint32_t)R + 1u;
             const int ox = (int)__umulhi(u.x, span) - R, oy = (int)__umulhi(u.y, span) - R;
             const int sr = clampi(f.x + ox, 0, h - 1), sc = clampi(f.y + oy, 0, w - 1);
-            const float e2 = loss(sr, sc);
+            const float e2 = loss(sr, sc, e);
             if (e2 < e) { f = make_int2(sr, sc); e = e2; }
         }
     }
@@ -431,9 +459,12 @@ __global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
 // recompute exactly the fields their interior neighbours read, so every interior pixel sees the same
 // Jacobi inputs as in the four-launch form and the results are identical.
 static constexpr int IT_TX = 30, IT_TY = 4;
+#ifndef IT_MINB
+#define IT_MINB 2
+#endif
 
 template <int P, bool TWO>
-__global__ void __launch_bounds__(32 * (IT_TY + 1), 2) k_iter_fast(FieldArgs a)
+__global__ void __launch_bounds__(32 * (IT_TY + 1), IT_MINB) k_iter_fast(FieldArgs a)
 {
     constexpr int D = 2 * P + 1;
     constexpr int NCH = (D + 2) / 2;
@@ -462,42 +493,57 @@ __global__ void __launch_bounds__(32 * (IT_TY + 1), 2) k_iter_fast(FieldArgs a)
                 tgA[dr][dc][2] = __uint_as_float(v.w);
             }
     }
-    auto loss = [&](int sr, int sc) -> float {
-        uint32_t dg = 0u;
-        float ds = 0.0f;
+    // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
+    auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
+        const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
+        const int o = idx & 1;
+        const uint4* cp = reinterpret_cast<const uint4*>(S + (idx - o));
+        uint32_t wd[4 * NCH];
 #pragma unroll
-        for (int dr = 0; dr < D; ++dr) {
-            const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
-            const int o = idx & 1;
-            const uint4* cp = reinterpret_cast<const uint4*>(S + (idx - o));
-            uint32_t wd[4 * NCH];
+        for (int k = 0; k < NCH; ++k) {
+            const uint4 v = __ldg(cp + k);
+            wd[4 * k] = v.x; wd[4 * k + 1] = v.y; wd[4 * k + 2] = v.z; wd[4 * k + 3] = v.w;
+        }
+        float rs = 0.0f;
 #pragma unroll
-            for (int k = 0; k < NCH; ++k) {
-                const uint4 v = __ldg(cp + k);
-                wd[4 * k] = v.x; wd[4 * k + 1] = v.y; wd[4 * k + 2] = v.z; wd[4 * k + 3] = v.w;
-            }
-            float rs = 0.0f;
+        for (int j = 0; j < D; ++j) {
+            const uint32_t g = o ? wd[2 * j + 2] : wd[2 * j];
+            const uint32_t d = __vabsdiffu4(g, tgG[dr][j]);
+            dg = __dp4a(d, d, dg);
+            if (TWO) {
+                const uint32_t sv = o ? wd[2 * j + 3] : wd[2 * j + 1];
 #pragma unroll
-            for (int j = 0; j < D; ++j) {
-                const uint32_t g = o ? wd[2 * j + 2] : wd[2 * j];
-                const uint32_t d = __vabsdiffu4(g, tgG[dr][j]);
-                dg = __dp4a(d, d, dg);
-                if (TWO) {
-                    const uint32_t sv = o ? wd[2 * j + 3] : wd[2 * j + 1];
-#pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) {
-                        const float dl = __fsub_rn(tgA[dr][j][ch], u8f(sv, ch));
-                        rs = __fmaf_rn(dl, dl, rs);
-                    }
+                for (int ch = 0; ch < 3; ++ch) {
+                    const float dl = __fsub_rn(tgA[dr][j][ch], u8f(sv, ch));
+                    rs = __fmaf_rn(dl, dl, rs);
                 }
             }
-            if (TWO) ds = __fadd_rn(ds, rs);
         }
+        if (TWO) ds = __fadd_rn(ds, rs);
+    };
+    // Loss with partial-distance elimination: every term is >= 0 and round-to-nearest sums are
+    // monotone, so once the partial loss after the first P rows is >= `bound` the full loss is too and
+    // the candidate cannot win the strict select (D16); its remaining rows are never loaded.  Results
+    // are unchanged: selected candidates are always evaluated in full, in the D20 order.
+    auto loss = [&](int sr, int sc, float bound) -> float {
+        uint32_t dg = 0u;
+        float ds = 0.0f;
+        constexpr int S1 = PDE_FAST_S1(P), S2 = PDE_FAST_S2(P);
+#pragma unroll
+        for (int dr = 0; dr < S1; ++dr) row(sr, sc, dr, dg, ds);
+        if (partial_loss(a.alpha, __uint2float_rn(dg), ds, TWO) >= bound) return __int_as_float(0x7f800000);
+        if (S2 < D) {
+#pragma unroll
+            for (int dr = S1; dr < S2; ++dr) row(sr, sc, dr, dg, ds);
+            if (partial_loss(a.alpha, __uint2float_rn(dg), ds, TWO) >= bound) return __int_as_float(0x7f800000);
+        }
+#pragma unroll
+        for (int dr = (S2 < D ? S2 : S1); dr < D; ++dr) row(sr, sc, dr, dg, ds);
         const float fg = __uint2float_rn(dg);
         return TWO ? __fmaf_rn(a.alpha, fg, ds) : fg;
     };
     auto select = [&](int2& f, float& e, int sr, int sc) {
-        const float e2 = loss(sr, sc);
+        const float e2 = loss(sr, sc, e);
         if (e2 < e) { f = make_int2(sr, sc); e = e2; }
     };
     const int2* Fi = a.Fin + t * a.fstride;
@@ -507,7 +553,7 @@ __global__ void __launch_bounds__(32 * (IT_TY + 1), 2) k_iter_fast(FieldArgs a)
     // E <- L(F) and field 0: d = (-1,0), neighbour (r-1, c) of F_in (clamped, D11)
     if (valid) {
         f = Fi[i];
-        e = loss(f.x, f.y);
+        e = loss(f.x, f.y, __int_as_float(0x7f800000));
         const int2 fn = r > 0 ? Fi[i - w] : f;
         select(f, e, min(fn.x + 1, h - 1), fn.y);
     }
@@ -587,52 +633,63 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
     const float4* S = reinterpret_cast<const float4*>(T.src + a.src_off);
     const uint4* S16 = reinterpret_cast<const uint4*>(T.src + a.src_off);
     const uint32_t ex = (uint32_t)(75 - a.L.k) << 24;
-    auto loss = [&](int sr, int sc) -> float {
-        float dg = 0.0f, ds = 0.0f;
+    auto row = [&](int sr, int sc, int dr, float& dg, float& ds) {
+        const int base = (sr + dr - P + B) * pitch + (sc - P + B);
+        float rg = 0.0f, rs = 0.0f;
 #pragma unroll
-        for (int dr = 0; dr < D; ++dr) {
-            const int base = (sr + dr - P + B) * pitch + (sc - P + B);
-            float rg = 0.0f, rs = 0.0f;
-#pragma unroll
-            for (int dc = 0; dc < D; ++dc) {
-                float4 s0, s1;
-                if (SFMT == SF16) {
-                    const uint4 v = __ldg(&S16[base + dc]);
-                    s0 = make_float4(u16f(v.x, 0x7410u, ex), u16f(v.x, 0x7432u, ex), u16f(v.y, 0x7410u, ex),
-                                     TWO ? u16f(v.z, 0x7410u, ex) : 0.0f);
-                    s1 = TWO ? make_float4(u16f(v.z, 0x7432u, ex), u16f(v.w, 0x7410u, ex), 0.0f, 0.0f) : s0;
-                } else {
-                    s0 = __ldg(&S[2 * (base + dc)]);
-                    s1 = TWO ? __ldg(&S[2 * (base + dc) + 1]) : s0;
-                }
-                const float4 q0 = t0[ly + dr][lx + dc];
-                float dl;
-                dl = __fsub_rn(q0.x, s0.x); rg = __fmaf_rn(dl, dl, rg);
-                dl = __fsub_rn(q0.y, s0.y); rg = __fmaf_rn(dl, dl, rg);
-                dl = __fsub_rn(q0.z, s0.z); rg = __fmaf_rn(dl, dl, rg);
-                if (TWO) {
-                    const float2 q1 = t1[ly + dr][lx + dc];
-                    dl = __fsub_rn(q0.w, s0.w); rs = __fmaf_rn(dl, dl, rs);
-                    dl = __fsub_rn(q1.x, s1.x); rs = __fmaf_rn(dl, dl, rs);
-                    dl = __fsub_rn(q1.y, s1.y); rs = __fmaf_rn(dl, dl, rs);
-                }
+        for (int dc = 0; dc < D; ++dc) {
+            float4 s0, s1;
+            if (SFMT == SF16) {
+                const uint4 v = __ldg(&S16[base + dc]);
+                s0 = make_float4(u16f(v.x, 0x7410u, ex), u16f(v.x, 0x7432u, ex), u16f(v.y, 0x7410u, ex),
+                                 TWO ? u16f(v.z, 0x7410u, ex) : 0.0f);
+                s1 = TWO ? make_float4(u16f(v.z, 0x7432u, ex), u16f(v.w, 0x7410u, ex), 0.0f, 0.0f) : s0;
+            } else {
+                s0 = __ldg(&S[2 * (base + dc)]);
+                s1 = TWO ? __ldg(&S[2 * (base + dc) + 1]) : s0;
             }
-            dg = __fadd_rn(dg, rg);
-            if (TWO) ds = __fadd_rn(ds, rs);
+            const float4 q0 = t0[ly + dr][lx + dc];
+            float dl;
+            dl = __fsub_rn(q0.x, s0.x); rg = __fmaf_rn(dl, dl, rg);
+            dl = __fsub_rn(q0.y, s0.y); rg = __fmaf_rn(dl, dl, rg);
+            dl = __fsub_rn(q0.z, s0.z); rg = __fmaf_rn(dl, dl, rg);
+            if (TWO) {
+                const float2 q1 = t1[ly + dr][lx + dc];
+                dl = __fsub_rn(q0.w, s0.w); rs = __fmaf_rn(dl, dl, rs);
+                dl = __fsub_rn(q1.x, s1.x); rs = __fmaf_rn(dl, dl, rs);
+                dl = __fsub_rn(q1.y, s1.y); rs = __fmaf_rn(dl, dl, rs);
+            }
         }
+        dg = __fadd_rn(dg, rg);
+        if (TWO) ds = __fadd_rn(ds, rs);
+    };
+    // Partial-distance elimination (see k_field_fast): monotone FP32 partial sums of non-negative terms.
+    auto loss = [&](int sr, int sc, float bound) -> float {
+        float dg = 0.0f, ds = 0.0f;
+        constexpr int S1 = PDE_GEN_S1(P), S2 = PDE_GEN_S2(P);
+#pragma unroll
+        for (int dr = 0; dr < S1; ++dr) row(sr, sc, dr, dg, ds);
+        if (partial_loss(a.alpha, dg, ds, TWO) >= bound) return __int_as_float(0x7f800000);
+        if (S2 < D) {
+#pragma unroll
+            for (int dr = S1; dr < S2; ++dr) row(sr, sc, dr, dg, ds);
+            if (partial_loss(a.alpha, dg, ds, TWO) >= bound) return __int_as_float(0x7f800000);
+        }
+#pragma unroll
+        for (int dr = (S2 < D ? S2 : S1); dr < D; ++dr) row(sr, sc, dr, dg, ds);
         return TWO ? __fmaf_rn(a.alpha, dg, ds) : dg;
     };
     const int2* Fi = a.Fin + t * a.fstride;
     const int i = r * w + c;
     int2 f = Fi[i];
-    float e = PHASE == 0 ? loss(f.x, f.y) : a.E[t * a.fstride + i];
+    float e = PHASE == 0 ? loss(f.x, f.y, __int_as_float(0x7f800000)) : a.E[t * a.fstride + i];
     {
         constexpr int dx = PHASE == 0 ? -1 : (PHASE == 1 ? 1 : 0);
         constexpr int dy = PHASE == 2 ? -1 : (PHASE == 3 ? 1 : 0);
         const int nr = clampi(r + dx, 0, h - 1), nc = clampi(c + dy, 0, w - 1);  // D11
         const int2 fn = Fi[nr * w + nc];
         const int sr = clampi(fn.x - dx, 0, h - 1), sc = clampi(fn.y - dy, 0, w - 1);  // D10
-        const float e2 = loss(sr, sc);
+        const float e2 = loss(sr, sc, e);
         if (e2 < e) { f = make_int2(sr, sc); e = e2; }
     }
     if (PHASE == 3) {
@@ -644,7 +701,7 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
             const uint32_t span = 2u * (uint32_t)R + 1u;
             const int ox = (int)__umulhi(u.x, span) - R, oy = (int)__umulhi(u.y, span) - R;
             const int sr = clampi(f.x + ox, 0, h - 1), sc = clampi(f.y + oy, 0, w - 1);
-            const float e2 = loss(sr, sc);
+            const float e2 = loss(sr, sc, e);
             if (e2 < e) { f = make_int2(sr, sc); e = e2; }
         }
     }

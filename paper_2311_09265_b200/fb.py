@@ -85,8 +85,8 @@ def load_library(build_if_missing: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
-    if build_if_missing and _build.needs_build():
+    path = os.environ.get("FB_LIB", _build.LIB)  # FB_LIB: development A/B of alternative builds
+    if path == _build.LIB and build_if_missing and _build.needs_build():
         _build.build_library()
     if not os.path.exists(path):
         raise RuntimeError(f"libfastblend.so not found at {path}; run __graft_entry__.build()")
