@@ -29,7 +29,8 @@ struct fb_ctx_s {
     size_t ws_bytes = 0;
     int64_t max_pairs = 0;
     uint64_t launches = 0;
-    bool fused = false;  // fused iteration kernel on the fast path (FB_FUSED=1; measured equal speed)
+    bool fused = false;  // fused iteration kernel on the fast path (FB_FUSED=1; measured slower)
+    bool fuse13 = true;  // fields 1-3 + random search fused on the fast path (FB_FUSE13=0 disables)
     std::string err;
     // kernel timing (fb_profile_*)
     bool prof = false;
@@ -416,6 +417,19 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
                 a.Fin = F[cur]; a.Fout = F[cur ^ 1];
                 ex.launch(nm, [&] { return fbk::launch_iter_fast(a, T, g.p, cfg.loss, s); },
                           (uint64_t)(5 + rk) * T * L.h * L.w);
+                cur ^= 1;
+                continue;
+            }
+            if (fast && ex.ctx->fuse13) {  // field 0, then fields 1-3 + random search in one launch
+                a.Fin = F[cur]; a.Fout = F[cur ^ 1];
+                ex.launch(names[0], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, 0, fast, s); },
+                          2ull * T * L.h * L.w);
+                cur ^= 1;
+                char nm[32];
+                snprintf(nm, sizeof nm, "field123.L%d", k);
+                a.Fin = F[cur]; a.Fout = F[cur ^ 1];
+                ex.launch(nm, [&] { return fbk::launch_iter13_fast(a, T, g.p, cfg.loss, s); },
+                          (uint64_t)(3 + rk) * T * L.h * L.w);
                 cur ^= 1;
                 continue;
             }
@@ -856,6 +870,8 @@ fb_status fb_ctx_create(int device, void* cuda_stream, fb_ctx* out)
     fb_ctx c = new fb_ctx_s;
     const char* fused = getenv("FB_FUSED");  // A/B knob: FB_FUSED=1 runs each level-0 iteration as one launch
     if (fused && fused[0] == '1') c->fused = true;
+    const char* f13 = getenv("FB_FUSE13");
+    if (f13 && f13[0] == '0') c->fuse13 = false;
     c->device = device;
     c->stream = static_cast<cudaStream_t>(cuda_stream);
     *out = c;

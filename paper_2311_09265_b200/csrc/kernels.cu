@@ -593,6 +593,135 @@ __global__ void __launch_bounds__(32 * (IT_TY + 1), IT_MINB) k_iter_fast(FieldAr
     a.E[t * a.fstride + i] = e;
 }
 
+// ---- fields 1-3 + random search in one launch (fast operands) --------------------------------------
+// Field 0 (E init and d = (-1,0)) runs as k_field_fast<PHASE 0>; this kernel then chains field 1
+// (reads the row below from that launch's output), field 2 (left neighbour's field-1 result by shuffle)
+// and field 3 (right neighbour's field-2 result by shuffle) and the random search.  Lanes 0 and 31 of
+// each warp are halo columns that recompute the fields their interior neighbours read, so the interior
+// pixels see exactly the Jacobi inputs of the per-field launches.  No shared memory, no barrier.
+static constexpr int I13_TY = 4;
+
+template <int P, bool TWO>
+__global__ void __launch_bounds__(32 * I13_TY, 3) k_iter13_fast(FieldArgs a)
+{
+    constexpr int D = 2 * P + 1;
+    constexpr int NCH = (D + 2) / 2;
+    const int t = blockIdx.x / a.tiles_per_task;
+    const int tile = blockIdx.x - t * a.tiles_per_task;
+    const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+    const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
+    const int c = tx * IT_TX - 1 + lane, r = ty * I13_TY + wy;
+    const int h = a.L.h, w = a.L.w, pitch = a.L.pitch;
+    const bool valid = (unsigned)r < (unsigned)h && (unsigned)c < (unsigned)w;
+    const DTask T = a.tasks[t];
+    const uint2* S = reinterpret_cast<const uint2*>(T.src + a.src_off);
+    const uint4* Tt = reinterpret_cast<const uint4*>(T.tgt);
+    uint32_t tgG[D][D];
+    float tgA[D][D][3];
+    if (valid) {
+#pragma unroll
+        for (int dr = 0; dr < D; ++dr)
+#pragma unroll
+            for (int dc = 0; dc < D; ++dc) {
+                const uint4 v = __ldg(&Tt[(r + dr - P + B) * pitch + (c + dc - P + B)]);
+                tgG[dr][dc] = v.x;
+                tgA[dr][dc][0] = __uint_as_float(v.y);
+                tgA[dr][dc][1] = __uint_as_float(v.z);
+                tgA[dr][dc][2] = __uint_as_float(v.w);
+            }
+    }
+    // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
+    auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
+        const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
+        const int o = idx & 1;
+        const uint4* cp = reinterpret_cast<const uint4*>(S + (idx - o));
+        uint32_t wd[4 * NCH];
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+            const uint4 v = __ldg(cp + k);
+            wd[4 * k] = v.x; wd[4 * k + 1] = v.y; wd[4 * k + 2] = v.z; wd[4 * k + 3] = v.w;
+        }
+        float rs = 0.0f;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const uint32_t g = o ? wd[2 * j + 2] : wd[2 * j];
+            const uint32_t d = __vabsdiffu4(g, tgG[dr][j]);
+            dg = __dp4a(d, d, dg);
+            if (TWO) {
+                const uint32_t sv = o ? wd[2 * j + 3] : wd[2 * j + 1];
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    const float dl = __fsub_rn(tgA[dr][j][ch], u8f(sv, ch));
+                    rs = __fmaf_rn(dl, dl, rs);
+                }
+            }
+        }
+        if (TWO) ds = __fadd_rn(ds, rs);
+    };
+    // Loss with partial-distance elimination: every term is >= 0 and round-to-nearest sums are
+    // monotone, so once the partial loss after the first P rows is >= `bound` the full loss is too and
+    // the candidate cannot win the strict select (D16); its remaining rows are never loaded.  Results
+    // are unchanged: selected candidates are always evaluated in full, in the D20 order.
+    auto loss = [&](int sr, int sc, float bound) -> float {
+        uint32_t dg = 0u;
+        float ds = 0.0f;
+        constexpr int S1 = PDE_FAST_S1(P), S2 = PDE_FAST_S2(P);
+#pragma unroll
+        for (int dr = 0; dr < S1; ++dr) row(sr, sc, dr, dg, ds);
+        if (partial_loss(a.alpha, __uint2float_rn(dg), ds, TWO) >= bound) return __int_as_float(0x7f800000);
+        if (S2 < D) {
+#pragma unroll
+            for (int dr = S1; dr < S2; ++dr) row(sr, sc, dr, dg, ds);
+            if (partial_loss(a.alpha, __uint2float_rn(dg), ds, TWO) >= bound) return __int_as_float(0x7f800000);
+        }
+#pragma unroll
+        for (int dr = (S2 < D ? S2 : S1); dr < D; ++dr) row(sr, sc, dr, dg, ds);
+        const float fg = __uint2float_rn(dg);
+        return TWO ? __fmaf_rn(a.alpha, fg, ds) : fg;
+    };
+    auto select = [&](int2& f, float& e, int sr, int sc) {
+        const float e2 = loss(sr, sc, e);
+        if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+    };
+    const int2* Fi = a.Fin + t * a.fstride;
+    const int i = r * w + c;
+    int2 f = make_int2(0, 0);
+    float e = 0.0f;
+    // field 1: d = (+1,0), neighbour (r+1, c) of F_in (= the field-0 result), clamped (D11)
+    if (valid) {
+        f = Fi[i];
+        e = a.E[t * a.fstride + i];
+        const int2 fn = r + 1 < h ? Fi[i + w] : f;
+        select(f, e, max(fn.x - 1, 0), fn.y);
+    }
+    // field 2: d = (0,-1), neighbour (r, c-1) of the field-1 result (lane - 1)
+    {
+        const int2 fl = make_int2(__shfl_up_sync(0xffffffffu, f.x, 1), __shfl_up_sync(0xffffffffu, f.y, 1));
+        if (valid && lane > 0) {
+            const int2 fn = c > 0 ? fl : f;
+            select(f, e, fn.x, min(fn.y + 1, w - 1));
+        }
+    }
+    // field 3: d = (0,+1), neighbour (r, c+1) of the field-2 result (lane + 1), then random search
+    {
+        const int2 fr = make_int2(__shfl_down_sync(0xffffffffu, f.x, 1), __shfl_down_sync(0xffffffffu, f.y, 1));
+        if (!valid || lane == 0 || lane == 31) return;
+        const int2 fn = c + 1 < w ? fr : f;
+        select(f, e, fn.x, max(fn.y - 1, 0));
+    }
+    for (int s = 0; s < a.rs_k; ++s) {
+        const int R = max(a.rs_r0 >> s, 1);
+        const uint4 u = philox4x32_10(
+            make_uint4((uint32_t)i, (1u << 28) | (a.level << 22) | (a.iter << 12) | (uint32_t)s, T.c2, T.c3),
+            a.rng.k0, a.rng.k1);
+        const uint32_t span = 2u * (uint32_t)R + 1u;
+        const int ox = (int)__umulhi(u.x, span) - R, oy = (int)__umulhi(u.y, span) - R;
+        select(f, e, clampi(f.x + ox, 0, h - 1), clampi(f.y + oy, 0, w - 1));
+    }
+    a.Fout[t * a.fstride + i] = f;
+    a.E[t * a.fstride + i] = e;
+}
+
 // ---- general variant: SF32 source, TF32 target staged in shared memory (any level, P <= 4) -------
 // SF16 channel: u16 lane `sel` (0x7410 low, 0x7432 high) of a word as the exact float n / 4^k, using
 // the magic 2^(23-2k) whose bit pattern is ex = (75-k) << 24: bits(ex | n) = 2^(23-2k) + n 4^-k.
@@ -834,6 +963,18 @@ cudaError_t launch_iter_fast(const FieldArgs& a0, int T, int p, int loss, cudaSt
     const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(32 * (IT_TY + 1));
     if (p == 1) { if (loss) k_iter_fast<1, true><<<grid, block, 0, s>>>(a); else k_iter_fast<1, false><<<grid, block, 0, s>>>(a); }
     else if (p == 2) { if (loss) k_iter_fast<2, true><<<grid, block, 0, s>>>(a); else k_iter_fast<2, false><<<grid, block, 0, s>>>(a); }
+    else return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_iter13_fast(const FieldArgs& a0, int T, int p, int loss, cudaStream_t s)
+{
+    FieldArgs a = a0;
+    a.tiles_x = (a.L.w + IT_TX - 1) / IT_TX;
+    a.tiles_per_task = a.tiles_x * ((a.L.h + I13_TY - 1) / I13_TY);
+    const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(32 * I13_TY);
+    if (p == 1) { if (loss) k_iter13_fast<1, true><<<grid, block, 0, s>>>(a); else k_iter13_fast<1, false><<<grid, block, 0, s>>>(a); }
+    else if (p == 2) { if (loss) k_iter13_fast<2, true><<<grid, block, 0, s>>>(a); else k_iter13_fast<2, false><<<grid, block, 0, s>>>(a); }
     else return cudaErrorInvalidValue;
     return cudaGetLastError();
 }

@@ -110,6 +110,9 @@ cudaError_t launch_field(const FieldArgs& a, int T, int p, int loss, int phase, 
 // The whole updating sequence of one iteration (E init, four propagation fields, random search) in one
 // launch, fast operands only (SF8/TF16, p <= 2).  Fin -> Fout, E written.
 cudaError_t launch_iter_fast(const FieldArgs& a, int T, int p, int loss, cudaStream_t s);
+// Fields 1-3 and the random search of one iteration in one launch (fast operands); Fin holds the
+// field-0 result and E its errors.  Fin -> Fout, E updated.
+cudaError_t launch_iter13_fast(const FieldArgs& a, int T, int p, int loss, cudaStream_t s);
 cudaError_t launch_remap_f3(const float* src, const int2* F, float* out, int B, int H, int W, int p,
                             cudaStream_t s);
 
