@@ -360,12 +360,14 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
                 bool self_done = false;
                 for (int t : members[gi]) {
                     if (!self_done && tasks[t].src_id > groups[gi].tgt_id) {
-                        mem.push_back(DMember{groups[gi].tstyle + g.L[k].off, -1, 1.0f});
+                        mem.push_back(DMember{groups[gi].tstyle + g.L[k].off, -1, 1.0f, nullptr, -1});
                         self_done = true;
                     }
-                    mem.push_back(DMember{tasks[t].ss + g.L[k].off, t, 1.0f});
+                    const int sf = src_fmt(slots.fmt0, k);
+                    mem.push_back(DMember{tasks[t].ss + g.L[k].off, t, 1.0f, tasks[t].src + slots.off[k],
+                                          sf == fbk::SF32 ? -1 : sf});
                 }
-                if (!self_done) mem.push_back(DMember{groups[gi].tstyle + g.L[k].off, -1, 1.0f});
+                if (!self_done) mem.push_back(DMember{groups[gi].tstyle + g.L[k].off, -1, 1.0f, nullptr, -1});
                 o.nm = (int)mem.size() - o.m0;
                 o.div = (float)o.nm;
                 o.fmt = (k == 0 && fast0) ? 2 : 3;
@@ -455,8 +457,12 @@ struct CombineList {
     std::vector<DOut> outs;
     std::vector<DMember> mem;
     void begin() { outs.push_back(DOut{(int)mem.size(), 0, 1.0f, 1, nullptr, nullptr}); }
-    void add_img(const float4* img, float w) { mem.push_back(DMember{img, -1, w}); ++outs.back().nm; }
-    void add_remap(const float4* src_level_img, int task, float w) { mem.push_back(DMember{src_level_img, task, w}); ++outs.back().nm; }
+    void add_img(const float4* img, float w) { mem.push_back(DMember{img, -1, w, nullptr, -1}); ++outs.back().nm; }
+    void add_remap(const float4* src_level_img, int task, float w)
+    {
+        mem.push_back(DMember{src_level_img, task, w, nullptr, -1});
+        ++outs.back().nm;
+    }
     void end(void* out, int fmt, float div) { outs.back().out = out; outs.back().fmt = fmt; outs.back().div = div; }
 };
 

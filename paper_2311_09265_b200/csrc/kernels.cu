@@ -40,6 +40,12 @@ __device__ __forceinline__ float u8f(uint32_t word, int ch)
 {
     return __fsub_rn(__uint_as_float(__byte_perm(word, 0x4B000000u, 0x7440u + (uint32_t)ch)), 8388608.0f);
 }
+// SF16 channel: u16 lane `sel` (0x7410 low, 0x7432 high) of a word as the exact float n / 4^k, using
+// the magic 2^(23-2k) whose bit pattern is ex = (75-k) << 24: bits(ex | n) = 2^(23-2k) + n 4^-k.
+__device__ __forceinline__ float u16f(uint32_t word, uint32_t sel, uint32_t ex)
+{
+    return __fsub_rn(__uint_as_float(__byte_perm(word, ex, sel)), __uint_as_float(ex));
+}
 __device__ __forceinline__ uint32_t pack_rgb(float r, float g, float b)  // exact for integer 0..255
 {
     return (uint32_t)r | ((uint32_t)g << 8) | ((uint32_t)b << 16);
@@ -215,6 +221,44 @@ __device__ __forceinline__ float3 remap_px(const float4* __restrict__ S, const i
 }
 
 // S^ refresh (GUIDE_STYLE, D17/D18): packed target = {G_tgt, remap(S_src, F)} over the padded grid.
+// Same remap reading the style channels from a packed source slot (SF8: u8 word, SF16: two u16 words),
+// converted exactly; identical values, a quarter / half of the bytes per tap.
+template <int P, int SFMT>
+__device__ __forceinline__ float3 remap_px_slot(const char* __restrict__ slot, int pitch, const int2* __restrict__ F,
+                                                int h, int w, int r, int c, uint32_t ex)
+{
+    float ax = 0.0f, ay = 0.0f, az = 0.0f;
+    int n = 0;
+#pragma unroll
+    for (int dr = -P; dr <= P; ++dr) {
+        const int tr = r + dr;
+        if ((unsigned)tr >= (unsigned)h) continue;
+#pragma unroll
+        for (int dc = -P; dc <= P; ++dc) {
+            const int tc = c + dc;
+            if ((unsigned)tc >= (unsigned)w) continue;
+            const int2 f = __ldg(&F[tr * w + tc]);
+            const int sr = f.x - dr, sc = f.y - dc;
+            if ((unsigned)sr >= (unsigned)h || (unsigned)sc >= (unsigned)w) continue;
+            const int idx = (sr + kBorder) * pitch + sc + kBorder;
+            float vx, vy, vz;
+            if (SFMT == SF8) {
+                const uint32_t sv = __ldg(reinterpret_cast<const uint32_t*>(slot) + 2 * idx + 1);
+                vx = u8f(sv, 0); vy = u8f(sv, 1); vz = u8f(sv, 2);
+            } else {
+                const uint2 sv = __ldg(reinterpret_cast<const uint2*>(slot) + 2 * idx + 1);
+                vx = u16f(sv.x, 0x7410u, ex); vy = u16f(sv.x, 0x7432u, ex); vz = u16f(sv.y, 0x7410u, ex);
+            }
+            ax = __fadd_rn(ax, vx);
+            ay = __fadd_rn(ay, vy);
+            az = __fadd_rn(az, vz);
+            ++n;
+        }
+    }
+    const float fn = (float)n;
+    return make_float3(__fdiv_rn(ax, fn), __fdiv_rn(ay, fn), __fdiv_rn(az, fn));
+}
+
 template <int P>
 __global__ void k_aux_remap(const DTask* __restrict__ tasks, const int2* __restrict__ F, long long fstride, Lvl L,
                             PLvl PL, int tfmt)
@@ -259,7 +303,13 @@ __global__ void k_combine(const DOut* __restrict__ outs, const DMember* __restri
                     const float4 v = __ldg(&mb.img[j]);
                     y = make_float3(v.x, v.y, v.z);
                 } else {
-                    y = remap_px<P>(mb.img, F + mb.task * fstride, h, w, r, c);
+                    if (mb.sfmt == SF8)
+                        y = remap_px_slot<P, SF8>(mb.slot, PL.pitch, F + mb.task * fstride, h, w, r, c, 0u);
+                    else if (mb.sfmt == SF16)
+                        y = remap_px_slot<P, SF16>(mb.slot, PL.pitch, F + mb.task * fstride, h, w, r, c,
+                                                   (uint32_t)(75 - PL.k) << 24);
+                    else
+                        y = remap_px<P>(mb.img, F + mb.task * fstride, h, w, r, c);
                 }
                 ax = __fmaf_rn(mb.w, y.x, ax);
                 ay = __fmaf_rn(mb.w, y.y, ay);
@@ -723,12 +773,6 @@ __global__ void __launch_bounds__(32 * I13_TY, 3) k_iter13_fast(FieldArgs a)
 }
 
 // ---- general variant: SF32 source, TF32 target staged in shared memory (any level, P <= 4) -------
-// SF16 channel: u16 lane `sel` (0x7410 low, 0x7432 high) of a word as the exact float n / 4^k, using
-// the magic 2^(23-2k) whose bit pattern is ex = (75-k) << 24: bits(ex | n) = 2^(23-2k) + n 4^-k.
-__device__ __forceinline__ float u16f(uint32_t word, uint32_t sel, uint32_t ex)
-{
-    return __fsub_rn(__uint_as_float(__byte_perm(word, ex, sel)), __uint_as_float(ex));
-}
 
 template <int P, bool TWO, int PHASE, int SFMT>
 __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)

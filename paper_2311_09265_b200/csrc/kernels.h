@@ -53,6 +53,8 @@ struct DMember {
     const float4* img;  // image at the combine's level (already offset to the level)
     int task;           // -1: plain image; >= 0: remap img with F of this task
     float w;            // weight (exact powers of two, 1, -1, or the Eq. 9 weights)
+    const char* slot;   // optional packed source slot level block holding the same image exactly
+    int sfmt;           // slot format (SF8 / SF16) or -1: remap reads 4/8 bytes per tap instead of 16
 };
 struct DOut {
     int m0, nm;           // member range
