@@ -480,8 +480,10 @@ __global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
         const int nr = clampi(r + dx, 0, h - 1), nc = clampi(c + dy, 0, w - 1);  // D11
         const int2 fn = Fi[nr * w + nc];
         const int sr = clampi(fn.x - dx, 0, h - 1), sc = clampi(fn.y - dy, 0, w - 1);  // D10
-        const float e2 = loss(sr, sc, e);
-        if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+        if (sr != f.x || sc != f.y) {  // an incumbent-equal candidate cannot win (see select)
+            const float e2 = loss(sr, sc, e);
+            if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+        }
     }
     if (PHASE == 3) {
         for (int s = 0; s < a.rs_k; ++s) {
@@ -492,8 +494,10 @@ __global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
             const uint32_t span = 2u * (uint32_t)R + 1u;
             const int ox = (int)__umulhi(u.x, span) - R, oy = (int)__umulhi(u.y, span) - R;
             const int sr = clampi(f.x + ox, 0, h - 1), sc = clampi(f.y + oy, 0, w - 1);
-            const float e2 = loss(sr, sc, e);
-            if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+            if (sr != f.x || sc != f.y) {
+                const float e2 = loss(sr, sc, e);
+                if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+            }
         }
     }
     a.Fout[t * a.fstride + i] = f;
@@ -592,9 +596,14 @@ __global__ void __launch_bounds__(32 * (IT_TY + 1), IT_MINB) k_iter_fast(FieldAr
         const float fg = __uint2float_rn(dg);
         return TWO ? __fmaf_rn(a.alpha, fg, ds) : fg;
     };
+    // A candidate equal to the incumbent has exactly the incumbent's loss (same aux within the
+    // iteration), so it cannot win the strict select (D16): skipping it changes nothing.
     auto select = [&](int2& f, float& e, int sr, int sc) {
-        const float e2 = loss(sr, sc, e);
-        if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+        if (sr == f.x && sc == f.y) return;
+        if (sr != f.x || sc != f.y) {  // an incumbent-equal candidate cannot win (see select)
+            const float e2 = loss(sr, sc, e);
+            if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+        }
     };
     const int2* Fi = a.Fin + t * a.fstride;
     const int i = r * w + c;
@@ -729,9 +738,14 @@ __global__ void __launch_bounds__(32 * I13_TY, 3) k_iter13_fast(FieldArgs a)
         const float fg = __uint2float_rn(dg);
         return TWO ? __fmaf_rn(a.alpha, fg, ds) : fg;
     };
+    // A candidate equal to the incumbent has exactly the incumbent's loss (same aux within the
+    // iteration), so it cannot win the strict select (D16): skipping it changes nothing.
     auto select = [&](int2& f, float& e, int sr, int sc) {
-        const float e2 = loss(sr, sc, e);
-        if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+        if (sr == f.x && sc == f.y) return;
+        if (sr != f.x || sc != f.y) {  // an incumbent-equal candidate cannot win (see select)
+            const float e2 = loss(sr, sc, e);
+            if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+        }
     };
     const int2* Fi = a.Fin + t * a.fstride;
     const int i = r * w + c;
@@ -862,8 +876,10 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
         const int nr = clampi(r + dx, 0, h - 1), nc = clampi(c + dy, 0, w - 1);  // D11
         const int2 fn = Fi[nr * w + nc];
         const int sr = clampi(fn.x - dx, 0, h - 1), sc = clampi(fn.y - dy, 0, w - 1);  // D10
-        const float e2 = loss(sr, sc, e);
-        if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+        if (sr != f.x || sc != f.y) {  // an incumbent-equal candidate cannot win (see select)
+            const float e2 = loss(sr, sc, e);
+            if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+        }
     }
     if (PHASE == 3) {
         for (int s = 0; s < a.rs_k; ++s) {
@@ -874,8 +890,10 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
             const uint32_t span = 2u * (uint32_t)R + 1u;
             const int ox = (int)__umulhi(u.x, span) - R, oy = (int)__umulhi(u.y, span) - R;
             const int sr = clampi(f.x + ox, 0, h - 1), sc = clampi(f.y + oy, 0, w - 1);
-            const float e2 = loss(sr, sc, e);
-            if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+            if (sr != f.x || sc != f.y) {
+                const float e2 = loss(sr, sc, e);
+                if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+            }
         }
     }
     a.Fout[t * a.fstride + i] = f;
