@@ -506,31 +506,40 @@ std::vector<std::pair<int, int>> make_batches(const std::vector<int>& cost, int 
 
 // ------------------------------------------------------------------------------------ direct schedule
 // Eq. 2 + Eq. 3 (balanced) or Eq. 7/8 (accurate), O(N*M) NNFs.
+// Streaming ("Users can process long videos in accurate mode"): each batch of
+// targets builds the pyramids and packed slots of only the frames its windows read, [first-M, last+M],
+// inside the batch's arena region, so device memory is O(batch + 2M) frames, not O(N).
 void blend_direct(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int N_total, int f0, int N, int M,
                   const uint8_t* guide, const uint8_t* style, int t0, int t1, float* out, fb_stats* st)
 {
-    const Pyr G = pyramid_u8(ex, g, guide, N);
-    const Pyr S = pyramid_u8(ex, g, style, N);
+    (void)N;
     const long long n0 = g.npx0();
-    std::vector<SlotSpec> specs;
-    for (int j = 0; j < N; ++j) specs.push_back(SlotSpec{guide + 3 * n0 * j, style + 3 * n0 * j, G.frame(j), S.frame(j)});
-    const Slots FR = pack_sources(ex, g, fbk::SF8, specs);
     std::vector<int> cost;
     for (int i = t0; i < t1; ++i) cost.push_back(std::min(N_total - 1, i + M) - std::max(0, i - M));
     const auto batches = make_batches(cost, batch_pairs(ex.ctx, g, cfg.loss));
     const size_t mark = ex.ar.off;
     for (auto [b0, b1] : batches) {
         ex.ar.off = mark;
+        // frames this batch reads (original ids), then their local (input) and batch indices
+        const int lo_b = std::max(0, t0 + b0 - M), hi_b = std::min(N_total - 1, t0 + b1 - 1 + M);
+        const int nb = hi_b - lo_b + 1;
+        const uint8_t* gb = guide + 3 * n0 * (lo_b - f0);
+        const uint8_t* sb = style + 3 * n0 * (lo_b - f0);
+        const Pyr G = pyramid_u8(ex, g, gb, nb);
+        const Pyr S = pyramid_u8(ex, g, sb, nb);
+        std::vector<SlotSpec> specs;
+        for (int j = 0; j < nb; ++j) specs.push_back(SlotSpec{gb + 3 * n0 * j, sb + 3 * n0 * j, G.frame(j), S.frame(j)});
+        const Slots FR = pack_sources(ex, g, fbk::SF8, specs);
         std::vector<TaskSpec> tasks;
         std::vector<GroupSpec> groups;
         std::vector<int> first(b1 - b0);
         for (int q = b0; q < b1; ++q) {
             const int i = t0 + q, lo = std::max(0, i - M), hi = std::min(N_total - 1, i + M);
             first[q - b0] = (int)tasks.size();
-            if (cfg.loss == FB_LOSS_MEAN_ALIGN) groups.push_back(GroupSpec{S.frame(i - f0), G.frame(i - f0), (uint32_t)i});
+            if (cfg.loss == FB_LOSS_MEAN_ALIGN) groups.push_back(GroupSpec{S.frame(i - lo_b), G.frame(i - lo_b), (uint32_t)i});
             for (int j = lo; j <= hi; ++j) {
                 if (j == i) continue;
-                tasks.push_back(TaskSpec{FR.slot(j - f0), S.frame(j - f0), G.frame(i - f0),
+                tasks.push_back(TaskSpec{FR.slot(j - lo_b), S.frame(j - lo_b), G.frame(i - lo_b),
                                          cfg.loss == FB_LOSS_MEAN_ALIGN ? q - b0 : -1, (uint32_t)j, (uint32_t)i, 0u});
             }
         }
@@ -542,8 +551,8 @@ void blend_direct(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int N_total, 
             int t = first[q - b0];
             cl.begin();
             for (int j = lo; j <= hi; ++j) {
-                if (j == i) cl.add_img(S.frame(i - f0), 1.0f);
-                else cl.add_remap(S.frame(j - f0), t++, 1.0f);
+                if (j == i) cl.add_img(S.frame(i - lo_b), 1.0f);
+                else cl.add_remap(S.frame(j - lo_b), t++, 1.0f);
             }
             cl.end(out + 3LL * n0 * q, 1, (float)(hi - lo + 1));
             if (st) st->remap_pixels += (uint64_t)(hi - lo) * n0;

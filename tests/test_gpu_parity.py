@@ -244,3 +244,15 @@ def test_error_statuses(fb, ctx):
     with pytest.raises(fb.FBError) as e:
         ctx.fb_interpolate_keyframes(fb.MatchCfg(), dev(g), [2, 1], dev(s[:2]))
     assert e.value.status == 1
+
+
+def test_streaming_workspace_is_O_window(fb):
+    """f4 / P:249: the direct schedule keeps only each batch's frames (+2M) resident, so the workspace of
+    an accurate-mode blend does not grow with the video length once batches are capped."""
+    ctx = fb.Context(0, max_batch_pairs=300)
+    cfg = fb.MatchCfg(loss=fb.MEAN_ALIGN)
+    w200 = ctx.workspace_size(fb.fb.OP_BLEND_DIRECT, cfg, 200, 512, 512, 15)
+    w2000 = ctx.workspace_size(fb.fb.OP_BLEND_DIRECT, cfg, 2000, 512, 512, 15)
+    assert w2000 == w200
+    full = fb.Context(0).workspace_size(fb.fb.OP_BLEND_DIRECT, cfg, 2000, 512, 512, 15)
+    assert w2000 < full / 5
