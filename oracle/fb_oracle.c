@@ -37,12 +37,12 @@ typedef struct {
     int32_t rs_radius0;      /* initial random-search radius, 0 = max(h_k, w_k) (D13, D33)  */
     int32_t rs_steps;        /* random-search steps, 0 = until radius < 1 (D13, D33)          */
     float alpha;             /* guide weight alpha (Eq. 3; Eq. 8)               */
-    int32_t loss;            /* 0 BASE (Eq. 1), 1 GUIDE_STYLE (Eq. 3), 2 MEAN_ALIGN (Eq. 8)   */
+    int32_t loss;            /* 0 BASE (Eq. 1), 1 GUIDE_STYLE (Eq. 3), 2 MEAN_ALIGN (Eq. 8), 3 PAIRWISE (Eq. 10) */
     int32_t init;            /* 0 random, 1 identity (D8)                              */
     uint64_t seed;           /* Philox key (D21)                                              */
 } orc_cfg;
 
-enum { ORC_BASE = 0, ORC_GUIDE_STYLE = 1, ORC_MEAN_ALIGN = 2 };
+enum { ORC_BASE = 0, ORC_GUIDE_STYLE = 1, ORC_MEAN_ALIGN = 2, ORC_PAIRWISE = 3 };
 enum { ORC_TAG_DIRECT = 0, ORC_TAG_TREE_BUILD_F = 1, ORC_TAG_TREE_QUERY_F = 2,
        ORC_TAG_TREE_BUILD_R = 3, ORC_TAG_TREE_QUERY_R = 4, ORC_TAG_INTERP = 5 };
 
@@ -188,6 +188,7 @@ typedef struct {
     int src_guide, tgt_guide, src_style, tgt_style; /* indices into the frame stack (-1 = none) */
     int group;                                       /* MEAN_ALIGN window id                     */
     int src_id, tgt_id, tag;                         /* RNG key (D21)                            */
+    int partner;                                     /* PAIRWISE: the counterpart task (D38)     */
 } orc_task;
 
 typedef struct {
@@ -230,16 +231,27 @@ typedef struct {
     int h, w, p, loss;
     float alpha;
     const float *sg, *tg, *ss, *aux; /* source guide, target guide, source style, aux (S^ or T-bar) */
+    const float* pss;                /* PAIRWISE: counterpart's source style (the other keyframe)   */
+    const int32_t* pF;               /* PAIRWISE: counterpart's NNF at the start of the iteration   */
 } orc_level_ctx;
 
 /* The loss L(S', T', F)(x,y) of a candidate (sr, sc) for target pixel (r, c):
  * BASE = Eq. 1; GUIDE_STYLE = Eq. 3, alpha*D(G_src,G_tgt) + D(S_src, S^);
- * MEAN_ALIGN = Eq. 8 (reading D27), alpha*D(G_src,G_tgt) + D(S_src, T-bar). */
+ * MEAN_ALIGN = Eq. 8 (reading D27), alpha*D(G_src,G_tgt) + D(S_src, T-bar);
+ * PAIRWISE = Eq. 10 (reading D38/D39), alpha*D(G_src,G_tgt) + ||S_l[F_l(x)] - S_r[F_r(x)]||^2:
+ * the second term compares the candidate's patch of this task's keyframe style with the patch of
+ * the counterpart keyframe's style at the counterpart's NNF (frozen at the iteration start). */
 static float level_loss(const orc_level_ctx* L, int r, int c, int sr, int sc)
 {
     float dg = orc_patch_dist(L->sg, L->tg, L->h, L->w, sr, sc, r, c, L->p);
     if (L->loss == ORC_BASE) return dg;
-    float ds = orc_patch_dist(L->ss, L->aux, L->h, L->w, sr, sc, r, c, L->p);
+    float ds;
+    if (L->loss == ORC_PAIRWISE) {
+        const int32_t* q = L->pF + 2 * ((size_t)r * L->w + c);
+        ds = orc_patch_dist(L->ss, L->pss, L->h, L->w, sr, sc, q[0], q[1], L->p);
+    } else {
+        ds = orc_patch_dist(L->ss, L->aux, L->h, L->w, sr, sc, r, c, L->p);
+    }
     return fmaf(L->alpha, dg, ds);
 }
 
@@ -305,7 +317,7 @@ static void level_field(const orc_level_ctx* L, const orc_cfg* cfg, int field, i
 void orc_field(const orc_cfg* cfg, int h, int w, const float* sg, const float* tg, const float* ss,
                const float* aux, int field, int k, int it, int src_id, int tgt_id, int tag, int32_t* F, float* E)
 {
-    orc_level_ctx L = { h, w, cfg->patch_radius, cfg->loss, cfg->alpha, sg, tg, ss, aux };
+    orc_level_ctx L = { h, w, cfg->patch_radius, cfg->loss, cfg->alpha, sg, tg, ss, aux, NULL, NULL };
     int32_t* Fo = (int32_t*)malloc(sizeof(int32_t) * 2 * (size_t)h * w);
     float* Eo = (float*)malloc(sizeof(float) * (size_t)h * w);
     level_field(&L, cfg, field, k, it, src_id, tgt_id, tag, F, E, Fo, Eo);
@@ -320,6 +332,7 @@ typedef struct {
     float** aux;     /* per task aux at current level [h_k, w_k, 3] */
     int32_t** F; float** E;
     int32_t** Fn; float** En;
+    int32_t** Fsnap;  /* PAIRWISE: every task's NNF at the start of the current iteration (D39) */
     lvl_t L[32];
 } orc_state;
 
@@ -335,7 +348,10 @@ static void refresh_aux(orc_state* st, int k)
     const orc_cfg* cfg = st->cfg;
     int h = st->L[k].h, w = st->L[k].w, p = cfg->patch_radius;
     size_t npx = (size_t)h * w;
-    if (cfg->loss == ORC_GUIDE_STYLE) {
+    if (cfg->loss == ORC_PAIRWISE) {
+        /* the counterpart NNFs are frozen at the start of the iteration (D39) */
+        for (int t = 0; t < st->T; ++t) memcpy(st->Fsnap[t], st->F[t], sizeof(int32_t) * 2 * npx);
+    } else if (cfg->loss == ORC_GUIDE_STYLE) {
         /* S^_i = remap of the task's source style with the current F at this level (D18) */
         for (int t = 0; t < st->T; ++t)
             orc_remap(st->pyr_ss[t] + 3 * st->L[k].off, h, w, st->F[t], p, st->aux[t]);
@@ -383,7 +399,11 @@ static void iterate_task(orc_state* st, int t, int k, int it, uint64_t* evals)
     size_t off = 3 * st->L[k].off;
     orc_level_ctx L = { st->L[k].h, st->L[k].w, cfg->patch_radius, cfg->loss, cfg->alpha,
                         st->pyr_sg[t] + off, st->pyr_tg[t] + off, st->pyr_ss[t] ? st->pyr_ss[t] + off : NULL,
-                        st->aux[t] };
+                        st->aux[t], NULL, NULL };
+    if (cfg->loss == ORC_PAIRWISE) {
+        L.pss = st->pyr_ss[tk->partner] + off;
+        L.pF = st->Fsnap[tk->partner];
+    }
     int K = rs_count(cfg, L.h, L.w);
     for (int field = -1; field < 4 + K; ++field) {
         level_field(&L, cfg, field, k, it, tk->src_id, tk->tgt_id, tk->tag, st->F[t], st->E[t], st->Fn[t], st->En[t]);
@@ -401,12 +421,18 @@ int orc_nnf(const orc_cfg* cfg, int T, int H, int W, const float* frames, const 
     st.cfg = cfg; st.T = T; st.H = H; st.W = W; st.tasks = tasks;
     st.lv = orc_level_count(H, W, cfg->patch_radius, cfg->levels);
     if (st.lv < 1) return -1;
+    if (cfg->loss == ORC_PAIRWISE)  /* every task needs a counterpart with a source style */
+        for (int t = 0; t < T; ++t)
+            if (tasks[t].partner < 0 || tasks[t].partner >= T || tasks[t].src_style < 0 ||
+                tasks[tasks[t].partner].src_style < 0)
+                return -2;
     size_t npx0 = (size_t)H * W, pyr = orc_pyramid_pixels(H, W, st.lv);
     for (int k = 0; k < st.lv; ++k) { st.L[k].h = H >> k; st.L[k].w = W >> k; st.L[k].off = level_offset(H, W, k); }
     st.pyr_sg = (float**)calloc(T, sizeof(float*)); st.pyr_tg = (float**)calloc(T, sizeof(float*));
     st.pyr_ss = (float**)calloc(T, sizeof(float*)); st.pyr_ts = (float**)calloc(T, sizeof(float*));
     st.aux = (float**)calloc(T, sizeof(float*));
     st.F = (int32_t**)calloc(T, sizeof(int32_t*)); st.E = (float**)calloc(T, sizeof(float*));
+    st.Fsnap = (int32_t**)calloc(T, sizeof(int32_t*));
     st.Fn = (int32_t**)calloc(T, sizeof(int32_t*)); st.En = (float**)calloc(T, sizeof(float*));
 #pragma omp parallel for schedule(static)
     for (int t = 0; t < T; ++t) {
@@ -426,6 +452,7 @@ int orc_nnf(const orc_cfg* cfg, int T, int H, int W, const float* frames, const 
         st.aux[t] = (float*)malloc(sizeof(float) * 3 * npx0);
         st.F[t] = (int32_t*)malloc(sizeof(int32_t) * 2 * npx0); st.E[t] = (float*)malloc(sizeof(float) * npx0);
         st.Fn[t] = (int32_t*)malloc(sizeof(int32_t) * 2 * npx0); st.En[t] = (float*)malloc(sizeof(float) * npx0);
+        st.Fsnap[t] = (int32_t*)malloc(sizeof(int32_t) * 2 * npx0);
     }
     uint64_t evals = 0;
     int32_t* tmp = (int32_t*)malloc(sizeof(int32_t) * 2 * npx0);
@@ -473,10 +500,10 @@ int orc_nnf(const orc_cfg* cfg, int T, int H, int W, const float* frames, const 
     }
     for (int t = 0; t < T; ++t) {
         free(st.pyr_sg[t]); free(st.pyr_tg[t]); free(st.pyr_ss[t]); free(st.pyr_ts[t]); free(st.aux[t]);
-        free(st.F[t]); free(st.E[t]); free(st.Fn[t]); free(st.En[t]);
+        free(st.F[t]); free(st.E[t]); free(st.Fn[t]); free(st.En[t]); free(st.Fsnap[t]);
     }
     free(st.pyr_sg); free(st.pyr_tg); free(st.pyr_ss); free(st.pyr_ts); free(st.aux);
-    free(st.F); free(st.E); free(st.Fn); free(st.En); free(tmp);
+    free(st.F); free(st.E); free(st.Fn); free(st.En); free(st.Fsnap); free(tmp);
     if (evals_out) *evals_out = evals;
     return 0;
 }
@@ -509,7 +536,7 @@ int orc_blend_direct(const orc_cfg* cfg, int N, int H, int W, int M, const uint8
         int i = targets[q], lo = i - M < 0 ? 0 : i - M, hi = i + M > N - 1 ? N - 1 : i + M;
         for (int j = lo; j <= hi; ++j) {
             if (j == i) continue;
-            orc_task tk = { j, i, N + j, cfg->loss == ORC_MEAN_ALIGN ? N + i : -1, q, j, i, ORC_TAG_DIRECT };
+            orc_task tk = { j, i, N + j, cfg->loss == ORC_MEAN_ALIGN ? N + i : -1, q, j, i, ORC_TAG_DIRECT, -1 };
             tasks[T++] = tk;
         }
     }
@@ -617,7 +644,7 @@ static int build_table_needed(const orc_cfg* cfg, int N, int H, int W, int M, in
     for (int a = 0; a < nb; ++a) {
         if (!need[(size_t)bd[a] * (lcap + 1) + bl[a]]) continue;
         int oi = orient == 0 ? bs[a] : N - 1 - bs[a], oj = orient == 0 ? bd[a] : N - 1 - bd[a];
-        orc_task tk = { oi, oj, N + oi, -1, 0, oi, oj, orient == 0 ? ORC_TAG_TREE_BUILD_F : ORC_TAG_TREE_BUILD_R };
+        orc_task tk = { oi, oj, N + oi, -1, 0, oi, oj, orient == 0 ? ORC_TAG_TREE_BUILD_F : ORC_TAG_TREE_BUILD_R, -1 };
         tasks[T] = tk; tcell[T] = a; ++T;
     }
     float* X = (float*)malloc(sizeof(float) * 3 * npx * (T > 0 ? T : 1));
@@ -678,7 +705,7 @@ static int query_unnormalised(const orc_cfg* cfg, int N, int H, int W, int M, in
         if (nodes[a] == v) continue; /* self node: identity, no NNF (D23) */
         int oi = orient == 0 ? nodes[a] : N - 1 - nodes[a];
         memcpy(fr + 3 * npx * (N + T), tab->bt[(size_t)nodes[a] * (tab->lcap + 1) + lvls[a]], sizeof(float) * 3 * npx);
-        orc_task tk = { oi, target, N + T, -1, 0, oi, target, orient == 0 ? ORC_TAG_TREE_QUERY_F : ORC_TAG_TREE_QUERY_R };
+        orc_task tk = { oi, target, N + T, -1, 0, oi, target, orient == 0 ? ORC_TAG_TREE_QUERY_F : ORC_TAG_TREE_QUERY_R, -1 };
         tasks[T] = tk; slot_of[a] = T; ++T;
     }
     float* X = (float*)malloc(sizeof(float) * 3 * npx * (T > 0 ? T : 1));
@@ -734,21 +761,28 @@ int orc_blend_tree(const orc_cfg* cfg, int N, int H, int W, int M, const uint8_t
 
 /* Keyframe interpolation, Eq. 9 (reading D28): for l < m < r consecutive keys,
  * out_m = fma(X_l, w_l, X_r * w_r), w_l = (r-m)/(r-l), w_r = (m-l)/(r-l); outside the key span the
- * nearest key's remap; keys verbatim.  X_k = remap of key style with NNF(G_k, G_m). */
+ * nearest key's remap; keys verbatim.  X_k = remap of key style with NNF(G_k, G_m).
+ * cfg->loss == PAIRWISE selects the alignment of Eq. 10 (D38-D40): the two NNFs of a
+ * frame between two keys are estimated jointly, each taking the other (frozen per iteration) in its
+ * loss; single-key frames and every other cfg->loss use the guide+style loss of Eq. 3. */
 int orc_interpolate(const orc_cfg* cfg, int N, int H, int W, const uint8_t* guide, int K,
                     const int32_t* key_index, const uint8_t* key_style, int n_targets, const int32_t* targets,
                     float* out, uint64_t* pairs_out, uint64_t* evals_out)
 {
     size_t npx = (size_t)H * W;
+    const int align = cfg->loss == ORC_PAIRWISE;
     float* frames = (float*)malloc(sizeof(float) * 3 * npx * ((size_t)N + K));
     u8_to_float(guide, 3 * npx * N, frames);
     u8_to_float(key_style, 3 * npx * K, frames + 3 * npx * N);
-    orc_task* tasks = (orc_task*)malloc(sizeof(orc_task) * (2 * (size_t)n_targets + 1));
-    int* ta = (int*)malloc(sizeof(int) * 2 * (n_targets + 1)); /* per target: task index of left/right */
-    int T = 0;
+    /* two task lists: [0] single-key / unaligned (GUIDE_STYLE), [1] aligned pairs (PAIRWISE) */
+    orc_task* tl[2];
+    int nt[2] = { 0, 0 };
+    tl[0] = (orc_task*)malloc(sizeof(orc_task) * (2 * (size_t)n_targets + 1));
+    tl[1] = (orc_task*)malloc(sizeof(orc_task) * (2 * (size_t)n_targets + 1));
+    int* ta = (int*)malloc(sizeof(int) * 4 * (n_targets + 1)); /* per target: (list, index) of left/right */
     for (int q = 0; q < n_targets; ++q) {
         int m = targets[q], a = -1;
-        ta[2 * q] = ta[2 * q + 1] = -1;
+        for (int z = 0; z < 4; ++z) ta[4 * q + z] = -1;
         for (int k = 0; k < K; ++k) if (key_index[k] == m) a = k;
         if (a >= 0) continue; /* key: verbatim */
         int left = -1, right = -1;
@@ -756,41 +790,53 @@ int orc_interpolate(const orc_cfg* cfg, int N, int H, int W, const uint8_t* guid
             if (key_index[k] < m) left = k;
             if (key_index[k] > m && right < 0) right = k;
         }
+        const int li = (align && left >= 0 && right >= 0) ? 1 : 0;
         if (left >= 0) {
-            orc_task tk = { key_index[left], m, N + left, -1, 0, key_index[left], m, ORC_TAG_INTERP };
-            ta[2 * q] = T; tasks[T++] = tk;
+            orc_task tk = { key_index[left], m, N + left, -1, 0, key_index[left], m, ORC_TAG_INTERP, -1 };
+            ta[4 * q] = li; ta[4 * q + 1] = nt[li]; tl[li][nt[li]++] = tk;
         }
         if (right >= 0) {
-            orc_task tk = { key_index[right], m, N + right, -1, 0, key_index[right], m, ORC_TAG_INTERP };
-            ta[2 * q + 1] = T; tasks[T++] = tk;
+            orc_task tk = { key_index[right], m, N + right, -1, 0, key_index[right], m, ORC_TAG_INTERP, -1 };
+            ta[4 * q + 2] = li; ta[4 * q + 3] = nt[li]; tl[li][nt[li]++] = tk;
+        }
+        if (li == 1) { /* counterparts */
+            tl[1][ta[4 * q + 1]].partner = ta[4 * q + 3];
+            tl[1][ta[4 * q + 3]].partner = ta[4 * q + 1];
         }
     }
-    float* X = (float*)malloc(sizeof(float) * 3 * npx * (T > 0 ? T : 1));
+    float* X[2];
     uint64_t evals = 0;
-    if (T > 0) {
-        orc_cfg c2 = *cfg; c2.loss = ORC_GUIDE_STYLE;
-        if (orc_nnf(&c2, T, H, W, frames, tasks, NULL, NULL, X, &evals) != 0) return -1;
+    for (int z = 0; z < 2; ++z) {
+        X[z] = (float*)malloc(sizeof(float) * 3 * npx * (nt[z] > 0 ? nt[z] : 1));
+        if (nt[z] > 0) {
+            orc_cfg c2 = *cfg;
+            c2.loss = z == 1 ? ORC_PAIRWISE : ORC_GUIDE_STYLE;
+            uint64_t ev = 0;
+            if (orc_nnf(&c2, nt[z], H, W, frames, tl[z], NULL, NULL, X[z], &ev) != 0) return -1;
+            evals += ev;
+        }
     }
     for (int q = 0; q < n_targets; ++q) {
         int m = targets[q];
         float* o = out + 3 * npx * q;
-        int tl = ta[2 * q], tr = ta[2 * q + 1];
-        if (tl < 0 && tr < 0) { /* key frame */
+        const int hl = ta[4 * q] >= 0, hr = ta[4 * q + 2] >= 0;
+        const float* xl = hl ? X[ta[4 * q]] + 3 * npx * ta[4 * q + 1] : NULL;
+        const float* xr = hr ? X[ta[4 * q + 2]] + 3 * npx * ta[4 * q + 3] : NULL;
+        if (!hl && !hr) { /* key frame */
             int a = 0;
             for (int k = 0; k < K; ++k) if (key_index[k] == m) a = k;
             memcpy(o, frames + 3 * npx * (N + a), sizeof(float) * 3 * npx);
-        } else if (tl < 0 || tr < 0) {
-            memcpy(o, X + 3 * npx * (tl < 0 ? tr : tl), sizeof(float) * 3 * npx);
+        } else if (!hl || !hr) {
+            memcpy(o, hl ? xl : xr, sizeof(float) * 3 * npx);
         } else {
-            int l = tasks[tl].src_id, r = tasks[tr].src_id;
+            int l = tl[ta[4 * q]][ta[4 * q + 1]].src_id, r = tl[ta[4 * q + 2]][ta[4 * q + 3]].src_id;
             float wl = (float)(r - m) / (float)(r - l), wr = (float)(m - l) / (float)(r - l);
-            const float* xl = X + 3 * npx * tl; const float* xr = X + 3 * npx * tr;
             for (size_t e = 0; e < 3 * npx; ++e) o[e] = fmaf(xl[e], wl, xr[e] * wr);
         }
     }
-    if (pairs_out) *pairs_out = (uint64_t)T;
+    if (pairs_out) *pairs_out = (uint64_t)(nt[0] + nt[1]);
     if (evals_out) *evals_out = evals;
-    free(frames); free(tasks); free(ta); free(X);
+    free(frames); free(tl[0]); free(tl[1]); free(ta); free(X[0]); free(X[1]);
     return 0;
 }
 

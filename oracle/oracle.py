@@ -15,7 +15,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 # -O2, no fast-math, no FP contraction: the only fused ops are the explicit fmaf() calls (D20).
 CFLAGS = ["-O2", "-std=c11", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off", "-fno-fast-math"]
 
-BASE, GUIDE_STYLE, MEAN_ALIGN = 0, 1, 2
+BASE, GUIDE_STYLE, MEAN_ALIGN, PAIRWISE = 0, 1, 2, 3
 INIT_RANDOM, INIT_IDENTITY = 0, 1
 TAG_DIRECT, TAG_TREE_BUILD_F, TAG_TREE_QUERY_F, TAG_TREE_BUILD_R, TAG_TREE_QUERY_R, TAG_INTERP, TAG_API = range(7)
 
@@ -37,7 +37,8 @@ class _Cfg(C.Structure):
 
 class _Task(C.Structure):
     _fields_ = [("src_guide", C.c_int), ("tgt_guide", C.c_int), ("src_style", C.c_int), ("tgt_style", C.c_int),
-                ("group", C.c_int), ("src_id", C.c_int), ("tgt_id", C.c_int), ("tag", C.c_int)]
+                ("group", C.c_int), ("src_id", C.c_int), ("tgt_id", C.c_int), ("tag", C.c_int),
+                ("partner", C.c_int)]
 
 
 @dataclass
@@ -152,14 +153,15 @@ def evals_per_task(cfg: Cfg, H: int, W: int) -> int:
 
 def nnf(cfg: Cfg, frames: np.ndarray, tasks: list[dict], want_x: bool = True):
     """frames float32 [NF,H,W,3]; tasks: dicts with src_guide, tgt_guide, src_style, tgt_style, group,
-    src_id, tgt_id, tag.  Returns (F [T,H,W,2] int32, E [T,H,W] float32, X [T,H,W,3] or None, evals)."""
+    src_id, tgt_id, tag, partner (PAIRWISE counterpart task index).  Returns (F [T,H,W,2] int32, E [T,H,W] float32, X [T,H,W,3] or None, evals)."""
     frames = np.ascontiguousarray(frames, np.float32)
     _, H, W, _ = frames.shape
     T = len(tasks)
     arr = (_Task * max(T, 1))()
     for i, t in enumerate(tasks):
         arr[i] = _Task(t["src_guide"], t["tgt_guide"], t.get("src_style", -1), t.get("tgt_style", -1),
-                       t.get("group", i), t.get("src_id", 0), t.get("tgt_id", 0), t.get("tag", TAG_API))
+                       t.get("group", i), t.get("src_id", 0), t.get("tgt_id", 0), t.get("tag", TAG_API),
+                       t.get("partner", -1))
     F = np.zeros((T, H, W, 2), np.int32)
     E = np.zeros((T, H, W), np.float32)
     X = np.zeros((T, H, W, 3), np.float32) if want_x else None

@@ -572,3 +572,67 @@ def test_ties_keep_the_incumbent(field):
     inner = (slice(6, 18), slice(6, 18))
     assert np.all(Ein[inner] == 0)
     np.testing.assert_array_equal(Fout[inner], Fin[inner])
+
+
+# ------------------------------------------------------------------ Eq. 10 alignment (f1, D38-D40)
+def np_patch_dist_centers(A, B, FA, FB, p):
+    """sum over taps d of (B(FB(x)+d) - A(FA(x)+d))^2, zero outside the image (D9), float64."""
+    h, w, _ = A.shape
+    Ap = np.pad(A.astype(np.float64), ((p, p), (p, p), (0, 0)))
+    Bp = np.pad(B.astype(np.float64), ((p, p), (p, p), (0, 0)))
+    D = np.zeros((h, w))
+    for dr in range(-p, p + 1):
+        for dc in range(-p, p + 1):
+            b = Bp[FB[..., 0] + dr + p, FB[..., 1] + dc + p]
+            a = Ap[FA[..., 0] + dr + p, FA[..., 1] + dc + p]
+            D += ((b - a) ** 2).sum(-1)
+    return D
+
+
+def _pair_tasks():
+    # frames: 0 = G_l, 1 = G_i, 2 = G_r, 3 = S_l, 4 = S_r
+    return [dict(src_guide=0, tgt_guide=1, src_style=3, src_id=0, tgt_id=1, tag=5, partner=1),
+            dict(src_guide=2, tgt_guide=1, src_style=4, src_id=2, tgt_id=1, tag=5, partner=0)]
+
+
+def test_pairwise_loss_uses_counterpart_frozen_at_iteration_start():
+    """Eq. 10: E_l(x) = alpha*||G_l[F_l(x)] - G_i[x]||^2 + ||S_l[F_l(x)] - S_r[F_r(x)]||^2 with F_r the
+    counterpart's NNF at the start of the last iteration (levels = 1, so n-1 iterations expose it)."""
+    g, s = moving_texture(3, 24, 28, seed=16)
+    frames = np.concatenate([g, s[[0, 2]]]).astype(np.float32)
+    p, alpha = 2, 3.0
+    cfg = O.Cfg(patch_radius=p, levels=1, iters_per_level=3, loss=O.PAIRWISE, alpha=alpha)
+    Fn, En, _, _ = O.nnf(cfg, frames, _pair_tasks(), want_x=False)
+    cfg.iters_per_level = 2
+    Fp, _, _, _ = O.nnf(cfg, frames, _pair_tasks(), want_x=False)
+    rr, cc = np.mgrid[0:24, 0:28]
+    ident = np.stack([rr, cc], -1)
+    for t, (gs, ss, other_ss) in enumerate(((0, 3, 4), (2, 4, 3))):
+        ref = alpha * np_patch_dist_centers(frames[gs], frames[1], Fn[t], ident, p) + \
+            np_patch_dist_centers(frames[ss], frames[other_ss], Fn[t], Fp[1 - t], p)
+        np.testing.assert_allclose(En[t], ref, rtol=2e-5, atol=1e-2)
+
+
+def test_pairwise_with_zero_counterpart_and_alpha0_equals_base_loss():
+    """alpha = 0 and a counterpart style of zeros: the loss is ||S_l[F_l(x)] - 0||^2, the base loss of S_l
+    against a black target, so PAIRWISE must equal BASE on (S_l -> zeros) bit for bit (same RNG keys)."""
+    g, s = moving_texture(3, 32, 36, seed=17)
+    z = np.zeros_like(s[0])
+    frames = np.stack([g[0], g[1], g[2], s[0], z, z]).astype(np.float32)
+    cfg = O.Cfg(patch_radius=2, iters_per_level=2, loss=O.PAIRWISE, alpha=0.0)
+    Fp_, Ep_, _, _ = O.nnf(cfg, frames, _pair_tasks(), want_x=False)
+    cfg.loss = O.BASE
+    Fb, Eb, _, _ = O.nnf(cfg, frames, [dict(src_guide=3, tgt_guide=5, src_id=0, tgt_id=1, tag=5)], want_x=False)
+    np.testing.assert_array_equal(Fp_[0], Fb[0])
+    np.testing.assert_array_equal(Ep_[0], Eb[0])
+
+
+def test_aligned_interpolation_equal_keys_static_video():
+    g, s = static_textured_video(7, 24, 24, flicker=False)
+    keys = [0, 6]
+    ks = np.stack([s[0], s[0]])
+    cfg = O.Cfg(patch_radius=2, iters_per_level=1, init=O.INIT_IDENTITY, loss=O.PAIRWISE)
+    out, pairs, _ = O.interpolate(cfg, g, keys, ks)
+    assert pairs == 2 * 5
+    for m in range(7):
+        np.testing.assert_allclose(out[m], s[0].astype(np.float32), atol=1e-4)
