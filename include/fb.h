@@ -36,16 +36,19 @@ typedef struct fb_ctx_s* fb_ctx;
 
 typedef enum {
     FB_OK = 0,
-    FB_ERR_INVALID_ARG = 1, /* N<1, M<0, p<1, n<0, alpha<0, bad enum, NULL required pointer, bad keys */
+    FB_ERR_INVALID_ARG = 1, /* N<1, M<0, p<1, n<0, alpha<0, bad enum, NULL required pointer, bad keys,
+                             * BASE/PAIRWISE for a window blend, non-mutual PAIRWISE counterparts */
     FB_ERR_SHAPE = 2,       /* min(H,W) < 2p+1, or explicit levels whose coarsest side < 2p+1 (D32)  */
     FB_ERR_CUDA = 3,        /* a CUDA runtime error (message in fb_last_error)                         */
     FB_ERR_NCCL = 4,        /* reserved for the multi-GPU entry points                                 */
     FB_ERR_WORKSPACE = 5,   /* no workspace set, or smaller than fb_workspace_size() requires          */
-    FB_ERR_UNSUPPORTED = 6  /* TREE + MEAN_ALIGN (accurate mode is O(N*M) by definition), p > 4  */
+    FB_ERR_UNSUPPORTED = 6  /* TREE + MEAN_ALIGN (accurate mode is O(N*M) by definition), p > 4 */
 } fb_status;
 
-/* Loss kinds: Eq. 1, Eq. 3, Eq. 8 (P:243-247 with reading D27). */
-typedef enum { FB_LOSS_BASE = 0, FB_LOSS_GUIDE_STYLE = 1, FB_LOSS_MEAN_ALIGN = 2 } fb_loss;
+/* Loss kinds: Eq. 1, Eq. 3, Eq. 8 (P:243-247 with reading D27), Eq. 10 (the
+ * keyframe alignment loss, readings D38-D40: alpha*||G_k[F_k]-G_i||^2 + ||S_k[F_k]-S_o[F_o]||^2
+ * with F_o the counterpart NNF frozen at the start of each iteration). */
+typedef enum { FB_LOSS_BASE = 0, FB_LOSS_GUIDE_STYLE = 1, FB_LOSS_MEAN_ALIGN = 2, FB_LOSS_PAIRWISE = 3 } fb_loss;
 /* Window schedules: DIRECT = balanced/accurate; TREE = fast (Alg. 3-5, Eq. 6). */
 typedef enum { FB_SCHED_DIRECT = 0, FB_SCHED_TREE = 1 } fb_schedule;
 /* NNF initialisation at the coarsest level: Philox-uniform or identity (D8/D33). */
@@ -125,9 +128,11 @@ fb_status fb_build_pyramid(fb_ctx ctx, const uint8_t* frames, int B, int H, int 
 /* ---- NNF estimation (Alg. 1) on B independent or window-coupled pairs ----------------
  * src_guide, tgt_guide: uint8 [B,H,W,3] (required).  src_style: uint8 [B,H,W,3], required unless
  * loss = BASE.  tgt_style: uint8 [B,H,W,3], required for MEAN_ALIGN only.  group: HOST int32 [B]
- * (MEAN_ALIGN only, else NULL): pairs with equal group ids share one target and one average remapped
- * image T-bar = (sum over the window, ascending src_id, of the remaps, with the target's own style at
- * its tgt_id) / (count+1), refreshed at the start of every iteration (Eq. 7, D27).
+ * (MEAN_ALIGN and PAIRWISE only, else NULL).  MEAN_ALIGN: pairs with equal group ids share one target
+ * and one average remapped image T-bar = (sum over the window, ascending src_id, of the remaps, with the
+ * target's own style at its tgt_id) / (count+1), refreshed at the start of every iteration (Eq. 7,
+ * P:237-239, D27).  PAIRWISE: group[b] is the index of pair b's counterpart (mutual, distinct): the two
+ * NNFs of one target from two keyframes, estimated jointly with Eq. 10.
  * pair_keys: HOST [B] (required).  Outputs (device, nullable except nnf_out): nnf_out int32 [B,H,W,2];
  * err_out float [B,H,W] = E after the last select (D30); remapped_out float [B,H,W,3] = Alg. 2 remap
  * of src_style with the final NNF. */
@@ -162,7 +167,9 @@ fb_status fb_blend_window_range(fb_ctx ctx, const fb_match_cfg* cfg, int schedul
  * guide uint8 [N,H,W,3]; key_index HOST int32 [K], strictly increasing in [0,N); key_style uint8
  * [K,H,W,3]; out float [N,H,W,3].  Keys are copied verbatim; a frame m between consecutive keys
  * l < m < r is fma(X_l, (r-m)/(r-l), X_r * ((m-l)/(r-l))) with X_k the remap of key k's style under
- * NNF(G_k, G_m) (GUIDE_STYLE loss); frames outside the key span take the nearest key's remap. */
+ * NNF(G_k, G_m); frames outside the key span take the nearest key's remap.  The NNFs use the GUIDE_STYLE
+ * loss, except cfg.loss = PAIRWISE: then the two NNFs of every frame between two keys are estimated
+ * jointly with the alignment loss of Eq. 10. */
 fb_status fb_interpolate_keyframes(fb_ctx ctx, const fb_match_cfg* cfg, int N, int H, int W, const uint8_t* guide,
                                    int K, const int32_t* key_index, const uint8_t* key_style, float* out,
                                    fb_stats* stats);

@@ -220,7 +220,7 @@ void validate_cfg(const fb_match_cfg* cfg)
     if (cfg->iters_per_level < 0 || cfg->levels < 0 || cfg->rs_radius0 < 0 || cfg->rs_steps < 0)
         throw Fail{FB_ERR_INVALID_ARG, "negative iteration / level / random-search parameter"};
     if (!(cfg->alpha >= 0.0f)) throw Fail{FB_ERR_INVALID_ARG, "alpha < 0"};
-    if (cfg->loss < 0 || cfg->loss > 2) throw Fail{FB_ERR_INVALID_ARG, "unknown loss"};
+    if (cfg->loss < 0 || cfg->loss > 3) throw Fail{FB_ERR_INVALID_ARG, "unknown loss"};
     if (cfg->init < 0 || cfg->init > 1) throw Fail{FB_ERR_INVALID_ARG, "unknown init"};
 }
 
@@ -303,6 +303,7 @@ struct TaskSpec {
     const float4* tg;  // target guide pyramid
     int group;         // MEAN_ALIGN window index (into groups), else -1
     uint32_t src_id, tgt_id, tag;
+    int partner = -1;  // PAIRWISE: index of the counterpart task in the batch (Eq. 10, D38)
 };
 struct GroupSpec {
     const float4* tstyle;  // target style pyramid (the self term of T-bar)
@@ -331,7 +332,9 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
         tbytes = std::max(tbytes, (size_t)g.PL[k].rows * g.PL[k].pitch * ((k == 0 && fast0) ? 16 : 32));
     tbytes = (tbytes + 255) & ~size_t(255);
     const bool per_group = cfg.loss == FB_LOSS_MEAN_ALIGN;
+    const bool pairwise = cfg.loss == FB_LOSS_PAIRWISE;
     char* tgt = ex.ar.take<char>(tbytes * (per_group ? groups.size() : (size_t)T));
+    int2* Fsnap = pairwise ? ex.ar.take<int2>((size_t)T * n0) : nullptr;  // counterpart NNFs (D39)
     std::vector<DTask> dt(T);
     for (int t = 0; t < T; ++t) {
         const TaskSpec& k = tasks[t];
@@ -341,6 +344,8 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
         dt[t].tg = k.tg;
         dt[t].c2 = k.src_id;
         dt[t].c3 = (k.tag << 28) | k.tgt_id;
+        dt[t].psrc = pairwise ? tasks[k.partner].src : nullptr;
+        dt[t].pF = pairwise ? Fsnap + (long long)k.partner * n0 : nullptr;
     }
     const DTask* d_tasks = ex.upload(dt);
     // T-bar member lists for every level (MEAN_ALIGN): ascending source id with the self term inserted.
@@ -393,7 +398,7 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
             ex.launch("upsample", [&] { return fbk::launch_upsample(F[cur], F[cur ^ 1], T, n0, g.L[k + 1], L, s); });
             cur ^= 1;
         }
-        if (cfg.loss == FB_LOSS_BASE)
+        if (cfg.loss == FB_LOSS_BASE || pairwise)  // the target operand is the target guide alone
             ex.launch("pack_tgt", [&] { return fbk::launch_pack_tgt_guide(d_tasks, T, L, PL, tfmt, s); });
         const int rk = rs_count(cfg, L), r0 = rs_r0(cfg, L);
         for (int it = 0; it < cfg.iters_per_level; ++it) {
@@ -401,6 +406,8 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
                 ex.launch("aux", [&] { return fbk::launch_aux_remap(d_tasks, T, F[cur], n0, L, PL, g.p, tfmt, s); },
                           (uint64_t)T * L.h * L.w);
                 if (st) st->remap_pixels += (uint64_t)T * L.h * L.w;
+            } else if (pairwise) {  // freeze the counterpart NNFs for this iteration (Eq. 10, D39)
+                ex.d2d(Fsnap, F[cur], sizeof(int2) * (size_t)T * n0);
             } else if (per_group) {  // T-bar refresh (Eq. 7, D27)
                 ex.launch(k == 0 ? "tbar.L0" : "tbar.L1+", [&] { return fbk::launch_combine(d_outs[k], (int)groups.size(), d_mem[k], F[cur], n0,
                                                                    L.h, L.w, g.p, fast ? 2 : 3, PL, s); },
@@ -716,8 +723,9 @@ void blend_tree(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N_total, i
 void interpolate(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N, const uint8_t* guide, int K,
                  const int32_t* keys, const uint8_t* key_style, float* out, fb_stats* st)
 {
-    fb_match_cfg cfg = cfg0;
-    cfg.loss = FB_LOSS_GUIDE_STYLE;
+    // cfg.loss == PAIRWISE: frames between two keys estimate both NNFs jointly with the alignment loss
+    // of Eq. 10 (D38-D40); single-key frames and all other losses use Eq. 3 (GUIDE_STYLE).
+    const bool align = cfg0.loss == FB_LOSS_PAIRWISE;
     const Pyr G = pyramid_u8(ex, g, guide, N);
     const Pyr KS = pyramid_u8(ex, g, key_style, K);
     const long long n0 = g.npx0();
@@ -726,8 +734,7 @@ void interpolate(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N, const 
         specs.push_back(SlotSpec{guide + 3 * n0 * keys[k], key_style + 3 * n0 * k, G.frame(keys[k]), KS.frame(k)});
     const Slots KSl = pack_sources(ex, g, fbk::SF8, specs);
     struct Tgt { int m, left, right, key; };  // key indices (or -1)
-    std::vector<Tgt> tg;
-    std::vector<int> cost;
+    std::vector<Tgt> tg[2];  // [0]: keys and GUIDE_STYLE targets, [1]: aligned (two-key) targets
     for (int m = 0; m < N; ++m) {
         Tgt t{m, -1, -1, -1};
         for (int k = 0; k < K; ++k) {
@@ -735,49 +742,58 @@ void interpolate(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N, const 
             if (keys[k] < m) t.left = k;
             if (keys[k] > m && t.right < 0) t.right = k;
         }
-        tg.push_back(t);
-        cost.push_back(t.key >= 0 ? 0 : (t.left >= 0) + (t.right >= 0));
+        tg[align && t.key < 0 && t.left >= 0 && t.right >= 0 ? 1 : 0].push_back(t);
     }
     const size_t mark = ex.ar.off;
-    for (auto [b0, b1] : make_batches(cost, batch_pairs(ex.ctx, g, cfg.loss))) {
-        ex.ar.off = mark;
-        std::vector<TaskSpec> tasks;
-        std::vector<int> tl(b1 - b0, -1), tr(b1 - b0, -1);
-        for (int q = b0; q < b1; ++q) {
-            const Tgt& t = tg[q];
-            if (t.key >= 0) continue;
-            if (t.left >= 0) {
-                tl[q - b0] = (int)tasks.size();
-                tasks.push_back(TaskSpec{KSl.slot(t.left), KS.frame(t.left), G.frame(t.m), -1, (uint32_t)keys[t.left],
-                                         (uint32_t)t.m, 5u});
+    for (int pass = 0; pass < 2; ++pass) {
+        fb_match_cfg cfg = cfg0;
+        cfg.loss = pass == 1 ? FB_LOSS_PAIRWISE : FB_LOSS_GUIDE_STYLE;
+        std::vector<int> cost;
+        for (const Tgt& t : tg[pass]) cost.push_back(t.key >= 0 ? 0 : (t.left >= 0) + (t.right >= 0));
+        for (auto [b0, b1] : make_batches(cost, batch_pairs(ex.ctx, g, cfg.loss))) {
+            ex.ar.off = mark;
+            std::vector<TaskSpec> tasks;
+            std::vector<int> tl(b1 - b0, -1), tr(b1 - b0, -1);
+            for (int q = b0; q < b1; ++q) {
+                const Tgt& t = tg[pass][q];
+                if (t.key >= 0) continue;
+                if (t.left >= 0) {
+                    tl[q - b0] = (int)tasks.size();
+                    tasks.push_back(TaskSpec{KSl.slot(t.left), KS.frame(t.left), G.frame(t.m), -1,
+                                             (uint32_t)keys[t.left], (uint32_t)t.m, 5u});
+                }
+                if (t.right >= 0) {
+                    tr[q - b0] = (int)tasks.size();
+                    tasks.push_back(TaskSpec{KSl.slot(t.right), KS.frame(t.right), G.frame(t.m), -1,
+                                             (uint32_t)keys[t.right], (uint32_t)t.m, 5u});
+                }
+                if (pass == 1) {  // counterparts (Eq. 10)
+                    tasks[tl[q - b0]].partner = tr[q - b0];
+                    tasks[tr[q - b0]].partner = tl[q - b0];
+                }
             }
-            if (t.right >= 0) {
-                tr[q - b0] = (int)tasks.size();
-                tasks.push_back(TaskSpec{KSl.slot(t.right), KS.frame(t.right), G.frame(t.m), -1,
-                                         (uint32_t)keys[t.right], (uint32_t)t.m, 5u});
+            BatchOut bo;
+            if (!tasks.empty()) bo = run_nnf(ex, cfg, g, KSl, tasks, {}, st);
+            CombineList cl;
+            for (int q = b0; q < b1; ++q) {
+                const Tgt& t = tg[pass][q];
+                cl.begin();
+                if (t.key >= 0) {
+                    cl.add_img(KS.frame(t.key), 1.0f);  // keyframes are not modified
+                } else if (t.left < 0 || t.right < 0) {
+                    const int k = t.left >= 0 ? t.left : t.right;
+                    cl.add_remap(KS.frame(k), t.left >= 0 ? tl[q - b0] : tr[q - b0], 1.0f);
+                } else {
+                    const int l = keys[t.left], r = keys[t.right], m = t.m;
+                    const float wl = (float)(r - m) / (float)(r - l), wr = (float)(m - l) / (float)(r - l);
+                    cl.add_remap(KS.frame(t.right), tr[q - b0], wr);  // A = X_r * w_r, then fma(X_l, w_l, A)
+                    cl.add_remap(KS.frame(t.left), tl[q - b0], wl);
+                }
+                cl.end(out + 3LL * n0 * t.m, 1, 1.0f);
             }
+            if (st) st->remap_pixels += (uint64_t)tasks.size() * n0;
+            run_combine(ex, g, 0, cl, bo.F, bo.fstride);
         }
-        BatchOut bo;
-        if (!tasks.empty()) bo = run_nnf(ex, cfg, g, KSl, tasks, {}, st);
-        CombineList cl;
-        for (int q = b0; q < b1; ++q) {
-            const Tgt& t = tg[q];
-            cl.begin();
-            if (t.key >= 0) {
-                cl.add_img(KS.frame(t.key), 1.0f);  // keyframes are not modified
-            } else if (t.left < 0 || t.right < 0) {
-                const int k = t.left >= 0 ? t.left : t.right;
-                cl.add_remap(KS.frame(k), t.left >= 0 ? tl[q - b0] : tr[q - b0], 1.0f);
-            } else {
-                const int l = keys[t.left], r = keys[t.right], m = t.m;
-                const float wl = (float)(r - m) / (float)(r - l), wr = (float)(m - l) / (float)(r - l);
-                cl.add_remap(KS.frame(t.right), tr[q - b0], wr);  // A = X_r * w_r, then fma(X_l, w_l, A)
-                cl.add_remap(KS.frame(t.left), tl[q - b0], wl);
-            }
-            cl.end(out + 3LL * n0 * t.m, 1, 1.0f);
-        }
-        if (st) st->remap_pixels += (uint64_t)tasks.size() * n0;
-        run_combine(ex, g, 0, cl, bo.F, bo.fstride);
     }
 }
 
@@ -815,6 +831,11 @@ void nnf_api(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int B, const uint8
         }
         tasks.push_back(TaskSpec{SL.slot(b), cfg.loss != FB_LOSS_BASE ? SS.frame(b) : nullptr, TG.frame(b), gi,
                                  (uint32_t)keys[b].src_id, (uint32_t)keys[b].tgt_id, (uint32_t)keys[b].task_tag});
+        if (cfg.loss == FB_LOSS_PAIRWISE) {
+            if (group[b] < 0 || group[b] >= B || group[group[b]] != b || group[b] == b)
+                throw Fail{FB_ERR_INVALID_ARG, "PAIRWISE: group[b] must name a distinct counterpart pair (mutual)"};
+            tasks.back().partner = group[b];
+        }
     }
     BatchOut bo = run_nnf(ex, cfg, g, SL, tasks, groups, st);
     const long long n0 = g.npx0();
@@ -983,6 +1004,7 @@ static void validate_nnf(const fb_match_cfg* cfg, int B, int H, int W, const uin
     if (!sg || !tg || !keys || !nnf_out) throw Fail{FB_ERR_INVALID_ARG, "NULL required pointer"};
     if (cfg->loss != FB_LOSS_BASE && !ss) throw Fail{FB_ERR_INVALID_ARG, "src_style required for this loss"};
     if (cfg->loss == FB_LOSS_MEAN_ALIGN && (!ts || !group)) throw Fail{FB_ERR_INVALID_ARG, "MEAN_ALIGN needs tgt_style and group"};
+    if (cfg->loss == FB_LOSS_PAIRWISE && !group) throw Fail{FB_ERR_INVALID_ARG, "PAIRWISE needs group (counterparts)"};
     for (int b = 0; b < B; ++b)
         if (keys[b].src_id < 0 || keys[b].tgt_id < 0 || keys[b].tgt_id >= (1 << 28) || keys[b].task_tag < 0 ||
             keys[b].task_tag > 15)
@@ -1012,7 +1034,8 @@ static void blend_range_body(Exec& ex, fb_stats* st, const fb_match_cfg* cfg, in
     if (schedule != FB_SCHED_DIRECT && schedule != FB_SCHED_TREE) throw Fail{FB_ERR_INVALID_ARG, "unknown schedule"};
     if (schedule == FB_SCHED_TREE && cfg->loss == FB_LOSS_MEAN_ALIGN)
         throw Fail{FB_ERR_UNSUPPORTED, "accurate mode (MEAN_ALIGN) is defined only for the direct schedule (P:249)"};
-    if (cfg->loss == FB_LOSS_BASE) throw Fail{FB_ERR_INVALID_ARG, "blending needs GUIDE_STYLE or MEAN_ALIGN"};
+    if (cfg->loss == FB_LOSS_BASE || cfg->loss == FB_LOSS_PAIRWISE)
+        throw Fail{FB_ERR_INVALID_ARG, "blending needs GUIDE_STYLE or MEAN_ALIGN"};
     if (!guide || !style || !out) throw Fail{FB_ERR_INVALID_ARG, "NULL required pointer"};
     if (t0 < 0 || t1 > N_total || t0 >= t1) throw Fail{FB_ERR_INVALID_ARG, "bad target range"};
     if (f0 < 0 || N < 1 || f0 + N > N_total || f0 > std::max(0, t0 - M) || f0 + N < std::min(N_total, t1 + M))
@@ -1079,6 +1102,8 @@ size_t fb_workspace_size(fb_ctx ctx, int op, const fb_match_cfg* cfg, int n, int
     if (op == FB_OP_NNF) {
         std::vector<fb_pair_key> keys(n, fb_pair_key{0, 0, 6});
         std::vector<int32_t> grp(n, 0);
+        if (cfg->loss == FB_LOSS_PAIRWISE)
+            for (int b = 0; b < n; ++b) grp[b] = (b ^ 1) < n ? (b ^ 1) : b;
         s = guarded(ctx, nullptr, [&](Exec& ex, fb_stats* st) {
             validate_cfg(cfg);
             const Geo g = make_geo(*cfg, H, W);

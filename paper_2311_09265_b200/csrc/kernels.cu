@@ -389,12 +389,32 @@ __device__ __forceinline__ float partial_loss(float alpha, float dg, float ds, b
     return two ? __fmaf_rn(alpha, dg, ds) : dg;
 }
 
+// Eq. 10 (PAIRWISE, D38/D39): the reference side of the second term is the counterpart keyframe's
+// style patch centred at the counterpart's NNF (frozen at the iteration start), gathered once per pixel
+// from its packed SF8 slot (zero border = zero padding, D9) and held in registers like a target patch.
+template <int P>
+__device__ __forceinline__ void load_pairwise_patch(const DTask& T, const FieldArgs& a, int i,
+                                                    float (&pa)[2 * P + 1][2 * P + 1][3])
+{
+    const int2 q = __ldg(&T.pF[i]);
+    const uint32_t* PS = reinterpret_cast<const uint32_t*>(T.psrc + a.src_off);
+#pragma unroll
+    for (int dr = 0; dr < 2 * P + 1; ++dr)
+#pragma unroll
+        for (int dc = 0; dc < 2 * P + 1; ++dc) {
+            const uint32_t sv = __ldg(PS + 2 * ((q.x + dr - P + B) * a.L.pitch + (q.y + dc - P + B)) + 1);
+            pa[dr][dc][0] = u8f(sv, 0);
+            pa[dr][dc][1] = u8f(sv, 1);
+            pa[dr][dc][2] = u8f(sv, 2);
+        }
+}
+
 // ---- fast variant: SF8 source, TF16 target, target patch in registers (P <= 2) -------------------
 // Guide term: at level 0 every guide value is an integer 0..255, every partial sum of the FP32 chain
 // is an integer below 2^24 (p <= 4), so the chain is exact and equals the integer SSD computed with
 // byte-wise |a-b| and dp4a; it is converted once, exactly.  Style term: the FP32 chain of D20 with the
 // u8 source channel converted exactly (u8f).
-template <int P, bool TWO, int PHASE>
+template <int P, bool TWO, int PHASE, bool PW = false>
 __global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
 {
     constexpr int D = 2 * P + 1;
@@ -421,6 +441,7 @@ __global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
             tgA[dr][dc][1] = __uint_as_float(v.z);
             tgA[dr][dc][2] = __uint_as_float(v.w);
         }
+    if (PW) load_pairwise_patch<P>(T, a, r * w + c, tgA);
     // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
     auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
         const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
@@ -520,6 +541,7 @@ static constexpr int IT_TX = 30, IT_TY = 4;
 template <int P, bool TWO>
 __global__ void __launch_bounds__(32 * (IT_TY + 1), IT_MINB) k_iter_fast(FieldArgs a)
 {
+    constexpr bool PW = false;
     constexpr int D = 2 * P + 1;
     constexpr int NCH = (D + 2) / 2;
     __shared__ int2 sF0[IT_TY + 1][32];
@@ -546,6 +568,7 @@ __global__ void __launch_bounds__(32 * (IT_TY + 1), IT_MINB) k_iter_fast(FieldAr
                 tgA[dr][dc][1] = __uint_as_float(v.z);
                 tgA[dr][dc][2] = __uint_as_float(v.w);
             }
+        if (PW) load_pairwise_patch<P>(T, a, r * w + c, tgA);
     }
     // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
     auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
@@ -660,7 +683,7 @@ __global__ void __launch_bounds__(32 * (IT_TY + 1), IT_MINB) k_iter_fast(FieldAr
 // pixels see exactly the Jacobi inputs of the per-field launches.  No shared memory, no barrier.
 static constexpr int I13_TY = 4;
 
-template <int P, bool TWO>
+template <int P, bool TWO, bool PW = false>
 __global__ void __launch_bounds__(32 * I13_TY, 3) k_iter13_fast(FieldArgs a)
 {
     constexpr int D = 2 * P + 1;
@@ -688,6 +711,7 @@ __global__ void __launch_bounds__(32 * I13_TY, 3) k_iter13_fast(FieldArgs a)
                 tgA[dr][dc][1] = __uint_as_float(v.z);
                 tgA[dr][dc][2] = __uint_as_float(v.w);
             }
+        if (PW) load_pairwise_patch<P>(T, a, r * w + c, tgA);
     }
     // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
     auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
@@ -788,7 +812,7 @@ __global__ void __launch_bounds__(32 * I13_TY, 3) k_iter13_fast(FieldArgs a)
 
 // ---- general variant: SF32 source, TF32 target staged in shared memory (any level, P <= 4) -------
 
-template <int P, bool TWO, int PHASE, int SFMT>
+template <int P, bool TWO, int PHASE, int SFMT, bool PW = false>
 __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
 {
     constexpr int D = 2 * P + 1, SX = TILE_X + 2 * P, SY = TILE_Y + 2 * P;
@@ -820,6 +844,28 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
     const float4* S = reinterpret_cast<const float4*>(T.src + a.src_off);
     const uint4* S16 = reinterpret_cast<const uint4*>(T.src + a.src_off);
     const uint32_t ex = (uint32_t)(75 - a.L.k) << 24;
+    float pa[PW ? D : 1][PW ? D : 1][3];  // PAIRWISE reference patch (Eq. 10, D39)
+    if (PW) {
+        const int2 q = __ldg(&T.pF[r * w + c]);
+#pragma unroll
+        for (int dr = 0; dr < D; ++dr)
+#pragma unroll
+            for (int dc = 0; dc < D; ++dc) {
+                const int idx = (q.x + dr - P + B) * pitch + (q.y + dc - P + B);
+                if (SFMT == SF16) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4*>(T.psrc + a.src_off) + idx);
+                    pa[PW ? dr : 0][PW ? dc : 0][0] = u16f(v.z, 0x7410u, ex);
+                    pa[PW ? dr : 0][PW ? dc : 0][1] = u16f(v.z, 0x7432u, ex);
+                    pa[PW ? dr : 0][PW ? dc : 0][2] = u16f(v.w, 0x7410u, ex);
+                } else {
+                    const float4 v0 = __ldg(reinterpret_cast<const float4*>(T.psrc + a.src_off) + 2 * idx);
+                    const float4 v1 = __ldg(reinterpret_cast<const float4*>(T.psrc + a.src_off) + 2 * idx + 1);
+                    pa[PW ? dr : 0][PW ? dc : 0][0] = v0.w;
+                    pa[PW ? dr : 0][PW ? dc : 0][1] = v1.x;
+                    pa[PW ? dr : 0][PW ? dc : 0][2] = v1.y;
+                }
+            }
+    }
     auto row = [&](int sr, int sc, int dr, float& dg, float& ds) {
         const int base = (sr + dr - P + B) * pitch + (sc - P + B);
         float rg = 0.0f, rs = 0.0f;
@@ -841,10 +887,17 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
             dl = __fsub_rn(q0.y, s0.y); rg = __fmaf_rn(dl, dl, rg);
             dl = __fsub_rn(q0.z, s0.z); rg = __fmaf_rn(dl, dl, rg);
             if (TWO) {
-                const float2 q1 = t1[ly + dr][lx + dc];
-                dl = __fsub_rn(q0.w, s0.w); rs = __fmaf_rn(dl, dl, rs);
-                dl = __fsub_rn(q1.x, s1.x); rs = __fmaf_rn(dl, dl, rs);
-                dl = __fsub_rn(q1.y, s1.y); rs = __fmaf_rn(dl, dl, rs);
+                float ar, ag, ab;
+                if (PW) {
+                    ar = pa[PW ? dr : 0][PW ? dc : 0][0]; ag = pa[PW ? dr : 0][PW ? dc : 0][1];
+                    ab = pa[PW ? dr : 0][PW ? dc : 0][2];
+                } else {
+                    const float2 q1 = t1[ly + dr][lx + dc];
+                    ar = q0.w; ag = q1.x; ab = q1.y;
+                }
+                dl = __fsub_rn(ar, s0.w); rs = __fmaf_rn(dl, dl, rs);
+                dl = __fsub_rn(ag, s1.x); rs = __fmaf_rn(dl, dl, rs);
+                dl = __fsub_rn(ab, s1.y); rs = __fmaf_rn(dl, dl, rs);
             }
         }
         dg = __fadd_rn(dg, rg);
@@ -993,27 +1046,27 @@ cudaError_t launch_remap_f3(const float* src, const int2* F, float* out, int Bn,
     return cudaGetLastError();
 }
 
-template <int P, bool TWO, int SFMT>
+template <int P, bool TWO, int SFMT, bool PW = false>
 static void launch_field_gen(const FieldArgs& a, int T, int phase, cudaStream_t s)
 {
     const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(TILE_X * TILE_Y);
     switch (phase) {
-    case 0: k_field_gen<P, TWO, 0, SFMT><<<grid, block, 0, s>>>(a); break;
-    case 1: k_field_gen<P, TWO, 1, SFMT><<<grid, block, 0, s>>>(a); break;
-    case 2: k_field_gen<P, TWO, 2, SFMT><<<grid, block, 0, s>>>(a); break;
-    default: k_field_gen<P, TWO, 3, SFMT><<<grid, block, 0, s>>>(a); break;
+    case 0: k_field_gen<P, TWO, 0, SFMT, PW><<<grid, block, 0, s>>>(a); break;
+    case 1: k_field_gen<P, TWO, 1, SFMT, PW><<<grid, block, 0, s>>>(a); break;
+    case 2: k_field_gen<P, TWO, 2, SFMT, PW><<<grid, block, 0, s>>>(a); break;
+    default: k_field_gen<P, TWO, 3, SFMT, PW><<<grid, block, 0, s>>>(a); break;
     }
 }
 
-template <int P, bool TWO>
+template <int P, bool TWO, bool PW = false>
 static void launch_field_fast(const FieldArgs& a, int T, int phase, cudaStream_t s)
 {
     const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(TILE_X * FAST_TY);
     switch (phase) {
-    case 0: k_field_fast<P, TWO, 0><<<grid, block, 0, s>>>(a); break;
-    case 1: k_field_fast<P, TWO, 1><<<grid, block, 0, s>>>(a); break;
-    case 2: k_field_fast<P, TWO, 2><<<grid, block, 0, s>>>(a); break;
-    default: k_field_fast<P, TWO, 3><<<grid, block, 0, s>>>(a); break;
+    case 0: k_field_fast<P, TWO, 0, PW><<<grid, block, 0, s>>>(a); break;
+    case 1: k_field_fast<P, TWO, 1, PW><<<grid, block, 0, s>>>(a); break;
+    case 2: k_field_fast<P, TWO, 2, PW><<<grid, block, 0, s>>>(a); break;
+    default: k_field_fast<P, TWO, 3, PW><<<grid, block, 0, s>>>(a); break;
     }
 }
 
@@ -1035,9 +1088,17 @@ cudaError_t launch_iter13_fast(const FieldArgs& a0, int T, int p, int loss, cuda
     a.tiles_x = (a.L.w + IT_TX - 1) / IT_TX;
     a.tiles_per_task = a.tiles_x * ((a.L.h + I13_TY - 1) / I13_TY);
     const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(32 * I13_TY);
-    if (p == 1) { if (loss) k_iter13_fast<1, true><<<grid, block, 0, s>>>(a); else k_iter13_fast<1, false><<<grid, block, 0, s>>>(a); }
-    else if (p == 2) { if (loss) k_iter13_fast<2, true><<<grid, block, 0, s>>>(a); else k_iter13_fast<2, false><<<grid, block, 0, s>>>(a); }
-    else return cudaErrorInvalidValue;
+    if (p == 1) {
+        if (loss == 3) k_iter13_fast<1, true, true><<<grid, block, 0, s>>>(a);
+        else if (loss) k_iter13_fast<1, true><<<grid, block, 0, s>>>(a);
+        else k_iter13_fast<1, false><<<grid, block, 0, s>>>(a);
+    } else if (p == 2) {
+        if (loss == 3) k_iter13_fast<2, true, true><<<grid, block, 0, s>>>(a);
+        else if (loss) k_iter13_fast<2, true><<<grid, block, 0, s>>>(a);
+        else k_iter13_fast<2, false><<<grid, block, 0, s>>>(a);
+    } else {
+        return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 
@@ -1046,14 +1107,33 @@ cudaError_t launch_field(const FieldArgs& a0, int T, int p, int loss, int phase,
     FieldArgs a = a0;
     a.tiles_x = (a.L.w + TILE_X - 1) / TILE_X;
     a.tiles_per_task = a.tiles_x * ((a.L.h + (fast ? FAST_TY : TILE_Y) - 1) / (fast ? FAST_TY : TILE_Y));
+    const bool pw = loss == 3;
     if (fast) {
-        if (p == 1) { loss ? launch_field_fast<1, true>(a, T, phase, s) : launch_field_fast<1, false>(a, T, phase, s); }
-        else if (p == 2) { loss ? launch_field_fast<2, true>(a, T, phase, s) : launch_field_fast<2, false>(a, T, phase, s); }
-        else return cudaErrorInvalidValue;
+        if (p == 1) {
+            if (pw) launch_field_fast<1, true, true>(a, T, phase, s);
+            else if (loss) launch_field_fast<1, true>(a, T, phase, s);
+            else launch_field_fast<1, false>(a, T, phase, s);
+        } else if (p == 2) {
+            if (pw) launch_field_fast<2, true, true>(a, T, phase, s);
+            else if (loss) launch_field_fast<2, true>(a, T, phase, s);
+            else launch_field_fast<2, false>(a, T, phase, s);
+        } else {
+            return cudaErrorInvalidValue;
+        }
     } else if (a.src_fmt == SF16) {
-        if (p == 1) { loss ? launch_field_gen<1, true, SF16>(a, T, phase, s) : launch_field_gen<1, false, SF16>(a, T, phase, s); }
-        else if (p == 2) { loss ? launch_field_gen<2, true, SF16>(a, T, phase, s) : launch_field_gen<2, false, SF16>(a, T, phase, s); }
-        else return cudaErrorInvalidValue;
+        if (p == 1) {
+            if (pw) launch_field_gen<1, true, SF16, true>(a, T, phase, s);
+            else if (loss) launch_field_gen<1, true, SF16>(a, T, phase, s);
+            else launch_field_gen<1, false, SF16>(a, T, phase, s);
+        } else if (p == 2) {
+            if (pw) launch_field_gen<2, true, SF16, true>(a, T, phase, s);
+            else if (loss) launch_field_gen<2, true, SF16>(a, T, phase, s);
+            else launch_field_gen<2, false, SF16>(a, T, phase, s);
+        } else {
+            return cudaErrorInvalidValue;
+        }
+    } else if (pw) {
+        FB_DISPATCH_P(p, (launch_field_gen<PP, true, SF32, true>(a, T, phase, s)));
     } else if (loss == 0) {
         FB_DISPATCH_P(p, (launch_field_gen<PP, false, SF32>(a, T, phase, s)));
     } else {

@@ -33,6 +33,8 @@ struct DTask {
     const float4* tg;  // target guide float4 pyramid (guide half of the packed target)
     uint32_t c2;       // Philox counter word 2: source frame id (D21)
     uint32_t c3;       // Philox counter word 3: tag << 28 | target frame id (D21)
+    const char* psrc;  // PAIRWISE (Eq. 10): the counterpart task's packed source slot (its keyframe style)
+    const int2* pF;    // PAIRWISE: the counterpart's NNF at the start of the iteration (D39), [h_k*w_k]
 };
 
 // Geometry of one pyramid level (unpadded float4 pyramids).
@@ -108,6 +110,7 @@ cudaError_t launch_combine(const DOut* outs, int n_outs, const DMember* mem, con
                            int h, int w, int p, int fmt, PLvl P, cudaStream_t s);
 // phase 0: E init + propagation (-1,0); 1: (+1,0); 2: (0,-1); 3: (0,+1) + all random-search steps.
 // fast = SF8/TF16 operands (target patch in registers); otherwise SF32/TF32 (target tile in smem).
+// loss: fb_loss (0 BASE, 1 GUIDE_STYLE, 2 MEAN_ALIGN, 3 PAIRWISE).
 cudaError_t launch_field(const FieldArgs& a, int T, int p, int loss, int phase, bool fast, cudaStream_t s);
 // The whole updating sequence of one iteration (E init, four propagation fields, random search) in one
 // launch, fast operands only (SF8/TF16, p <= 2).  Fin -> Fout, E written.

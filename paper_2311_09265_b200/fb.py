@@ -15,7 +15,7 @@ import torch
 
 from . import build as _build
 
-BASE, GUIDE_STYLE, MEAN_ALIGN = 0, 1, 2
+BASE, GUIDE_STYLE, MEAN_ALIGN, PAIRWISE = 0, 1, 2, 3
 DIRECT, TREE = 0, 1
 INIT_RANDOM, INIT_IDENTITY = 0, 1
 OP_NNF, OP_BLEND_DIRECT, OP_BLEND_TREE, OP_INTERPOLATE = 0, 1, 2, 3

@@ -62,11 +62,13 @@ def test_config3_fast_200x512_window30(P, ctx, video512):
     check(out[targets], ref)
 
 
-def test_config4_interpolation_768(P, ctx):
-    """configs[3]: 2 keyframes (0 and 101) rendering the 100 in-between 768^2 frames."""
+@pytest.mark.parametrize("align", [False, True])
+def test_config4_interpolation_768(P, ctx, align):
+    """configs[3]: 2 keyframes (0 and 101) rendering the 100 in-between 768^2 frames (with and without
+    the Eq. 10 alignment of the two NNFs)."""
     g, s = moving_texture(102, 768, 768, seed=4)
     keys = [0, 101]
-    cfg = P.MatchCfg(loss=P.GUIDE_STYLE)
+    cfg = P.MatchCfg(loss=P.PAIRWISE if align else P.GUIDE_STYLE)
     out, st = ctx.fb_interpolate_keyframes(cfg, torch.from_numpy(g).cuda(), keys, torch.from_numpy(s[keys]).cuda())
     assert st["nnf_pairs"] == 200
     targets = [0, 1, 50, 100]

@@ -256,3 +256,44 @@ def test_streaming_workspace_is_O_window(fb):
     assert w2000 == w200
     full = fb.Context(0).workspace_size(fb.fb.OP_BLEND_DIRECT, cfg, 2000, 512, 512, 15)
     assert w2000 < full / 5
+
+
+# ------------------------------------------------------------------------------ f1 alignment (Eq. 10)
+@pytest.mark.parametrize("p,H,W", [(2, 64, 64), (1, 45, 77), (2, 45, 77), (3, 40, 52)])
+def test_pairwise_nnf_matches_oracle(fb, ctx, p, H, W):
+    g, s = moving_texture(3, H, W, seed=21 + p)
+    cfg = fb.MatchCfg(patch_radius=p, iters_per_level=2, loss=fb.PAIRWISE, alpha=4.0)
+    sg = np.stack([g[0], g[2]])
+    tg = np.stack([g[1], g[1]])
+    ss = np.stack([s[0], s[2]])
+    F, E, X, st = ctx.fb_nnf_estimate(cfg, dev(sg), dev(tg), dev(ss), group=[1, 0],
+                                      pair_keys=[(0, 1, 5), (2, 1, 5)])
+    frames = np.concatenate([g, s[[0, 2]]]).astype(np.float32)
+    tasks = [dict(src_guide=0, tgt_guide=1, src_style=3, src_id=0, tgt_id=1, tag=5, partner=1),
+             dict(src_guide=2, tgt_guide=1, src_style=4, src_id=2, tgt_id=1, tag=5, partner=0)]
+    Fr, Er, Xr, ev = O.nnf(ocfg(cfg), frames, tasks)
+    assert st["candidate_evals"] == ev
+    assert_nnf(F, E, Fr, Er)
+    assert_frames(X, Xr)
+
+
+@pytest.mark.parametrize("keys", [[0, 7], [2, 5, 9], [4]])
+def test_aligned_interpolation_parity(fb, ctx, keys):
+    N = 10
+    g, s = moving_texture(N, 40, 48, seed=18)
+    cfg = fb.MatchCfg(iters_per_level=2, loss=fb.PAIRWISE)
+    out, st = ctx.fb_interpolate_keyframes(cfg, dev(g), keys, dev(s[keys]))
+    ref, pairs, evals = O.interpolate(ocfg(cfg), g, keys, s[keys])
+    assert st["nnf_pairs"] == pairs and st["candidate_evals"] == evals
+    assert_frames(out, ref)
+
+
+def test_pairwise_rejects_bad_counterparts(fb, ctx):
+    g, s = moving_texture(3, 32, 32)
+    cfg = fb.MatchCfg(loss=fb.PAIRWISE)
+    with pytest.raises(fb.FBError) as e:
+        ctx.fb_nnf_estimate(cfg, dev(g[:2]), dev(g[1:]), dev(s[:2]), group=[1, 1], pair_keys=[(0, 1, 5), (2, 1, 5)])
+    assert e.value.status == 1
+    with pytest.raises(fb.FBError) as e:
+        ctx.fb_blend_window(cfg, fb.DIRECT, dev(g), dev(s), 1)
+    assert e.value.status == 1
