@@ -66,6 +66,9 @@ typedef struct {
     int32_t loss;            /* fb_loss                                                             */
     int32_t init;            /* fb_init                                                             */
     uint64_t seed;           /* Philox4x32-10 key (D21)                                             */
+    int32_t prop_scales;     /* propagation scales J (jump flood, D41): steps 2^(J-1)..1, each with the
+                                four directions of P:72; 0 or 1 = the paper's unit-step propagation   */
+    int32_t reserved;        /* must be 0                                                           */
 } fb_match_cfg;
 
 typedef struct {

@@ -40,6 +40,8 @@ typedef struct {
     int32_t loss;            /* 0 BASE (Eq. 1), 1 GUIDE_STYLE (Eq. 3), 2 MEAN_ALIGN (Eq. 8), 3 PAIRWISE (Eq. 10) */
     int32_t init;            /* 0 random, 1 identity (D8)                              */
     uint64_t seed;           /* Philox key (D21)                                              */
+    int32_t prop_scales;     /* J propagation scales, steps 2^(J-1)..1 (jump flood, D41); 0/1 = P:72 */
+    int32_t reserved;
 } orc_cfg;
 
 enum { ORC_BASE = 0, ORC_GUIDE_STYLE = 1, ORC_MEAN_ALIGN = 2, ORC_PAIRWISE = 3 };
@@ -214,6 +216,9 @@ static int rs_radius(const orc_cfg* cfg, int hk, int wk, int s)
     return R < 1 ? 1 : R;
 }
 
+/* D41: number of propagation scales (1 = the paper's unit-step propagation) */
+static int prop_scales(const orc_cfg* cfg) { return cfg->prop_scales > 1 ? cfg->prop_scales : 1; }
+
 uint64_t orc_evals_per_task(const orc_cfg* cfg, int H, int W)
 {
     int lv = orc_level_count(H, W, cfg->patch_radius, cfg->levels);
@@ -221,7 +226,7 @@ uint64_t orc_evals_per_task(const orc_cfg* cfg, int H, int W)
     uint64_t n = 0;
     for (int k = 0; k < lv; ++k) {
         int hk = H >> k, wk = W >> k;
-        n += (uint64_t)hk * wk * cfg->iters_per_level * (uint64_t)(1 + 4 + rs_count(cfg, hk, wk));
+        n += (uint64_t)hk * wk * cfg->iters_per_level * (uint64_t)(1 + 4 * prop_scales(cfg) + rs_count(cfg, hk, wk));
     }
     return n;
 }
@@ -259,14 +264,15 @@ static float level_loss(const orc_level_ctx* L, int r, int c, int sr, int sc)
  *   field = -1: E <- L(F)
  *   field = 0..3: propagation F'(x,y) = F(x+dx, y+dy) - (dx,dy) with (dx,dy) = (-1,0),(1,0),(0,-1),(0,1)
  *                 (P:72), neighbour index clamped (D11), candidate clamped to the source (D10);
- *                 Jacobi: every pixel reads the F of the previous field
+ *                 Jacobi: every pixel reads the F of the previous field.  With a jump-flood
+ *                 step s (D41) the neighbour is x + s*d and the candidate F(x + s*d) - s*d.
  *   field = 4+s: random search step s: F'(x,y) = F(x,y) + (dx,dy), dx,dy uniform integers in [-R_s, R_s]
  *                 with R_s = r0 >> s (D13) from the Philox stream of D21
  * followed by the strict-min select F(E'<E) <- F'(E'<E), E(E'<E) <- E'(E'<E).
  * F, E are updated in place; Fo/Eo are scratch of the same size. */
 static const int PROP_DIRS[4][2] = { { -1, 0 }, { 1, 0 }, { 0, -1 }, { 0, 1 } };
 
-static void level_field(const orc_level_ctx* L, const orc_cfg* cfg, int field, int k, int it, int src_id,
+static void level_field(const orc_level_ctx* L, const orc_cfg* cfg, int field, int step, int k, int it, int src_id,
                         int tgt_id, int tag, int32_t* F, float* E, int32_t* Fo, float* Eo)
 {
     int h = L->h, w = L->w;
@@ -281,7 +287,7 @@ static void level_field(const orc_level_ctx* L, const orc_cfg* cfg, int field, i
         return;
     }
     if (field < 4) {
-        int dx = PROP_DIRS[field][0], dy = PROP_DIRS[field][1];
+        int dx = step * PROP_DIRS[field][0], dy = step * PROP_DIRS[field][1];
 #pragma omp parallel for schedule(static)
         for (int r = 0; r < h; ++r)
             for (int c = 0; c < w; ++c) {
@@ -320,7 +326,19 @@ void orc_field(const orc_cfg* cfg, int h, int w, const float* sg, const float* t
     orc_level_ctx L = { h, w, cfg->patch_radius, cfg->loss, cfg->alpha, sg, tg, ss, aux, NULL, NULL };
     int32_t* Fo = (int32_t*)malloc(sizeof(int32_t) * 2 * (size_t)h * w);
     float* Eo = (float*)malloc(sizeof(float) * (size_t)h * w);
-    level_field(&L, cfg, field, k, it, src_id, tgt_id, tag, F, E, Fo, Eo);
+    level_field(&L, cfg, field, 1, k, it, src_id, tgt_id, tag, F, E, Fo, Eo);
+    free(Fo); free(Eo);
+}
+
+/* Same with a propagation step (jump flood, D41). */
+void orc_field_step(const orc_cfg* cfg, int h, int w, const float* sg, const float* tg, const float* ss,
+                    const float* aux, int field, int step, int k, int it, int src_id, int tgt_id, int tag,
+                    int32_t* F, float* E)
+{
+    orc_level_ctx L = { h, w, cfg->patch_radius, cfg->loss, cfg->alpha, sg, tg, ss, aux, NULL, NULL };
+    int32_t* Fo = (int32_t*)malloc(sizeof(int32_t) * 2 * (size_t)h * w);
+    float* Eo = (float*)malloc(sizeof(float) * (size_t)h * w);
+    level_field(&L, cfg, field, step, k, it, src_id, tgt_id, tag, F, E, Fo, Eo);
     free(Fo); free(Eo);
 }
 
@@ -405,8 +423,20 @@ static void iterate_task(orc_state* st, int t, int k, int it, uint64_t* evals)
         L.pF = st->Fsnap[tk->partner];
     }
     int K = rs_count(cfg, L.h, L.w);
-    for (int field = -1; field < 4 + K; ++field) {
-        level_field(&L, cfg, field, k, it, tk->src_id, tk->tgt_id, tk->tag, st->F[t], st->E[t], st->Fn[t], st->En[t]);
+    /* E <- L(F); propagation at every scale (descending steps, D41; one unit-step scale = P:72); then
+     * the K random-search fields */
+    const int J = prop_scales(cfg);
+    level_field(&L, cfg, -1, 1, k, it, tk->src_id, tk->tgt_id, tk->tag, st->F[t], st->E[t], st->Fn[t], st->En[t]);
+    *evals += (uint64_t)L.h * L.w;
+    for (int j = J - 1; j >= 0; --j)
+        for (int d = 0; d < 4; ++d) {
+            level_field(&L, cfg, d, 1 << j, k, it, tk->src_id, tk->tgt_id, tk->tag, st->F[t], st->E[t], st->Fn[t],
+                        st->En[t]);
+            *evals += (uint64_t)L.h * L.w;
+        }
+    for (int field = 4; field < 4 + K; ++field) {
+        level_field(&L, cfg, field, 1, k, it, tk->src_id, tk->tgt_id, tk->tag, st->F[t], st->E[t], st->Fn[t],
+                    st->En[t]);
         *evals += (uint64_t)L.h * L.w;
     }
 }

@@ -32,7 +32,8 @@ def build(force: bool = False) -> str:
 class _Cfg(C.Structure):
     _fields_ = [("patch_radius", C.c_int32), ("levels", C.c_int32), ("iters_per_level", C.c_int32),
                 ("rs_radius0", C.c_int32), ("rs_steps", C.c_int32), ("alpha", C.c_float),
-                ("loss", C.c_int32), ("init", C.c_int32), ("seed", C.c_uint64)]
+                ("loss", C.c_int32), ("init", C.c_int32), ("seed", C.c_uint64), ("prop_scales", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class _Task(C.Structure):
@@ -53,10 +54,11 @@ class Cfg:
     loss: int = GUIDE_STYLE
     init: int = INIT_RANDOM
     seed: int = 1
+    prop_scales: int = 1
 
     def c(self) -> _Cfg:
         return _Cfg(self.patch_radius, self.levels, self.iters_per_level, self.rs_radius0, self.rs_steps,
-                    self.alpha, self.loss, self.init, self.seed)
+                    self.alpha, self.loss, self.init, self.seed, self.prop_scales, 0)
 
 
 _lib = None
@@ -88,6 +90,7 @@ def load():
         _lib.orc_tree_build_tasks.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.orc_field.argtypes = [P(_Cfg), C.c_int, C.c_int] + [C.c_void_p] * 4 + [C.c_int] * 6 + [C.c_void_p] * 2
         _lib.orc_set_threads.argtypes = [C.c_int]
+        _lib.orc_field_step.argtypes = [P(_Cfg), C.c_int, C.c_int] + [C.c_void_p] * 4 + [C.c_int] * 7 + [C.c_void_p] * 2
     return _lib
 
 
@@ -244,7 +247,7 @@ def tree_build_tasks(N: int, lcap: int):
 
 
 def field(cfg: Cfg, sg, tg, F, E, field_id: int, ss=None, aux=None, k: int = 0, it: int = 0,
-          src_id: int = 0, tgt_id: int = 0, tag: int = TAG_API):
+          src_id: int = 0, tgt_id: int = 0, tag: int = TAG_API, step: int = 1):
     """One element of Alg. 1's updating sequence at a single level (field -1 = E init, 0..3 =
     propagation directions, 4+s = random-search step s).  Returns the updated (F, E)."""
     sg = np.ascontiguousarray(sg, np.float32)
@@ -255,6 +258,6 @@ def field(cfg: Cfg, sg, tg, F, E, field_id: int, ss=None, aux=None, k: int = 0, 
     ss_ = None if ss is None else np.ascontiguousarray(ss, np.float32)
     aux_ = None if aux is None else np.ascontiguousarray(aux, np.float32)
     cc = cfg.c()
-    load().orc_field(C.byref(cc), h, w, _p(sg), _p(tg), None if ss_ is None else _p(ss_),
-                     None if aux_ is None else _p(aux_), field_id, k, it, src_id, tgt_id, tag, _p(F), _p(E))
+    load().orc_field_step(C.byref(cc), h, w, _p(sg), _p(tg), None if ss_ is None else _p(ss_),
+                          None if aux_ is None else _p(aux_), field_id, step, k, it, src_id, tgt_id, tag, _p(F), _p(E))
     return F, E

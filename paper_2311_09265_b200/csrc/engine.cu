@@ -208,7 +208,8 @@ uint64_t evals_per_pair(const fb_match_cfg& c, const Geo& g)
 {
     uint64_t n = 0;
     for (int k = 0; k < g.Lv; ++k)
-        n += (uint64_t)g.L[k].h * g.L[k].w * (uint64_t)c.iters_per_level * (uint64_t)(5 + rs_count(c, g.L[k]));
+        n += (uint64_t)g.L[k].h * g.L[k].w * (uint64_t)c.iters_per_level *
+             (uint64_t)(1 + 4 * std::max(1, c.prop_scales) + rs_count(c, g.L[k]));
     return n;
 }
 
@@ -222,6 +223,7 @@ void validate_cfg(const fb_match_cfg* cfg)
     if (!(cfg->alpha >= 0.0f)) throw Fail{FB_ERR_INVALID_ARG, "alpha < 0"};
     if (cfg->loss < 0 || cfg->loss > 3) throw Fail{FB_ERR_INVALID_ARG, "unknown loss"};
     if (cfg->init < 0 || cfg->init > 1) throw Fail{FB_ERR_INVALID_ARG, "unknown init"};
+    if (cfg->prop_scales < 0 || cfg->prop_scales > 12) throw Fail{FB_ERR_INVALID_ARG, "prop_scales not in [0, 12]"};
 }
 
 // ------------------------------------------------------------------------------------ pyramids
@@ -420,34 +422,45 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
             a.src_fmt = src_fmt(slots.fmt0, k);
             char names[4][32];
             for (int ph = 0; ph < 4; ++ph) snprintf(names[ph], sizeof names[ph], "field%d.L%d", ph, k);
-            if (fast && ex.ctx->fused) {  // one fused launch per iteration
+            const int J = std::max(1, cfg.prop_scales);  // jump-flood scales (D41)
+            a.einit = 1;
+            a.do_rs = 0;
+            if (fast && ex.ctx->fused && J == 1) {  // one fused launch per iteration (FB_FUSED=1)
                 char nm[32];
                 snprintf(nm, sizeof nm, "iter.L%d", k);
+                a.step = 1;
                 a.Fin = F[cur]; a.Fout = F[cur ^ 1];
                 ex.launch(nm, [&] { return fbk::launch_iter_fast(a, T, g.p, cfg.loss, s); },
                           (uint64_t)(5 + rk) * T * L.h * L.w);
                 cur ^= 1;
                 continue;
             }
-            if (fast && ex.ctx->fuse13) {  // field 0, then fields 1-3 + random search in one launch
-                a.Fin = F[cur]; a.Fout = F[cur ^ 1];
-                ex.launch(names[0], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, 0, fast, s); },
-                          2ull * T * L.h * L.w);
-                cur ^= 1;
-                char nm[32];
-                snprintf(nm, sizeof nm, "field123.L%d", k);
-                a.Fin = F[cur]; a.Fout = F[cur ^ 1];
-                ex.launch(nm, [&] { return fbk::launch_iter13_fast(a, T, g.p, cfg.loss, s); },
-                          (uint64_t)(3 + rk) * T * L.h * L.w);
-                cur ^= 1;
-                continue;
-            }
-            for (int ph = 0; ph < 4; ++ph) {
-                a.Fin = F[cur]; a.Fout = F[cur ^ 1];
-                const uint64_t per_px = ph == 0 ? 2 : ph == 3 ? 1 + (uint64_t)rk : 1;
-                ex.launch(names[ph], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, ph, fast, s); },
-                          per_px * (uint64_t)T * L.h * L.w);
-                cur ^= 1;
+            for (int j = J - 1; j >= 0; --j) {
+                a.step = 1 << j;
+                const bool last = j == 0;
+                if (last && fast && ex.ctx->fuse13) {  // field 0, then fields 1-3 + random search in one launch
+                    a.Fin = F[cur]; a.Fout = F[cur ^ 1];
+                    ex.launch(names[0], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, 0, fast, s); },
+                              (1ull + (uint64_t)a.einit) * T * L.h * L.w);
+                    cur ^= 1;
+                    char nm[32];
+                    snprintf(nm, sizeof nm, "field123.L%d", k);
+                    a.Fin = F[cur]; a.Fout = F[cur ^ 1];
+                    ex.launch(nm, [&] { return fbk::launch_iter13_fast(a, T, g.p, cfg.loss, s); },
+                              (uint64_t)(3 + rk) * T * L.h * L.w);
+                    cur ^= 1;
+                    continue;
+                }
+                for (int ph = 0; ph < 4; ++ph) {
+                    a.Fin = F[cur]; a.Fout = F[cur ^ 1];
+                    a.do_rs = last && ph == 3;
+                    const uint64_t per_px = 1 + (ph == 0 ? (uint64_t)a.einit : 0) + (a.do_rs ? (uint64_t)rk : 0);
+                    ex.launch(names[ph], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, ph, fast, s); },
+                              per_px * (uint64_t)T * L.h * L.w);
+                    cur ^= 1;
+                    a.einit = 0;
+                }
+                a.einit = 0;
             }
         }
     }

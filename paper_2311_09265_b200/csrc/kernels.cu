@@ -494,10 +494,10 @@ __global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
     const int2* Fi = a.Fin + t * a.fstride;
     const int i = r * w + c;
     int2 f = Fi[i];
-    float e = PHASE == 0 ? loss(f.x, f.y, __int_as_float(0x7f800000)) : a.E[t * a.fstride + i];
+    float e = PHASE == 0 && a.einit ? loss(f.x, f.y, __int_as_float(0x7f800000)) : a.E[t * a.fstride + i];
     {
-        constexpr int dx = PHASE == 0 ? -1 : (PHASE == 1 ? 1 : 0);
-        constexpr int dy = PHASE == 2 ? -1 : (PHASE == 3 ? 1 : 0);
+        const int dx = (PHASE == 0 ? -1 : (PHASE == 1 ? 1 : 0)) * a.step;  // jump-flood step (D41)
+        const int dy = (PHASE == 2 ? -1 : (PHASE == 3 ? 1 : 0)) * a.step;
         const int nr = clampi(r + dx, 0, h - 1), nc = clampi(c + dy, 0, w - 1);  // D11
         const int2 fn = Fi[nr * w + nc];
         const int sr = clampi(fn.x - dx, 0, h - 1), sc = clampi(fn.y - dy, 0, w - 1);  // D10
@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
             if (e2 < e) { f = make_int2(sr, sc); e = e2; }
         }
     }
-    if (PHASE == 3) {
+    if (PHASE == 3 && a.do_rs) {
         for (int s = 0; s < a.rs_k; ++s) {
             const int R = max(a.rs_r0 >> s, 1);
             const uint4 u = philox4x32_10(
@@ -922,10 +922,10 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
     const int2* Fi = a.Fin + t * a.fstride;
     const int i = r * w + c;
     int2 f = Fi[i];
-    float e = PHASE == 0 ? loss(f.x, f.y, __int_as_float(0x7f800000)) : a.E[t * a.fstride + i];
+    float e = PHASE == 0 && a.einit ? loss(f.x, f.y, __int_as_float(0x7f800000)) : a.E[t * a.fstride + i];
     {
-        constexpr int dx = PHASE == 0 ? -1 : (PHASE == 1 ? 1 : 0);
-        constexpr int dy = PHASE == 2 ? -1 : (PHASE == 3 ? 1 : 0);
+        const int dx = (PHASE == 0 ? -1 : (PHASE == 1 ? 1 : 0)) * a.step;  // jump-flood step (D41)
+        const int dy = (PHASE == 2 ? -1 : (PHASE == 3 ? 1 : 0)) * a.step;
         const int nr = clampi(r + dx, 0, h - 1), nc = clampi(c + dy, 0, w - 1);  // D11
         const int2 fn = Fi[nr * w + nc];
         const int sr = clampi(fn.x - dx, 0, h - 1), sc = clampi(fn.y - dy, 0, w - 1);  // D10
@@ -934,7 +934,7 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
             if (e2 < e) { f = make_int2(sr, sc); e = e2; }
         }
     }
-    if (PHASE == 3) {
+    if (PHASE == 3 && a.do_rs) {
         for (int s = 0; s < a.rs_k; ++s) {
             const int R = max(a.rs_r0 >> s, 1);
             const uint4 u = philox4x32_10(

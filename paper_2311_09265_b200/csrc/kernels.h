@@ -84,6 +84,9 @@ struct FieldArgs {
     uint32_t level, iter;  // for the Philox counter (D21)
     int rs_r0, rs_k;       // random-search radius r0 and step count at this level (D13, D33)
     int src_fmt;           // SF16 or SF32 for the general kernel
+    int step;              // propagation step (jump flood scale, D41; 1 = P:72)
+    int einit;             // phase 0 recomputes E <- L(F) (first field of the iteration)
+    int do_rs;             // phase 3 runs the random search (last field of the iteration)
 };
 
 // Packing jobs: one per (slot, level) for sources, one per task/group for BASE targets.

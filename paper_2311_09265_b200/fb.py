@@ -39,7 +39,8 @@ class FBError(RuntimeError):
 class _Cfg(C.Structure):
     _fields_ = [("patch_radius", C.c_int32), ("levels", C.c_int32), ("iters_per_level", C.c_int32),
                 ("rs_radius0", C.c_int32), ("rs_steps", C.c_int32), ("alpha", C.c_float),
-                ("loss", C.c_int32), ("init", C.c_int32), ("seed", C.c_uint64)]
+                ("loss", C.c_int32), ("init", C.c_int32), ("seed", C.c_uint64), ("prop_scales", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class _Stats(C.Structure):
@@ -61,7 +62,7 @@ class _Key(C.Structure):
 @dataclass
 class MatchCfg:
     """fb_match_cfg.  Defaults: "patch 5" (p=2), auto pyramid, n=5, full-image random search,
-    alpha=10, Philox seed 1 (D1, D6, D13-D15)."""
+    alpha=10, Philox seed 1, unit-step propagation (D1, D6, D13-D15, D41)."""
     patch_radius: int = 2
     levels: int = 0
     iters_per_level: int = 5
@@ -71,10 +72,11 @@ class MatchCfg:
     loss: int = GUIDE_STYLE
     init: int = INIT_RANDOM
     seed: int = 1
+    prop_scales: int = 1
 
     def c(self) -> _Cfg:
         return _Cfg(self.patch_radius, self.levels, self.iters_per_level, self.rs_radius0, self.rs_steps,
-                    self.alpha, self.loss, self.init, self.seed)
+                    self.alpha, self.loss, self.init, self.seed, self.prop_scales, 0)
 
 
 _lib = None

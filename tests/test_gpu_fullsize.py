@@ -24,7 +24,8 @@ def ctx(P):
 
 
 def ocfg(c):
-    return O.Cfg(c.patch_radius, c.levels, c.iters_per_level, c.rs_radius0, c.rs_steps, c.alpha, c.loss, c.init, c.seed)
+    return O.Cfg(c.patch_radius, c.levels, c.iters_per_level, c.rs_radius0, c.rs_steps, c.alpha, c.loss, c.init, c.seed,
+                 c.prop_scales)
 
 
 def check(got, ref):

@@ -29,7 +29,8 @@ def ctx(fb):
 
 
 def ocfg(c):
-    return O.Cfg(c.patch_radius, c.levels, c.iters_per_level, c.rs_radius0, c.rs_steps, c.alpha, c.loss, c.init, c.seed)
+    return O.Cfg(c.patch_radius, c.levels, c.iters_per_level, c.rs_radius0, c.rs_steps, c.alpha, c.loss, c.init, c.seed,
+                 c.prop_scales)
 
 
 def dev(a):
@@ -120,7 +121,8 @@ def test_nnf_estimate_matches_oracle(fb, ctx, loss, H, W):
 
 
 @pytest.mark.parametrize("kw", [dict(p=1), dict(p=3), dict(p=4, n=1), dict(init=1), dict(rs_radius0=4, rs_steps=3),
-                                dict(levels=1, n=3), dict(alpha=0.0), dict(seed=123456789012345)])
+                                dict(levels=1, n=3), dict(alpha=0.0), dict(seed=123456789012345),
+                                dict(prop_scales=3), dict(p=3, prop_scales=4), dict(p=1, prop_scales=2)])
 def test_nnf_estimate_config_variants(fb, ctx, kw):
     cfg, (sg, tg, ss, ts, keys), frames, tasks = _nnf_case(fb, 1, 40, 52, B=2, **kw)
     F, E, X, _ = ctx.fb_nnf_estimate(cfg, dev(sg), dev(tg), dev(ss), pair_keys=keys)
@@ -297,3 +299,17 @@ def test_pairwise_rejects_bad_counterparts(fb, ctx):
     with pytest.raises(fb.FBError) as e:
         ctx.fb_blend_window(cfg, fb.DIRECT, dev(g), dev(s), 1)
     assert e.value.status == 1
+
+
+@pytest.mark.parametrize("mode", ["balanced", "accurate", "fast"])
+def test_jump_flood_blend_parity(fb, ctx, mode):
+    """f3 / D41: jump-flood propagation (J = 3 scales) through every schedule."""
+    g, s = moving_texture(7, 48, 40, seed=25)
+    loss = fb.MEAN_ALIGN if mode == "accurate" else fb.GUIDE_STYLE
+    sched = fb.TREE if mode == "fast" else fb.DIRECT
+    cfg = fb.MatchCfg(iters_per_level=2, loss=loss, prop_scales=3)
+    out, st = ctx.fb_blend_window(cfg, sched, dev(g), dev(s), 2)
+    fn = O.blend_tree if mode == "fast" else O.blend_direct
+    ref, pairs, evals = fn(ocfg(cfg), g, s, 2)
+    assert st["candidate_evals"] == evals
+    assert_frames(out, ref)

@@ -216,9 +216,10 @@ def _shifted_pair(h, w, a, b, seed=6):
     return S, T, Ftrue
 
 
-@pytest.mark.parametrize("field", [0, 1, 2, 3])
-def test_propagation_field(field):
-    """F'(x,y) = F(x+dx, y+dy) - (dx,dy), Jacobi, strict-min select."""
+@pytest.mark.parametrize("field,step", [(0, 1), (1, 1), (2, 1), (3, 1), (0, 3), (3, 2), (1, 4)])
+def test_propagation_field(field, step):
+    """F'(x,y) = F(x+dx, y+dy) - (dx,dy), Jacobi, strict-min select; with a
+    jump-flood step s (D41) the neighbour is x + s d and the candidate F(x + s d) - s d."""
     h, w, p = 20, 22, 2
     a, b = 1, -2
     S, T, Ftrue = _shifted_pair(h, w, a, b)
@@ -229,8 +230,9 @@ def test_propagation_field(field):
     Fin[bad] = np.stack([rng.integers(0, h, bad.sum()), rng.integers(0, w, bad.sum())], -1)
     _, Ein = O.field(cfg, S, T, Fin, np.zeros((h, w), np.float32), -1)
     np.testing.assert_array_equal(Ein, np_patch_dist_field(S, T, Fin, p).astype(np.float32))
-    Fout, Eout = O.field(cfg, S, T, Fin, Ein, field)
+    Fout, Eout = O.field(cfg, S, T, Fin, Ein, field, step=step)
     dx, dy = [(-1, 0), (1, 0), (0, -1), (0, 1)][field]
+    dx, dy = dx * step, dy * step
     assert np.all(Eout <= Ein)
     changed = np.any(Fout != Fin, -1)
     assert np.all(Eout[changed] < Ein[changed])
@@ -242,7 +244,8 @@ def test_propagation_field(field):
             # Jacobi: the only admissible outcomes are the incumbent or the neighbour-derived candidate
             assert tuple(Fout[r, c]) in (tuple(Fin[r, c]), cand)
             interior = p <= r + a < h - p and p <= c + b < w - p and p <= r < h - p and p <= c < w - p
-            if bad[r, c] and not bad[nr, nc] and (nr, nc) != (r, c) and interior and Ein[r, c] > 0:
+            unclamped = (nr, nc) == (r + dx, c + dy) and 0 <= nr + a < h and 0 <= nc + b < w
+            if bad[r, c] and not bad[nr, nc] and unclamped and interior and Ein[r, c] > 0:
                 assert tuple(Fout[r, c]) == tuple(Ftrue[r, c]) and Eout[r, c] == 0
                 fixed_expected += 1
     assert fixed_expected > 10
@@ -636,3 +639,36 @@ def test_aligned_interpolation_equal_keys_static_video():
     assert pairs == 2 * 5
     for m in range(7):
         np.testing.assert_allclose(out[m], s[0].astype(np.float32), atol=1e-4)
+
+
+def test_jump_flood_counts_and_single_scale_identity():
+    """D41: J scales add 4 evaluations per scale per pixel per iteration; J = 1 is the paper's
+    propagation bit for bit."""
+    g, s = moving_texture(2, 40, 48, seed=19)
+    frames = np.concatenate([g, s]).astype(np.float32)
+    task = [dict(src_guide=0, tgt_guide=1, src_style=2, src_id=0, tgt_id=1, tag=6)]
+    c1 = O.Cfg(iters_per_level=2, prop_scales=1)
+    c0 = O.Cfg(iters_per_level=2, prop_scales=0)
+    F1, E1, _, ev1 = O.nnf(c1, frames, task, want_x=False)
+    F0, E0, _, ev0 = O.nnf(c0, frames, task, want_x=False)
+    np.testing.assert_array_equal(F1, F0)
+    c4 = O.Cfg(iters_per_level=2, prop_scales=4)
+    _, _, _, ev4 = O.nnf(c4, frames, task, want_x=False)
+    npx = sum((40 >> k) * (48 >> k) for k in range(O.level_count(40, 48, 2)))
+    assert ev4 - ev1 == 2 * 4 * 3 * npx
+
+
+def test_jump_flood_converges_at_least_as_fast_on_a_shift():
+    """A pure shift is recovered faster with long propagation steps: after one iteration at one level
+    with identity init, J = 5 reaches the exact shift on more pixels than J = 1 (D41 motivation)."""
+    S = textured_frame(64, 64, seed=23).astype(np.float32)
+    T = np.roll(S, (5, -7), axis=(0, 1))
+    frames = np.stack([S, T])
+    task = [dict(src_guide=0, tgt_guide=1, src_id=0, tgt_id=1)]
+    rr, cc = np.mgrid[0:64, 0:64]
+    good = {}
+    for J in (1, 5):
+        cfg = O.Cfg(levels=1, iters_per_level=1, loss=O.BASE, prop_scales=J, rs_radius0=1, rs_steps=1)
+        F, E, _, _ = O.nnf(cfg, frames, task, want_x=False)
+        good[J] = np.mean(E[0] == 0)
+    assert good[5] >= good[1]
