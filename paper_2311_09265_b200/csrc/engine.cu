@@ -277,7 +277,8 @@ Slots pack_sources(Exec& ex, const Geo& g, int fmt0, const std::vector<SlotSpec>
     for (int k = 0; k < g.Lv; ++k) {
         S.off[k] = off;
         const int f = src_fmt(fmt0, k);
-        off = (off + (size_t)g.PL[k].rows * g.PL[k].pitch * src_bytes(f) + 255) & ~size_t(255);
+        const size_t copies = f == fbk::SF8 ? fbk::kSF8Copies : 1;
+        off = (off + copies * g.PL[k].rows * g.PL[k].pitch * src_bytes(f) + 255) & ~size_t(255);
     }
     S.stride = off;
     const int n = (int)specs.size();

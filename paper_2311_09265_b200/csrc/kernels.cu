@@ -86,10 +86,12 @@ __global__ void k_pack_src(const PackSrc* __restrict__ jobs, int fmt, PLvl L)
 {
     const PackSrc J = jobs[blockIdx.y];
     const int n = L.rows * L.pitch;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int copies = fmt == SF8 ? kSF8Copies : 1;
+    for (int ii = blockIdx.x * blockDim.x + threadIdx.x; ii < n * copies; ii += gridDim.x * blockDim.x) {
+        const int cpy = ii / n, i = ii - cpy * n;  // copy cpy holds texel (pr, pc + cpy) at (pr, pc)
         const int pr = i / L.pitch, pc = i - pr * L.pitch;
-        const int r = pr - B, c = pc - B;
-        const bool in = (unsigned)r < (unsigned)L.h && (unsigned)c < (unsigned)L.w;
+        const int r = pr - B, c = pc + cpy - B;
+        const bool in = (unsigned)r < (unsigned)L.h && (unsigned)c < (unsigned)L.w && pc + cpy < L.pitch;
         if (fmt == SF8) {
             uint2 v = make_uint2(0u, 0u);
             if (in) {
@@ -100,7 +102,7 @@ __global__ void k_pack_src(const PackSrc* __restrict__ jobs, int fmt, PLvl L)
                     v.y = s[0] | (s[1] << 8) | (s[2] << 16);
                 }
             }
-            reinterpret_cast<uint2*>(J.out)[i] = v;
+            reinterpret_cast<uint2*>(J.out)[(size_t)cpy * n + i] = v;
         } else if (fmt == SF16) {
             // level k of a u8 pyramid: v = n / 4^k with n < 2^16 (k <= 4); store n
             const float sc = (float)(1 << (2 * L.k));
@@ -445,8 +447,9 @@ __global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
     // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
     auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
         const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
-        const int o = idx & 1;
-        const uint4* cp = reinterpret_cast<const uint4*>(S + (idx - o));
+        const int o = kSF8Copies == 2 ? 0 : (idx & 1);  // with two copies the row start is always even
+        const uint4* cp = reinterpret_cast<const uint4*>(
+            S + (kSF8Copies == 2 ? (size_t)(idx & 1) * (a.L.rows * pitch) + (idx & ~1) : (size_t)(idx - o)));
         uint32_t wd[4 * NCH];
 #pragma unroll
         for (int k = 0; k < NCH; ++k) {
@@ -573,8 +576,9 @@ __global__ void __launch_bounds__(32 * (IT_TY + 1), IT_MINB) k_iter_fast(FieldAr
     // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
     auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
         const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
-        const int o = idx & 1;
-        const uint4* cp = reinterpret_cast<const uint4*>(S + (idx - o));
+        const int o = kSF8Copies == 2 ? 0 : (idx & 1);  // with two copies the row start is always even
+        const uint4* cp = reinterpret_cast<const uint4*>(
+            S + (kSF8Copies == 2 ? (size_t)(idx & 1) * (a.L.rows * pitch) + (idx & ~1) : (size_t)(idx - o)));
         uint32_t wd[4 * NCH];
 #pragma unroll
         for (int k = 0; k < NCH; ++k) {
@@ -716,8 +720,9 @@ __global__ void __launch_bounds__(32 * I13_TY, 3) k_iter13_fast(FieldArgs a)
     // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
     auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
         const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
-        const int o = idx & 1;
-        const uint4* cp = reinterpret_cast<const uint4*>(S + (idx - o));
+        const int o = kSF8Copies == 2 ? 0 : (idx & 1);  // with two copies the row start is always even
+        const uint4* cp = reinterpret_cast<const uint4*>(
+            S + (kSF8Copies == 2 ? (size_t)(idx & 1) * (a.L.rows * pitch) + (idx & ~1) : (size_t)(idx - o)));
         uint32_t wd[4 * NCH];
 #pragma unroll
         for (int k = 0; k < NCH; ++k) {
@@ -978,7 +983,7 @@ cudaError_t launch_box(float4* pyr, int Bn, long long pyr_stride, Lvl prev, Lvl 
 cudaError_t launch_pack_src(const PackSrc* jobs, int n, int fmt, PLvl L, cudaStream_t s)
 {
     if (n <= 0) return cudaSuccess;
-    k_pack_src<<<grid1d((long long)L.rows * L.pitch, n), 256, 0, s>>>(jobs, fmt, L);
+    k_pack_src<<<grid1d((long long)L.rows * L.pitch * (fmt == SF8 ? kSF8Copies : 1), n), 256, 0, s>>>(jobs, fmt, L);
     return cudaGetLastError();
 }
 

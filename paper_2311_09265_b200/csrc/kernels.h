@@ -21,6 +21,10 @@
 namespace fbk {
 
 constexpr int kBorder = 4;  // >= the largest compiled patch radius
+#ifndef FB_SF8_COPIES
+#define FB_SF8_COPIES 2      // SF8 planes stored twice, copy 1 shifted left by one texel: every patch row
+#endif                       // starts 16-byte aligned in copy (col & 1), so no parity selects are needed
+constexpr int kSF8Copies = FB_SF8_COPIES;
 
 enum SrcFmt { SF8 = 0, SF32 = 1, SF16 = 2 };
 enum TgtFmt { TF16 = 0, TF32 = 1 };
