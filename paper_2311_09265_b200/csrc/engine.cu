@@ -159,10 +159,11 @@ fbk::PLvl padded(int h, int w, int k)
 // SF8 at level 0 and the exact 16-bit integer form SF16 at levels 1..4 (values n / 4^k, n < 2^16).
 int src_fmt(int fmt0, int k)
 {
+    if (fmt0 == fbk::SF8F) return k == 0 ? fbk::SF8F : fbk::SF32;  // float styles: u8 guide + f32 style
     if (fmt0 != fbk::SF8) return fbk::SF32;
     return k == 0 ? fbk::SF8 : (k <= 4 ? fbk::SF16 : fbk::SF32);
 }
-size_t src_bytes(int fmt) { return fmt == fbk::SF8 ? 8 : fmt == fbk::SF16 ? 16 : 32; }
+size_t src_bytes(int fmt) { return fmt == fbk::SF8 ? 8 : (fmt == fbk::SF16 || fmt == fbk::SF8F) ? 16 : 32; }
 
 int level_count(int H, int W, int p, int requested)  // D6, D32
 {
@@ -271,7 +272,7 @@ struct Slots {
 Slots pack_sources(Exec& ex, const Geo& g, int fmt0, const std::vector<SlotSpec>& specs)
 {
     Slots S;
-    if (g.p > 2) fmt0 = fbk::SF32;  // the register-resident fast kernel is compiled for p <= 2 only
+    if (g.p > 2) fmt0 = fbk::SF32;  // the register-resident fast kernels are compiled for p <= 2 only
     S.fmt0 = fmt0;
     size_t off = 0;
     for (int k = 0; k < g.Lv; ++k) {
@@ -325,7 +326,7 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
     const int T = (int)tasks.size();
     const long long n0 = g.npx0();
     const cudaStream_t s = ex.ctx->stream;
-    const bool fast0 = slots.fmt0 == fbk::SF8 && g.p <= 2;  // level-0 fast operands (SF8 / TF16)
+    const bool fast0 = (slots.fmt0 == fbk::SF8 || slots.fmt0 == fbk::SF8F) && g.p <= 2;  // level-0 fast operands
     BatchOut out;
     out.fstride = n0;
     int2* F[2] = {ex.ar.take<int2>((size_t)T * n0), ex.ar.take<int2>((size_t)T * n0)};
@@ -698,7 +699,7 @@ void blend_tree(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N_total, i
                                              (uint32_t)i, tag_query});
                 }
             }
-            const Slots QS = pack_sources(ex, g, fbk::SF32, qspecs);
+            const Slots QS = pack_sources(ex, g, fbk::SF8F, qspecs);
             for (size_t t = 0; t < tasks.size(); ++t) tasks[t].src = QS.slot((long long)t);
             BatchOut bo;
             if (!tasks.empty()) bo = run_nnf(ex, cfg, g, QS, tasks, {}, st);

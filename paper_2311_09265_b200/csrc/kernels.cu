@@ -103,6 +103,15 @@ __global__ void k_pack_src(const PackSrc* __restrict__ jobs, int fmt, PLvl L)
                 }
             }
             reinterpret_cast<uint2*>(J.out)[(size_t)cpy * n + i] = v;
+        } else if (fmt == SF8F) {
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (in) {
+                const float4 g = J.gp[r * L.w + c];
+                const float4 sv = J.sp ? J.sp[r * L.w + c] : make_float4(0.f, 0.f, 0.f, 0.f);
+                v = make_uint4(pack_rgb(g.x, g.y, g.z), __float_as_uint(sv.x), __float_as_uint(sv.y),
+                               __float_as_uint(sv.z));
+            }
+            reinterpret_cast<uint4*>(J.out)[i] = v;
         } else if (fmt == SF16) {
             // level k of a u8 pyramid: v = n / 4^k with n < 2^16 (k <= 4); store n
             const float sc = (float)(1 << (2 * L.k));
@@ -416,7 +425,7 @@ __device__ __forceinline__ void load_pairwise_patch(const DTask& T, const FieldA
 // is an integer below 2^24 (p <= 4), so the chain is exact and equals the integer SSD computed with
 // byte-wise |a-b| and dp4a; it is converted once, exactly.  Style term: the FP32 chain of D20 with the
 // u8 source channel converted exactly (u8f).
-template <int P, bool TWO, int PHASE, bool PW = false>
+template <int P, bool TWO, int PHASE, bool PW = false, int SFL = 0>
 __global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
 {
     constexpr int D = 2 * P + 1;
@@ -447,6 +456,23 @@ __global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
     // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
     auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
         const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
+        if (SFL == 1) {  // SF8F float style (blending-table cells): one 16-byte texel per tap
+            const uint4* tp = reinterpret_cast<const uint4*>(S) + idx;
+            float rs = 0.0f;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const uint4 v = __ldg(tp + j);
+                const uint32_t d = __vabsdiffu4(v.x, tgG[dr][j]);
+                dg = __dp4a(d, d, dg);
+                if (TWO) {
+                    float dl = __fsub_rn(tgA[dr][j][0], __uint_as_float(v.y)); rs = __fmaf_rn(dl, dl, rs);
+                    dl = __fsub_rn(tgA[dr][j][1], __uint_as_float(v.z)); rs = __fmaf_rn(dl, dl, rs);
+                    dl = __fsub_rn(tgA[dr][j][2], __uint_as_float(v.w)); rs = __fmaf_rn(dl, dl, rs);
+                }
+            }
+            if (TWO) ds = __fadd_rn(ds, rs);
+            return;
+        }
         const int o = kSF8Copies == 2 ? 0 : (idx & 1);  // with two copies the row start is always even
         const uint4* cp = reinterpret_cast<const uint4*>(
             S + (kSF8Copies == 2 ? (size_t)(idx & 1) * (a.L.rows * pitch) + (idx & ~1) : (size_t)(idx - o)));
@@ -545,6 +571,7 @@ template <int P, bool TWO>
 __global__ void __launch_bounds__(32 * (IT_TY + 1), IT_MINB) k_iter_fast(FieldArgs a)
 {
     constexpr bool PW = false;
+    constexpr int SFL = 0;
     constexpr int D = 2 * P + 1;
     constexpr int NCH = (D + 2) / 2;
     __shared__ int2 sF0[IT_TY + 1][32];
@@ -576,6 +603,23 @@ __global__ void __launch_bounds__(32 * (IT_TY + 1), IT_MINB) k_iter_fast(FieldAr
     // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
     auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
         const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
+        if (SFL == 1) {  // SF8F float style (blending-table cells): one 16-byte texel per tap
+            const uint4* tp = reinterpret_cast<const uint4*>(S) + idx;
+            float rs = 0.0f;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const uint4 v = __ldg(tp + j);
+                const uint32_t d = __vabsdiffu4(v.x, tgG[dr][j]);
+                dg = __dp4a(d, d, dg);
+                if (TWO) {
+                    float dl = __fsub_rn(tgA[dr][j][0], __uint_as_float(v.y)); rs = __fmaf_rn(dl, dl, rs);
+                    dl = __fsub_rn(tgA[dr][j][1], __uint_as_float(v.z)); rs = __fmaf_rn(dl, dl, rs);
+                    dl = __fsub_rn(tgA[dr][j][2], __uint_as_float(v.w)); rs = __fmaf_rn(dl, dl, rs);
+                }
+            }
+            if (TWO) ds = __fadd_rn(ds, rs);
+            return;
+        }
         const int o = kSF8Copies == 2 ? 0 : (idx & 1);  // with two copies the row start is always even
         const uint4* cp = reinterpret_cast<const uint4*>(
             S + (kSF8Copies == 2 ? (size_t)(idx & 1) * (a.L.rows * pitch) + (idx & ~1) : (size_t)(idx - o)));
@@ -687,7 +731,7 @@ __global__ void __launch_bounds__(32 * (IT_TY + 1), IT_MINB) k_iter_fast(FieldAr
 // pixels see exactly the Jacobi inputs of the per-field launches.  No shared memory, no barrier.
 static constexpr int I13_TY = 4;
 
-template <int P, bool TWO, bool PW = false>
+template <int P, bool TWO, bool PW = false, int SFL = 0>
 __global__ void __launch_bounds__(32 * I13_TY, 3) k_iter13_fast(FieldArgs a)
 {
     constexpr int D = 2 * P + 1;
@@ -720,6 +764,23 @@ __global__ void __launch_bounds__(32 * I13_TY, 3) k_iter13_fast(FieldArgs a)
     // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
     auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
         const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
+        if (SFL == 1) {  // SF8F float style (blending-table cells): one 16-byte texel per tap
+            const uint4* tp = reinterpret_cast<const uint4*>(S) + idx;
+            float rs = 0.0f;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const uint4 v = __ldg(tp + j);
+                const uint32_t d = __vabsdiffu4(v.x, tgG[dr][j]);
+                dg = __dp4a(d, d, dg);
+                if (TWO) {
+                    float dl = __fsub_rn(tgA[dr][j][0], __uint_as_float(v.y)); rs = __fmaf_rn(dl, dl, rs);
+                    dl = __fsub_rn(tgA[dr][j][1], __uint_as_float(v.z)); rs = __fmaf_rn(dl, dl, rs);
+                    dl = __fsub_rn(tgA[dr][j][2], __uint_as_float(v.w)); rs = __fmaf_rn(dl, dl, rs);
+                }
+            }
+            if (TWO) ds = __fadd_rn(ds, rs);
+            return;
+        }
         const int o = kSF8Copies == 2 ? 0 : (idx & 1);  // with two copies the row start is always even
         const uint4* cp = reinterpret_cast<const uint4*>(
             S + (kSF8Copies == 2 ? (size_t)(idx & 1) * (a.L.rows * pitch) + (idx & ~1) : (size_t)(idx - o)));
@@ -1063,15 +1124,15 @@ static void launch_field_gen(const FieldArgs& a, int T, int phase, cudaStream_t 
     }
 }
 
-template <int P, bool TWO, bool PW = false>
+template <int P, bool TWO, bool PW = false, int SFL = 0>
 static void launch_field_fast(const FieldArgs& a, int T, int phase, cudaStream_t s)
 {
     const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(TILE_X * FAST_TY);
     switch (phase) {
-    case 0: k_field_fast<P, TWO, 0, PW><<<grid, block, 0, s>>>(a); break;
-    case 1: k_field_fast<P, TWO, 1, PW><<<grid, block, 0, s>>>(a); break;
-    case 2: k_field_fast<P, TWO, 2, PW><<<grid, block, 0, s>>>(a); break;
-    default: k_field_fast<P, TWO, 3, PW><<<grid, block, 0, s>>>(a); break;
+    case 0: k_field_fast<P, TWO, 0, PW, SFL><<<grid, block, 0, s>>>(a); break;
+    case 1: k_field_fast<P, TWO, 1, PW, SFL><<<grid, block, 0, s>>>(a); break;
+    case 2: k_field_fast<P, TWO, 2, PW, SFL><<<grid, block, 0, s>>>(a); break;
+    default: k_field_fast<P, TWO, 3, PW, SFL><<<grid, block, 0, s>>>(a); break;
     }
 }
 
@@ -1093,6 +1154,13 @@ cudaError_t launch_iter13_fast(const FieldArgs& a0, int T, int p, int loss, cuda
     a.tiles_x = (a.L.w + IT_TX - 1) / IT_TX;
     a.tiles_per_task = a.tiles_x * ((a.L.h + I13_TY - 1) / I13_TY);
     const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(32 * I13_TY);
+    if (a.src_fmt == SF8F) {
+        if (loss != 1 && loss != 2) return cudaErrorInvalidValue;
+        if (p == 1) k_iter13_fast<1, true, false, 1><<<grid, block, 0, s>>>(a);
+        else if (p == 2) k_iter13_fast<2, true, false, 1><<<grid, block, 0, s>>>(a);
+        else return cudaErrorInvalidValue;
+        return cudaGetLastError();
+    }
     if (p == 1) {
         if (loss == 3) k_iter13_fast<1, true, true><<<grid, block, 0, s>>>(a);
         else if (loss) k_iter13_fast<1, true><<<grid, block, 0, s>>>(a);
@@ -1113,7 +1181,12 @@ cudaError_t launch_field(const FieldArgs& a0, int T, int p, int loss, int phase,
     a.tiles_x = (a.L.w + TILE_X - 1) / TILE_X;
     a.tiles_per_task = a.tiles_x * ((a.L.h + (fast ? FAST_TY : TILE_Y) - 1) / (fast ? FAST_TY : TILE_Y));
     const bool pw = loss == 3;
-    if (fast) {
+    if (fast && a.src_fmt == SF8F) {  // float-style level-0 sources (tree queries): GUIDE_STYLE only
+        if (pw || !loss) return cudaErrorInvalidValue;
+        if (p == 1) launch_field_fast<1, true, false, 1>(a, T, phase, s);
+        else if (p == 2) launch_field_fast<2, true, false, 1>(a, T, phase, s);
+        else return cudaErrorInvalidValue;
+    } else if (fast) {
         if (p == 1) {
             if (pw) launch_field_fast<1, true, true>(a, T, phase, s);
             else if (loss) launch_field_fast<1, true>(a, T, phase, s);

@@ -11,6 +11,8 @@
 //      source  SF8  (level 0, uint8 style): uint2 {G rgb u8, S rgb u8}                        8 B
 //              SF16 (levels 1..4, uint8 style): uint4 of u16 n = v * 4^k {G.r,G.g | G.b,0 |
 //                   S.r,S.g | S.b,0}; exact because level-k values are multiples of 4^-k (D6) 16 B
+//              SF8F (level 0, float style, e.g. blending-table cells): uint4 {G rgb u8, S.r, S.g, S.b
+//                   as f32}; the guide is still u8-exact at level 0                              16 B
 //              SF32 (otherwise):           float4 {G.r,G.g,G.b,S.r}, float4 {S.g,S.b,0,0}     32 B
 //      target  TF16 (with SF8):            uint4  {G rgb u8, aux.r, aux.g, aux.b (f32 bits)}  16 B
 //              TF32 (with SF32):           float4 {G.r,G.g,G.b,aux.r}, float4 {aux.g,aux.b,0,0} 32 B
@@ -26,7 +28,7 @@ constexpr int kBorder = 4;  // >= the largest compiled patch radius
 #endif                       // starts 16-byte aligned in copy (col & 1), so no parity selects are needed
 constexpr int kSF8Copies = FB_SF8_COPIES;
 
-enum SrcFmt { SF8 = 0, SF32 = 1, SF16 = 2 };
+enum SrcFmt { SF8 = 0, SF32 = 1, SF16 = 2, SF8F = 3 };
 enum TgtFmt { TF16 = 0, TF32 = 1 };
 
 // One NNF task (pair).
@@ -87,7 +89,7 @@ struct FieldArgs {
     Rng rng;
     uint32_t level, iter;  // for the Philox counter (D21)
     int rs_r0, rs_k;       // random-search radius r0 and step count at this level (D13, D33)
-    int src_fmt;           // SF16 or SF32 for the general kernel
+    int src_fmt;           // SF16 or SF32 for the general kernel; SF8 or SF8F for the fast kernels
     int step;              // propagation step (jump flood scale, D41; 1 = P:72)
     int einit;             // phase 0 recomputes E <- L(F) (first field of the iteration)
     int do_rs;             // phase 3 runs the random search (last field of the iteration)
