@@ -41,7 +41,7 @@ typedef struct {
     int32_t init;            /* 0 random, 1 identity (D8)                              */
     uint64_t seed;           /* Philox key (D21)                                              */
     int32_t prop_scales;     /* J propagation scales, steps 2^(J-1)..1 (jump flood, D41); 0/1 = P:72 */
-    int32_t reserved;
+    int32_t tracking;        /* interpolation: NNF(S,T_{i-1}), NNF(S,T_{i+1}) as candidates (D42) */
 } orc_cfg;
 
 enum { ORC_BASE = 0, ORC_GUIDE_STYLE = 1, ORC_MEAN_ALIGN = 2, ORC_PAIRWISE = 3 };
@@ -191,6 +191,7 @@ typedef struct {
     int group;                                       /* MEAN_ALIGN window id                     */
     int src_id, tgt_id, tag;                         /* RNG key (D21)                            */
     int partner;                                     /* PAIRWISE: the counterpart task (D38)     */
+    int track_prev, track_next;                      /* tracking neighbours (tasks for T_{i-1}, T_{i+1}), -1 */
 } orc_task;
 
 typedef struct {
@@ -319,6 +320,29 @@ static void level_field(const orc_level_ctx* L, const orc_cfg* cfg, int field, i
         }
 }
 
+/* Tracking field (D42): the whole field of a neighbouring frame's NNF (frozen at the start
+ * of the iteration) as the candidate, F'(x) = G(x), followed by the strict-min select. */
+static void level_track_field(const orc_level_ctx* L, const int32_t* G, int32_t* F, float* E)
+{
+    int h = L->h, w = L->w;
+#pragma omp parallel for schedule(static)
+    for (int r = 0; r < h; ++r)
+        for (int c = 0; c < w; ++c) {
+            size_t i = (size_t)r * w + c;
+            int sr = G[2 * i], sc = G[2 * i + 1];
+            float e = level_loss(L, r, c, sr, sc);
+            if (e < E[i]) { F[2 * i] = sr; F[2 * i + 1] = sc; E[i] = e; } /* pointwise: in place is Jacobi */
+        }
+}
+
+/* Tracking-field entry for the pins: one level, explicit candidate field G. */
+void orc_track_field(const orc_cfg* cfg, int h, int w, const float* sg, const float* tg, const float* ss,
+                     const float* aux, const int32_t* G, int32_t* F, float* E)
+{
+    orc_level_ctx L = { h, w, cfg->patch_radius, cfg->loss, cfg->alpha, sg, tg, ss, aux, NULL, NULL };
+    level_track_field(&L, G, F, E);
+}
+
 /* Single-field entry for the pins (tests/test_oracle_pins.py): one level, explicit F/E/aux. */
 void orc_field(const orc_cfg* cfg, int h, int w, const float* sg, const float* tg, const float* ss,
                const float* aux, int field, int k, int it, int src_id, int tgt_id, int tag, int32_t* F, float* E)
@@ -366,10 +390,11 @@ static void refresh_aux(orc_state* st, int k)
     const orc_cfg* cfg = st->cfg;
     int h = st->L[k].h, w = st->L[k].w, p = cfg->patch_radius;
     size_t npx = (size_t)h * w;
-    if (cfg->loss == ORC_PAIRWISE) {
-        /* the counterpart NNFs are frozen at the start of the iteration (D39) */
+    if (cfg->loss == ORC_PAIRWISE || cfg->tracking) {
+        /* counterpart (D39) and tracking (D42) NNFs are frozen at the start of the iteration */
         for (int t = 0; t < st->T; ++t) memcpy(st->Fsnap[t], st->F[t], sizeof(int32_t) * 2 * npx);
-    } else if (cfg->loss == ORC_GUIDE_STYLE) {
+    }
+    if (cfg->loss == ORC_GUIDE_STYLE) {
         /* S^_i = remap of the task's source style with the current F at this level (D18) */
         for (int t = 0; t < st->T; ++t)
             orc_remap(st->pyr_ss[t] + 3 * st->L[k].off, h, w, st->F[t], p, st->aux[t]);
@@ -432,6 +457,13 @@ static void iterate_task(orc_state* st, int t, int k, int it, uint64_t* evals)
         for (int d = 0; d < 4; ++d) {
             level_field(&L, cfg, d, 1 << j, k, it, tk->src_id, tk->tgt_id, tk->tag, st->F[t], st->E[t], st->Fn[t],
                         st->En[t]);
+            *evals += (uint64_t)L.h * L.w;
+        }
+    if (cfg->tracking) /* tracking candidates T_{i-1} then T_{i+1} (D42) */
+        for (int z = 0; z < 2; ++z) {
+            int nb = z == 0 ? tk->track_prev : tk->track_next;
+            if (nb < 0) continue;
+            level_track_field(&L, st->Fsnap[nb], st->F[t], st->E[t]);
             *evals += (uint64_t)L.h * L.w;
         }
     for (int field = 4; field < 4 + K; ++field) {
@@ -566,7 +598,7 @@ int orc_blend_direct(const orc_cfg* cfg, int N, int H, int W, int M, const uint8
         int i = targets[q], lo = i - M < 0 ? 0 : i - M, hi = i + M > N - 1 ? N - 1 : i + M;
         for (int j = lo; j <= hi; ++j) {
             if (j == i) continue;
-            orc_task tk = { j, i, N + j, cfg->loss == ORC_MEAN_ALIGN ? N + i : -1, q, j, i, ORC_TAG_DIRECT, -1 };
+            orc_task tk = { j, i, N + j, cfg->loss == ORC_MEAN_ALIGN ? N + i : -1, q, j, i, ORC_TAG_DIRECT, -1, -1, -1 };
             tasks[T++] = tk;
         }
     }
@@ -674,7 +706,7 @@ static int build_table_needed(const orc_cfg* cfg, int N, int H, int W, int M, in
     for (int a = 0; a < nb; ++a) {
         if (!need[(size_t)bd[a] * (lcap + 1) + bl[a]]) continue;
         int oi = orient == 0 ? bs[a] : N - 1 - bs[a], oj = orient == 0 ? bd[a] : N - 1 - bd[a];
-        orc_task tk = { oi, oj, N + oi, -1, 0, oi, oj, orient == 0 ? ORC_TAG_TREE_BUILD_F : ORC_TAG_TREE_BUILD_R, -1 };
+        orc_task tk = { oi, oj, N + oi, -1, 0, oi, oj, orient == 0 ? ORC_TAG_TREE_BUILD_F : ORC_TAG_TREE_BUILD_R, -1, -1, -1 };
         tasks[T] = tk; tcell[T] = a; ++T;
     }
     float* X = (float*)malloc(sizeof(float) * 3 * npx * (T > 0 ? T : 1));
@@ -735,7 +767,7 @@ static int query_unnormalised(const orc_cfg* cfg, int N, int H, int W, int M, in
         if (nodes[a] == v) continue; /* self node: identity, no NNF (D23) */
         int oi = orient == 0 ? nodes[a] : N - 1 - nodes[a];
         memcpy(fr + 3 * npx * (N + T), tab->bt[(size_t)nodes[a] * (tab->lcap + 1) + lvls[a]], sizeof(float) * 3 * npx);
-        orc_task tk = { oi, target, N + T, -1, 0, oi, target, orient == 0 ? ORC_TAG_TREE_QUERY_F : ORC_TAG_TREE_QUERY_R, -1 };
+        orc_task tk = { oi, target, N + T, -1, 0, oi, target, orient == 0 ? ORC_TAG_TREE_QUERY_F : ORC_TAG_TREE_QUERY_R, -1, -1, -1 };
         tasks[T] = tk; slot_of[a] = T; ++T;
     }
     float* X = (float*)malloc(sizeof(float) * 3 * npx * (T > 0 ? T : 1));
@@ -804,6 +836,17 @@ int orc_interpolate(const orc_cfg* cfg, int N, int H, int W, const uint8_t* guid
     float* frames = (float*)malloc(sizeof(float) * 3 * npx * ((size_t)N + K));
     u8_to_float(guide, 3 * npx * N, frames);
     u8_to_float(key_style, 3 * npx * K, frames + 3 * npx * N);
+    /* with tracking (D42) every frame's estimation depends on its neighbours', so the closure of any
+     * target is the whole video: estimate all frames and output the requested ones */
+    int* all = NULL;
+    const int n_req = n_targets;
+    const int32_t* req = targets;
+    if (cfg->tracking) {
+        all = (int*)malloc(sizeof(int) * (N > 0 ? N : 1));
+        for (int m = 0; m < N; ++m) all[m] = m;
+        targets = all;
+        n_targets = N;
+    }
     /* two task lists: [0] single-key / unaligned (GUIDE_STYLE), [1] aligned pairs (PAIRWISE) */
     orc_task* tl[2];
     int nt[2] = { 0, 0 };
@@ -822,11 +865,11 @@ int orc_interpolate(const orc_cfg* cfg, int N, int H, int W, const uint8_t* guid
         }
         const int li = (align && left >= 0 && right >= 0) ? 1 : 0;
         if (left >= 0) {
-            orc_task tk = { key_index[left], m, N + left, -1, 0, key_index[left], m, ORC_TAG_INTERP, -1 };
+            orc_task tk = { key_index[left], m, N + left, -1, 0, key_index[left], m, ORC_TAG_INTERP, -1, -1, -1 };
             ta[4 * q] = li; ta[4 * q + 1] = nt[li]; tl[li][nt[li]++] = tk;
         }
         if (right >= 0) {
-            orc_task tk = { key_index[right], m, N + right, -1, 0, key_index[right], m, ORC_TAG_INTERP, -1 };
+            orc_task tk = { key_index[right], m, N + right, -1, 0, key_index[right], m, ORC_TAG_INTERP, -1, -1, -1 };
             ta[4 * q + 2] = li; ta[4 * q + 3] = nt[li]; tl[li][nt[li]++] = tk;
         }
         if (li == 1) { /* counterparts */
@@ -834,6 +877,14 @@ int orc_interpolate(const orc_cfg* cfg, int N, int H, int W, const uint8_t* guid
             tl[1][ta[4 * q + 3]].partner = ta[4 * q + 1];
         }
     }
+    if (cfg->tracking) /* D42: neighbours = tasks of the same key for targets m-1 and m+1 in the same list */
+        for (int z = 0; z < 2; ++z)
+            for (int a2 = 0; a2 < nt[z]; ++a2)
+                for (int b2 = 0; b2 < nt[z]; ++b2) {
+                    if (tl[z][b2].src_id != tl[z][a2].src_id) continue;
+                    if (tl[z][b2].tgt_id == tl[z][a2].tgt_id - 1) tl[z][a2].track_prev = b2;
+                    if (tl[z][b2].tgt_id == tl[z][a2].tgt_id + 1) tl[z][a2].track_next = b2;
+                }
     float* X[2];
     uint64_t evals = 0;
     for (int z = 0; z < 2; ++z) {
@@ -846,9 +897,10 @@ int orc_interpolate(const orc_cfg* cfg, int N, int H, int W, const uint8_t* guid
             evals += ev;
         }
     }
-    for (int q = 0; q < n_targets; ++q) {
+    for (int qr = 0; qr < n_req; ++qr) {
+        int q = cfg->tracking ? req[qr] : qr;
         int m = targets[q];
-        float* o = out + 3 * npx * q;
+        float* o = out + 3 * npx * qr;
         const int hl = ta[4 * q] >= 0, hr = ta[4 * q + 2] >= 0;
         const float* xl = hl ? X[ta[4 * q]] + 3 * npx * ta[4 * q + 1] : NULL;
         const float* xr = hr ? X[ta[4 * q + 2]] + 3 * npx * ta[4 * q + 3] : NULL;
@@ -866,7 +918,7 @@ int orc_interpolate(const orc_cfg* cfg, int N, int H, int W, const uint8_t* guid
     }
     if (pairs_out) *pairs_out = (uint64_t)(nt[0] + nt[1]);
     if (evals_out) *evals_out = evals;
-    free(frames); free(tl[0]); free(tl[1]); free(ta); free(X[0]); free(X[1]);
+    free(frames); free(tl[0]); free(tl[1]); free(ta); free(X[0]); free(X[1]); free(all);
     return 0;
 }
 

@@ -33,13 +33,13 @@ class _Cfg(C.Structure):
     _fields_ = [("patch_radius", C.c_int32), ("levels", C.c_int32), ("iters_per_level", C.c_int32),
                 ("rs_radius0", C.c_int32), ("rs_steps", C.c_int32), ("alpha", C.c_float),
                 ("loss", C.c_int32), ("init", C.c_int32), ("seed", C.c_uint64), ("prop_scales", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("tracking", C.c_int32)]
 
 
 class _Task(C.Structure):
     _fields_ = [("src_guide", C.c_int), ("tgt_guide", C.c_int), ("src_style", C.c_int), ("tgt_style", C.c_int),
                 ("group", C.c_int), ("src_id", C.c_int), ("tgt_id", C.c_int), ("tag", C.c_int),
-                ("partner", C.c_int)]
+                ("partner", C.c_int), ("track_prev", C.c_int), ("track_next", C.c_int)]
 
 
 @dataclass
@@ -55,10 +55,11 @@ class Cfg:
     init: int = INIT_RANDOM
     seed: int = 1
     prop_scales: int = 1
+    tracking: int = 0
 
     def c(self) -> _Cfg:
         return _Cfg(self.patch_radius, self.levels, self.iters_per_level, self.rs_radius0, self.rs_steps,
-                    self.alpha, self.loss, self.init, self.seed, self.prop_scales, 0)
+                    self.alpha, self.loss, self.init, self.seed, self.prop_scales, self.tracking)
 
 
 _lib = None
@@ -90,6 +91,7 @@ def load():
         _lib.orc_tree_build_tasks.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.orc_field.argtypes = [P(_Cfg), C.c_int, C.c_int] + [C.c_void_p] * 4 + [C.c_int] * 6 + [C.c_void_p] * 2
         _lib.orc_set_threads.argtypes = [C.c_int]
+        _lib.orc_track_field.argtypes = [P(_Cfg), C.c_int, C.c_int] + [C.c_void_p] * 7
         _lib.orc_field_step.argtypes = [P(_Cfg), C.c_int, C.c_int] + [C.c_void_p] * 4 + [C.c_int] * 7 + [C.c_void_p] * 2
     return _lib
 
@@ -164,7 +166,7 @@ def nnf(cfg: Cfg, frames: np.ndarray, tasks: list[dict], want_x: bool = True):
     for i, t in enumerate(tasks):
         arr[i] = _Task(t["src_guide"], t["tgt_guide"], t.get("src_style", -1), t.get("tgt_style", -1),
                        t.get("group", i), t.get("src_id", 0), t.get("tgt_id", 0), t.get("tag", TAG_API),
-                       t.get("partner", -1))
+                       t.get("partner", -1), t.get("track_prev", -1), t.get("track_next", -1))
     F = np.zeros((T, H, W, 2), np.int32)
     E = np.zeros((T, H, W), np.float32)
     X = np.zeros((T, H, W, 3), np.float32) if want_x else None
@@ -260,4 +262,20 @@ def field(cfg: Cfg, sg, tg, F, E, field_id: int, ss=None, aux=None, k: int = 0, 
     cc = cfg.c()
     load().orc_field_step(C.byref(cc), h, w, _p(sg), _p(tg), None if ss_ is None else _p(ss_),
                           None if aux_ is None else _p(aux_), field_id, step, k, it, src_id, tgt_id, tag, _p(F), _p(E))
+    return F, E
+
+
+def track_field(cfg: Cfg, sg, tg, G, F, E, ss=None, aux=None):
+    """One tracking field (D42): candidate F'(x) = G(x), strict-min select.  Returns (F, E)."""
+    sg = np.ascontiguousarray(sg, np.float32)
+    tg = np.ascontiguousarray(tg, np.float32)
+    h, w, _ = sg.shape
+    G = np.ascontiguousarray(G, np.int32)
+    F = np.array(F, np.int32, copy=True, order="C")
+    E = np.array(E, np.float32, copy=True, order="C")
+    ss_ = None if ss is None else np.ascontiguousarray(ss, np.float32)
+    aux_ = None if aux is None else np.ascontiguousarray(aux, np.float32)
+    cc = cfg.c()
+    load().orc_track_field(C.byref(cc), h, w, _p(sg), _p(tg), None if ss_ is None else _p(ss_),
+                           None if aux_ is None else _p(aux_), _p(G), _p(F), _p(E))
     return F, E

@@ -672,3 +672,69 @@ def test_jump_flood_converges_at_least_as_fast_on_a_shift():
         F, E, _, _ = O.nnf(cfg, frames, task, want_x=False)
         good[J] = np.mean(E[0] == 0)
     assert good[5] >= good[1]
+
+
+# ------------------------------------------------------------------ tracking (f2, D42)
+def test_tracking_field_takes_neighbour_field_where_strictly_better():
+    """P:256-259 / D42: a tracking field proposes the neighbouring frame's NNF at the same pixel,
+    F'(x) = G(x), kept iff its loss is strictly smaller (D16)."""
+    h, w, p = 20, 24, 2
+    S, T, Ftrue = _shifted_pair(h, w, 2, 1, seed=8)
+    cfg = O.Cfg(patch_radius=p, loss=O.BASE, levels=1)
+    rng = np.random.default_rng(3)
+    Fin = np.stack([rng.integers(0, h, (h, w)), rng.integers(0, w, (h, w))], -1).astype(np.int32)
+    _, Ein = O.field(cfg, S, T, Fin, np.zeros((h, w), np.float32), -1)
+    G = Ftrue.copy()
+    G[rng.random((h, w)) < 0.4] = 0  # a partly wrong neighbour field
+    Fout, Eout = O.track_field(cfg, S, T, G, Fin, Ein)
+    lossG = np_patch_dist_field(S, T, G, p).astype(np.float32)
+    take = lossG < Ein
+    np.testing.assert_array_equal(Fout[take], G[take])
+    np.testing.assert_array_equal(Fout[~take], Fin[~take])
+    np.testing.assert_array_equal(Eout, np.where(take, lossG, Ein))
+
+
+def test_tracking_adds_one_field_per_neighbour():
+    """Interpolation with tracking evaluates, per iteration, one extra field for every existing
+    neighbour task of the same key (T_{i-1}, T_{i+1})."""
+    N = 6
+    g, s = moving_texture(N, 32, 32, seed=31)
+    keys = [0]
+    base = O.Cfg(iters_per_level=2)
+    _, pairs, ev0 = O.interpolate(base, g, keys, s[keys])
+    tr = O.Cfg(iters_per_level=2, tracking=1)
+    _, _, ev1 = O.interpolate(tr, g, keys, s[keys])
+    npx = sum((32 >> k) * (32 >> k) for k in range(O.level_count(32, 32, 2)))
+    links = 2 * (pairs - 1)  # a chain of `pairs` tasks for targets 1..5 of key 0
+    assert ev1 - ev0 == links * npx * 2
+
+
+def test_tracking_closure_is_the_whole_span():
+    """With tracking the estimation of frame m depends on its neighbours, so a targets subset must
+    equal the same frames of the full run."""
+    g, s = moving_texture(7, 32, 32, seed=32)
+    cfg = O.Cfg(iters_per_level=1, tracking=1)
+    full, _, _ = O.interpolate(cfg, g, [0, 6], s[[0, 6]])
+    sub, _, _ = O.interpolate(cfg, g, [0, 6], s[[0, 6]], targets=[3, 1])
+    np.testing.assert_array_equal(sub[0], full[3])
+    np.testing.assert_array_equal(sub[1], full[1])
+
+
+def test_tracking_is_jacobi_across_frames():
+    """D42: the neighbours' NNFs are frozen at the iteration start, so the result does not depend on
+    the order in which the coupled estimations are processed."""
+    g, s = moving_texture(4, 32, 36, seed=33)
+    frames = np.concatenate([g, s[:1]]).astype(np.float32)
+    cfg = O.Cfg(iters_per_level=2, tracking=1)
+
+    def tasks(order):
+        pos = {m: order.index(m) for m in order}
+        out = []
+        for m in order:
+            out.append(dict(src_guide=0, tgt_guide=m, src_style=4, src_id=0, tgt_id=m, tag=5,
+                            track_prev=pos.get(m - 1, -1), track_next=pos.get(m + 1, -1)))
+        return out
+    Fa, Ea, _, _ = O.nnf(cfg, frames, tasks([1, 2, 3]), want_x=False)
+    Fb, Eb, _, _ = O.nnf(cfg, frames, tasks([3, 2, 1]), want_x=False)
+    np.testing.assert_array_equal(Fa, Fb[::-1])
+    np.testing.assert_array_equal(Ea, Eb[::-1])
