@@ -68,7 +68,8 @@ typedef struct {
     uint64_t seed;           /* Philox4x32-10 key (D21)                                             */
     int32_t prop_scales;     /* propagation scales J (jump flood, D41): steps 2^(J-1)..1, each with the
                                 four directions of P:72; 0 or 1 = the paper's unit-step propagation   */
-    int32_t reserved;        /* must be 0                                                           */
+    int32_t tracking;        /* interpolation: add NNF(S,T_{i-1}), NNF(S,T_{i+1}) as candidate fields
+                                (D42); 0 = off                                            */
 } fb_match_cfg;
 
 typedef struct {
@@ -172,7 +173,9 @@ fb_status fb_blend_window_range(fb_ctx ctx, const fb_match_cfg* cfg, int schedul
  * l < m < r is fma(X_l, (r-m)/(r-l), X_r * ((m-l)/(r-l))) with X_k the remap of key k's style under
  * NNF(G_k, G_m); frames outside the key span take the nearest key's remap.  The NNFs use the GUIDE_STYLE
  * loss, except cfg.loss = PAIRWISE: then the two NNFs of every frame between two keys are estimated
- * jointly with the alignment loss of Eq. 10. */
+ * jointly with the alignment loss of Eq. 10.  cfg.tracking = 1 adds the object tracking of
+ * P:256-259 (D42): each NNF(S_k, G_m) also tries NNF(S_k, G_{m-1}) and NNF(S_k, G_{m+1}) (frozen at the
+ * start of every iteration) as whole candidate fields; all frames of a key span advance in lockstep. */
 fb_status fb_interpolate_keyframes(fb_ctx ctx, const fb_match_cfg* cfg, int N, int H, int W, const uint8_t* guide,
                                    int K, const int32_t* key_index, const uint8_t* key_style, float* out,
                                    fb_stats* stats);

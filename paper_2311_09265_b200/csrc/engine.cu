@@ -225,6 +225,7 @@ void validate_cfg(const fb_match_cfg* cfg)
     if (cfg->loss < 0 || cfg->loss > 3) throw Fail{FB_ERR_INVALID_ARG, "unknown loss"};
     if (cfg->init < 0 || cfg->init > 1) throw Fail{FB_ERR_INVALID_ARG, "unknown init"};
     if (cfg->prop_scales < 0 || cfg->prop_scales > 12) throw Fail{FB_ERR_INVALID_ARG, "prop_scales not in [0, 12]"};
+    if (cfg->tracking < 0 || cfg->tracking > 1) throw Fail{FB_ERR_INVALID_ARG, "tracking must be 0 or 1"};
 }
 
 // ------------------------------------------------------------------------------------ pyramids
@@ -308,6 +309,7 @@ struct TaskSpec {
     int group;         // MEAN_ALIGN window index (into groups), else -1
     uint32_t src_id, tgt_id, tag;
     int partner = -1;  // PAIRWISE: index of the counterpart task in the batch (Eq. 10, D38)
+    int track[2] = {-1, -1};  // tracking: batch indices of the tasks for T_{i-1}, T_{i+1} (D42)
 };
 struct GroupSpec {
     const float4* tstyle;  // target style pyramid (the self term of T-bar)
@@ -337,8 +339,14 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
     tbytes = (tbytes + 255) & ~size_t(255);
     const bool per_group = cfg.loss == FB_LOSS_MEAN_ALIGN;
     const bool pairwise = cfg.loss == FB_LOSS_PAIRWISE;
+    bool tracking = false;
+    uint64_t track_links = 0;
+    for (const TaskSpec& k : tasks)
+        for (int z = 0; z < 2; ++z)
+            if (k.track[z] >= 0) { tracking = true; ++track_links; }
     char* tgt = ex.ar.take<char>(tbytes * (per_group ? groups.size() : (size_t)T));
-    int2* Fsnap = pairwise ? ex.ar.take<int2>((size_t)T * n0) : nullptr;  // counterpart NNFs (D39)
+    // NNFs frozen at the start of each iteration: counterparts (D39) and tracking neighbours (D42)
+    int2* Fsnap = (pairwise || tracking) ? ex.ar.take<int2>((size_t)T * n0) : nullptr;
     std::vector<DTask> dt(T);
     for (int t = 0; t < T; ++t) {
         const TaskSpec& k = tasks[t];
@@ -350,6 +358,7 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
         dt[t].c3 = (k.tag << 28) | k.tgt_id;
         dt[t].psrc = pairwise ? tasks[k.partner].src : nullptr;
         dt[t].pF = pairwise ? Fsnap + (long long)k.partner * n0 : nullptr;
+        for (int z = 0; z < 2; ++z) dt[t].trk[z] = k.track[z] >= 0 ? Fsnap + (long long)k.track[z] * n0 : nullptr;
     }
     const DTask* d_tasks = ex.upload(dt);
     // T-bar member lists for every level (MEAN_ALIGN): ascending source id with the self term inserted.
@@ -406,12 +415,12 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
             ex.launch("pack_tgt", [&] { return fbk::launch_pack_tgt_guide(d_tasks, T, L, PL, tfmt, s); });
         const int rk = rs_count(cfg, L), r0 = rs_r0(cfg, L);
         for (int it = 0; it < cfg.iters_per_level; ++it) {
+            if (Fsnap)  // freeze counterpart / tracking NNFs for this iteration (D39, D42)
+                ex.d2d(Fsnap, F[cur], sizeof(int2) * (size_t)T * n0);
             if (cfg.loss == FB_LOSS_GUIDE_STYLE) {  // S^ refresh (D17/D18)
                 ex.launch("aux", [&] { return fbk::launch_aux_remap(d_tasks, T, F[cur], n0, L, PL, g.p, tfmt, s); },
                           (uint64_t)T * L.h * L.w);
                 if (st) st->remap_pixels += (uint64_t)T * L.h * L.w;
-            } else if (pairwise) {  // freeze the counterpart NNFs for this iteration (Eq. 10, D39)
-                ex.d2d(Fsnap, F[cur], sizeof(int2) * (size_t)T * n0);
             } else if (per_group) {  // T-bar refresh (Eq. 7, D27)
                 ex.launch(k == 0 ? "tbar.L0" : "tbar.L1+", [&] { return fbk::launch_combine(d_outs[k], (int)groups.size(), d_mem[k], F[cur], n0,
                                                                    L.h, L.w, g.p, fast ? 2 : 3, PL, s); },
@@ -470,6 +479,8 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
     if (st) {
         st->nnf_pairs += (uint64_t)T;
         st->candidate_evals += (uint64_t)T * evals_per_pair(cfg, g);
+        for (int k = 0; k < g.Lv; ++k)  // tracking fields (D42)
+            st->candidate_evals += track_links * (uint64_t)g.L[k].h * g.L[k].w * (uint64_t)cfg.iters_per_level;
     }
     return out;
 }
@@ -765,7 +776,15 @@ void interpolate(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N, const 
         cfg.loss = pass == 1 ? FB_LOSS_PAIRWISE : FB_LOSS_GUIDE_STYLE;
         std::vector<int> cost;
         for (const Tgt& t : tg[pass]) cost.push_back(t.key >= 0 ? 0 : (t.left >= 0) + (t.right >= 0));
-        for (auto [b0, b1] : make_batches(cost, batch_pairs(ex.ctx, g, cfg.loss))) {
+        // with tracking every frame of a pass is coupled to its neighbours (D42): one batch per pass
+        int cap = batch_pairs(ex.ctx, g, cfg.loss);
+        if (cfg0.tracking) {
+            long long total = 0;
+            for (int c : cost) total += c;
+            if (total > kMaxBatchPairs) throw Fail{FB_ERR_UNSUPPORTED, "tracking needs all pairs of a key span in one batch"};
+            cap = (int)std::max<long long>(cap, total);
+        }
+        for (auto [b0, b1] : make_batches(cost, cap)) {
             ex.ar.off = mark;
             std::vector<TaskSpec> tasks;
             std::vector<int> tl(b1 - b0, -1), tr(b1 - b0, -1);
@@ -785,6 +804,16 @@ void interpolate(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N, const 
                 if (pass == 1) {  // counterparts (Eq. 10)
                     tasks[tl[q - b0]].partner = tr[q - b0];
                     tasks[tr[q - b0]].partner = tl[q - b0];
+                }
+            }
+            if (cfg0.tracking) {  // D42: same keyframe, targets m-1 / m+1 (tasks of this pass)
+                std::map<std::pair<uint32_t, uint32_t>, int> by;  // (key frame id, target id) -> task
+                for (int t = 0; t < (int)tasks.size(); ++t) by[{tasks[t].src_id, tasks[t].tgt_id}] = t;
+                for (auto& tk : tasks) {
+                    auto p = by.find({tk.src_id, tk.tgt_id - 1});
+                    auto n = by.find({tk.src_id, tk.tgt_id + 1});
+                    tk.track[0] = p != by.end() ? p->second : -1;
+                    tk.track[1] = n != by.end() ? n->second : -1;
                 }
             }
             BatchOut bo;

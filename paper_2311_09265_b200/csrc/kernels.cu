@@ -536,6 +536,15 @@ __global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
         }
     }
     if (PHASE == 3 && a.do_rs) {
+#pragma unroll
+        for (int z = 0; z < 2; ++z)  // tracking fields T_{i-1}, T_{i+1} (D42)
+            if (T.trk[z]) {
+                const int2 g = __ldg(&T.trk[z][i]);
+                if (g.x != f.x || g.y != f.y) {
+                    const float e2 = loss(g.x, g.y, e);
+                    if (e2 < e) { f = g; e = e2; }
+                }
+            }
         for (int s = 0; s < a.rs_k; ++s) {
             const int R = max(a.rs_r0 >> s, 1);
             const uint4 u = philox4x32_10(
@@ -710,6 +719,12 @@ __global__ void __launch_bounds__(32 * (IT_TY + 1), IT_MINB) k_iter_fast(FieldAr
         const int2 fn = c + 1 < w ? fr : f;
         select(f, e, fn.x, max(fn.y - 1, 0));
     }
+#pragma unroll
+    for (int z = 0; z < 2; ++z)  // tracking fields T_{i-1}, T_{i+1} (D42)
+        if (T.trk[z]) {
+            const int2 g = __ldg(&T.trk[z][i]);
+            select(f, e, g.x, g.y);
+        }
     for (int s = 0; s < a.rs_k; ++s) {
         const int R = max(a.rs_r0 >> s, 1);
         const uint4 u = philox4x32_10(
@@ -863,6 +878,12 @@ __global__ void __launch_bounds__(32 * I13_TY, 3) k_iter13_fast(FieldArgs a)
         const int2 fn = c + 1 < w ? fr : f;
         select(f, e, fn.x, max(fn.y - 1, 0));
     }
+#pragma unroll
+    for (int z = 0; z < 2; ++z)  // tracking fields T_{i-1}, T_{i+1} (D42)
+        if (T.trk[z]) {
+            const int2 g = __ldg(&T.trk[z][i]);
+            select(f, e, g.x, g.y);
+        }
     for (int s = 0; s < a.rs_k; ++s) {
         const int R = max(a.rs_r0 >> s, 1);
         const uint4 u = philox4x32_10(
@@ -1001,6 +1022,15 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
         }
     }
     if (PHASE == 3 && a.do_rs) {
+#pragma unroll
+        for (int z = 0; z < 2; ++z)  // tracking fields T_{i-1}, T_{i+1} (D42)
+            if (T.trk[z]) {
+                const int2 g = __ldg(&T.trk[z][i]);
+                if (g.x != f.x || g.y != f.y) {
+                    const float e2 = loss(g.x, g.y, e);
+                    if (e2 < e) { f = g; e = e2; }
+                }
+            }
         for (int s = 0; s < a.rs_k; ++s) {
             const int R = max(a.rs_r0 >> s, 1);
             const uint4 u = philox4x32_10(

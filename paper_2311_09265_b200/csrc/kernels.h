@@ -41,6 +41,7 @@ struct DTask {
     uint32_t c3;       // Philox counter word 3: tag << 28 | target frame id (D21)
     const char* psrc;  // PAIRWISE (Eq. 10): the counterpart task's packed source slot (its keyframe style)
     const int2* pF;    // PAIRWISE: the counterpart's NNF at the start of the iteration (D39), [h_k*w_k]
+    const int2* trk[2];  // tracking (D42): NNFs of the tasks for T_{i-1}, T_{i+1} at the iteration start
 };
 
 // Geometry of one pyramid level (unpadded float4 pyramids).

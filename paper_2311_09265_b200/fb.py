@@ -40,7 +40,7 @@ class _Cfg(C.Structure):
     _fields_ = [("patch_radius", C.c_int32), ("levels", C.c_int32), ("iters_per_level", C.c_int32),
                 ("rs_radius0", C.c_int32), ("rs_steps", C.c_int32), ("alpha", C.c_float),
                 ("loss", C.c_int32), ("init", C.c_int32), ("seed", C.c_uint64), ("prop_scales", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("tracking", C.c_int32)]
 
 
 class _Stats(C.Structure):
@@ -73,10 +73,11 @@ class MatchCfg:
     init: int = INIT_RANDOM
     seed: int = 1
     prop_scales: int = 1
+    tracking: int = 0
 
     def c(self) -> _Cfg:
         return _Cfg(self.patch_radius, self.levels, self.iters_per_level, self.rs_radius0, self.rs_steps,
-                    self.alpha, self.loss, self.init, self.seed, self.prop_scales, 0)
+                    self.alpha, self.loss, self.init, self.seed, self.prop_scales, self.tracking)
 
 
 _lib = None

@@ -25,7 +25,7 @@ def ctx(P):
 
 def ocfg(c):
     return O.Cfg(c.patch_radius, c.levels, c.iters_per_level, c.rs_radius0, c.rs_steps, c.alpha, c.loss, c.init, c.seed,
-                 c.prop_scales)
+                 c.prop_scales, c.tracking)
 
 
 def check(got, ref):

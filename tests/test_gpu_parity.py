@@ -30,7 +30,7 @@ def ctx(fb):
 
 def ocfg(c):
     return O.Cfg(c.patch_radius, c.levels, c.iters_per_level, c.rs_radius0, c.rs_steps, c.alpha, c.loss, c.init, c.seed,
-                 c.prop_scales)
+                 c.prop_scales, c.tracking)
 
 
 def dev(a):
@@ -312,4 +312,16 @@ def test_jump_flood_blend_parity(fb, ctx, mode):
     fn = O.blend_tree if mode == "fast" else O.blend_direct
     ref, pairs, evals = fn(ocfg(cfg), g, s, 2)
     assert st["candidate_evals"] == evals
+    assert_frames(out, ref)
+
+
+# ------------------------------------------------------------------------------ f2 tracking (D42)
+@pytest.mark.parametrize("keys,align", [([0, 8], False), ([0, 8], True), ([3], False), ([1, 5, 9], True)])
+def test_tracking_interpolation_parity(fb, ctx, keys, align):
+    N = 10
+    g, s = moving_texture(N, 40, 44, seed=27)
+    cfg = fb.MatchCfg(iters_per_level=2, loss=fb.PAIRWISE if align else fb.GUIDE_STYLE, tracking=1)
+    out, st = ctx.fb_interpolate_keyframes(cfg, dev(g), keys, dev(s[keys]))
+    ref, pairs, evals = O.interpolate(ocfg(cfg), g, keys, s[keys])
+    assert st["nnf_pairs"] == pairs and st["candidate_evals"] == evals
     assert_frames(out, ref)
