@@ -273,7 +273,7 @@ struct Slots {
 Slots pack_sources(Exec& ex, const Geo& g, int fmt0, const std::vector<SlotSpec>& specs)
 {
     Slots S;
-    if (g.p > 2) fmt0 = fbk::SF32;  // the register-resident fast kernels are compiled for p <= 2 only
+    if (g.p > 2 && fmt0 == fbk::SF8F) fmt0 = fbk::SF32;  // float styles at p > 2: general kernel
     S.fmt0 = fmt0;
     size_t off = 0;
     for (int k = 0; k < g.Lv; ++k) {
@@ -328,7 +328,9 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
     const int T = (int)tasks.size();
     const long long n0 = g.npx0();
     const cudaStream_t s = ex.ctx->stream;
-    const bool fast0 = (slots.fmt0 == fbk::SF8 || slots.fmt0 == fbk::SF8F) && g.p <= 2;  // level-0 fast operands
+    // level 0 uses packed u8 operands (TF16 targets) with SF8 / SF8F sources: in registers (fast kernels,
+    // p <= 2) or as a shared-memory tile (mid kernel, p = 3, 4)
+    const bool fast0 = slots.fmt0 == fbk::SF8 || slots.fmt0 == fbk::SF8F;
     BatchOut out;
     out.fstride = n0;
     int2* F[2] = {ex.ar.take<int2>((size_t)T * n0), ex.ar.take<int2>((size_t)T * n0)};
@@ -402,8 +404,10 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
     for (int k = g.Lv - 1; k >= 0; --k) {
         const Lvl L = g.L[k];
         const fbk::PLvl PL = g.PL[k];
-        const bool fast = k == 0 && fast0;
-        const int tfmt = fast ? fbk::TF16 : fbk::TF32;
+        const bool tf16 = k == 0 && fast0;
+        const bool fast = tf16 && g.p <= 2;                 // kernel kind 1
+        const int kind = fast ? 1 : (tf16 ? 2 : 0);        // 2: mid kernel (p = 3, 4)
+        const int tfmt = tf16 ? fbk::TF16 : fbk::TF32;
         if (k == g.Lv - 1) {
             ex.launch("init", [&] { return fbk::launch_init(d_tasks, T, F[cur], n0, L, cfg.init == FB_INIT_IDENTITY,
                                                             rng, (uint32_t)k, s); });
@@ -423,7 +427,7 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
                 if (st) st->remap_pixels += (uint64_t)T * L.h * L.w;
             } else if (per_group) {  // T-bar refresh (Eq. 7, D27)
                 ex.launch(k == 0 ? "tbar.L0" : "tbar.L1+", [&] { return fbk::launch_combine(d_outs[k], (int)groups.size(), d_mem[k], F[cur], n0,
-                                                                   L.h, L.w, g.p, fast ? 2 : 3, PL, s); },
+                                                                   L.h, L.w, g.p, tf16 ? 2 : 3, PL, s); },
                           (uint64_t)T * L.h * L.w);
                 if (st) st->remap_pixels += (uint64_t)T * L.h * L.w;
             }
@@ -451,7 +455,7 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
                 const bool last = j == 0;
                 if (last && fast && ex.ctx->fuse13) {  // field 0, then fields 1-3 + random search in one launch
                     a.Fin = F[cur]; a.Fout = F[cur ^ 1];
-                    ex.launch(names[0], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, 0, fast, s); },
+                    ex.launch(names[0], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, 0, kind, s); },
                               (1ull + (uint64_t)a.einit) * T * L.h * L.w);
                     cur ^= 1;
                     char nm[32];
@@ -466,7 +470,7 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
                     a.Fin = F[cur]; a.Fout = F[cur ^ 1];
                     a.do_rs = last && ph == 3;
                     const uint64_t per_px = 1 + (ph == 0 ? (uint64_t)a.einit : 0) + (a.do_rs ? (uint64_t)rk : 0);
-                    ex.launch(names[ph], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, ph, fast, s); },
+                    ex.launch(names[ph], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, ph, kind, s); },
                               per_px * (uint64_t)T * L.h * L.w);
                     cur ^= 1;
                     a.einit = 0;
@@ -758,7 +762,7 @@ void interpolate(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N, const 
     std::vector<SlotSpec> specs;
     for (int k = 0; k < K; ++k)
         specs.push_back(SlotSpec{guide + 3 * n0 * keys[k], key_style + 3 * n0 * k, G.frame(keys[k]), KS.frame(k)});
-    const Slots KSl = pack_sources(ex, g, fbk::SF8, specs);
+    const Slots KSl = pack_sources(ex, g, (align && g.p > 2) ? fbk::SF32 : fbk::SF8, specs);
     struct Tgt { int m, left, right, key; };  // key indices (or -1)
     std::vector<Tgt> tg[2];  // [0]: keys and GUIDE_STYLE targets, [1]: aligned (two-key) targets
     for (int m = 0; m < N; ++m) {
@@ -855,7 +859,7 @@ void nnf_api(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int B, const uint8
     for (int b = 0; b < B; ++b)
         specs.push_back(SlotSpec{sg + 3 * np * b, cfg.loss != FB_LOSS_BASE ? ss + 3 * np * b : nullptr, SG.frame(b),
                                  cfg.loss != FB_LOSS_BASE ? SS.frame(b) : nullptr});
-    const Slots SL = pack_sources(ex, g, fbk::SF8, specs);
+    const Slots SL = pack_sources(ex, g, (cfg.loss == FB_LOSS_PAIRWISE && g.p > 2) ? fbk::SF32 : fbk::SF8, specs);
     std::vector<TaskSpec> tasks;
     std::vector<GroupSpec> groups;
     std::map<int32_t, int> gidx;

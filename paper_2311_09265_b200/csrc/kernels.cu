@@ -897,6 +897,115 @@ __global__ void __launch_bounds__(32 * I13_TY, 3) k_iter13_fast(FieldArgs a)
     a.E[t * a.fstride + i] = e;
 }
 
+// ---- level-0 variant for p = 3, 4: SF8 source, TF16 target tile in shared memory -----------------
+// The target patch of p >= 3 does not fit in registers, so it is staged per tile; the source rows and the
+// exact integer guide term (every partial < 2^24 for p <= 4 at level 0) are those of k_field_fast.
+template <int P, bool TWO, int PHASE>
+__global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_mid(FieldArgs a)
+{
+    constexpr int D = 2 * P + 1, SX = TILE_X + 2 * P, SY = TILE_Y + 2 * P;
+    constexpr int NCH = (D + 2) / 2;  // 16-byte chunks covering D texels from an even start
+    __shared__ uint4 tT[SY][SX];
+    const int t = blockIdx.x / a.tiles_per_task;
+    const int tile = blockIdx.x - t * a.tiles_per_task;
+    const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+    const int h = a.L.h, w = a.L.w, pitch = a.L.pitch;
+    const DTask T = a.tasks[t];
+    {
+        const uint4* Tt = reinterpret_cast<const uint4*>(T.tgt);
+        for (int k = threadIdx.x; k < SX * SY; k += TILE_X * TILE_Y) {
+            const int yy = k / SX, xx = k - yy * SX;
+            const int pr = ty * TILE_Y + yy - P + B, pc = tx * TILE_X + xx - P + B;
+            tT[yy][xx] = (pr < a.L.rows && pc < pitch) ? __ldg(&Tt[pr * pitch + pc]) : make_uint4(0u, 0u, 0u, 0u);
+        }
+    }
+    __syncthreads();
+    const int lx = threadIdx.x & (TILE_X - 1), ly = threadIdx.x / TILE_X;
+    const int c = tx * TILE_X + lx, r = ty * TILE_Y + ly;
+    if (r >= h || c >= w) return;
+    const uint2* S = reinterpret_cast<const uint2*>(T.src + a.src_off);
+    const int plane = a.L.rows * pitch;
+    auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
+        const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
+        const uint4* cp = reinterpret_cast<const uint4*>(
+            S + (kSF8Copies == 2 ? (size_t)(idx & 1) * plane + (idx & ~1) : (size_t)(idx & ~1)));
+        const int o = kSF8Copies == 2 ? 0 : (idx & 1);
+        uint32_t wd[4 * NCH];
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+            const uint4 v = __ldg(cp + k);
+            wd[4 * k] = v.x; wd[4 * k + 1] = v.y; wd[4 * k + 2] = v.z; wd[4 * k + 3] = v.w;
+        }
+        float rs = 0.0f;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const uint4 tv = tT[ly + dr][lx + j];
+            const uint32_t g = o ? wd[2 * j + 2] : wd[2 * j];
+            const uint32_t d = __vabsdiffu4(g, tv.x);
+            dg = __dp4a(d, d, dg);
+            if (TWO) {
+                const uint32_t sv = o ? wd[2 * j + 3] : wd[2 * j + 1];
+                float dl = __fsub_rn(__uint_as_float(tv.y), u8f(sv, 0)); rs = __fmaf_rn(dl, dl, rs);
+                dl = __fsub_rn(__uint_as_float(tv.z), u8f(sv, 1)); rs = __fmaf_rn(dl, dl, rs);
+                dl = __fsub_rn(__uint_as_float(tv.w), u8f(sv, 2)); rs = __fmaf_rn(dl, dl, rs);
+            }
+        }
+        if (TWO) ds = __fadd_rn(ds, rs);
+    };
+    auto loss = [&](int sr, int sc, float bound) -> float {
+        uint32_t dg = 0u;
+        float ds = 0.0f;
+        constexpr int S1 = PDE_GEN_S1(P), S2 = PDE_GEN_S2(P);
+#pragma unroll
+        for (int dr = 0; dr < S1; ++dr) row(sr, sc, dr, dg, ds);
+        if (partial_loss(a.alpha, __uint2float_rn(dg), ds, TWO) >= bound) return __int_as_float(0x7f800000);
+        if (S2 < D) {
+#pragma unroll
+            for (int dr = S1; dr < S2; ++dr) row(sr, sc, dr, dg, ds);
+            if (partial_loss(a.alpha, __uint2float_rn(dg), ds, TWO) >= bound) return __int_as_float(0x7f800000);
+        }
+#pragma unroll
+        for (int dr = (S2 < D ? S2 : S1); dr < D; ++dr) row(sr, sc, dr, dg, ds);
+        const float fg = __uint2float_rn(dg);
+        return TWO ? __fmaf_rn(a.alpha, fg, ds) : fg;
+    };
+    auto select = [&](int2& f, float& e, int sr, int sc) {
+        if (sr == f.x && sc == f.y) return;  // incumbent-equal candidates cannot win
+        const float e2 = loss(sr, sc, e);
+        if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+    };
+    const int2* Fi = a.Fin + t * a.fstride;
+    const int i = r * w + c;
+    int2 f = Fi[i];
+    float e = PHASE == 0 && a.einit ? loss(f.x, f.y, __int_as_float(0x7f800000)) : a.E[t * a.fstride + i];
+    {
+        const int dx = (PHASE == 0 ? -1 : (PHASE == 1 ? 1 : 0)) * a.step;
+        const int dy = (PHASE == 2 ? -1 : (PHASE == 3 ? 1 : 0)) * a.step;
+        const int nr = clampi(r + dx, 0, h - 1), nc = clampi(c + dy, 0, w - 1);  // D11
+        const int2 fn = Fi[nr * w + nc];
+        select(f, e, clampi(fn.x - dx, 0, h - 1), clampi(fn.y - dy, 0, w - 1));  // D10
+    }
+    if (PHASE == 3 && a.do_rs) {
+#pragma unroll
+        for (int z = 0; z < 2; ++z)  // tracking fields (D42)
+            if (T.trk[z]) {
+                const int2 g = __ldg(&T.trk[z][i]);
+                select(f, e, g.x, g.y);
+            }
+        for (int s = 0; s < a.rs_k; ++s) {
+            const int R = max(a.rs_r0 >> s, 1);
+            const uint4 u = philox4x32_10(
+                make_uint4((uint32_t)i, (1u << 28) | (a.level << 22) | (a.iter << 12) | (uint32_t)s, T.c2, T.c3),
+                a.rng.k0, a.rng.k1);
+            const uint32_t span = 2u * (uint32_t)R + 1u;
+            const int ox = (int)__umulhi(u.x, span) - R, oy = (int)__umulhi(u.y, span) - R;
+            select(f, e, clampi(f.x + ox, 0, h - 1), clampi(f.y + oy, 0, w - 1));
+        }
+    }
+    a.Fout[t * a.fstride + i] = f;
+    a.E[t * a.fstride + i] = e;
+}
+
 // ---- general variant: SF32 source, TF32 target staged in shared memory (any level, P <= 4) -------
 
 template <int P, bool TWO, int PHASE, int SFMT, bool PW = false>
@@ -1205,12 +1314,32 @@ cudaError_t launch_iter13_fast(const FieldArgs& a0, int T, int p, int loss, cuda
     return cudaGetLastError();
 }
 
-cudaError_t launch_field(const FieldArgs& a0, int T, int p, int loss, int phase, bool fast, cudaStream_t s)
+template <int P, bool TWO>
+static void launch_field_mid(const FieldArgs& a, int T, int phase, cudaStream_t s)
 {
+    const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(TILE_X * TILE_Y);
+    switch (phase) {
+    case 0: k_field_mid<P, TWO, 0><<<grid, block, 0, s>>>(a); break;
+    case 1: k_field_mid<P, TWO, 1><<<grid, block, 0, s>>>(a); break;
+    case 2: k_field_mid<P, TWO, 2><<<grid, block, 0, s>>>(a); break;
+    default: k_field_mid<P, TWO, 3><<<grid, block, 0, s>>>(a); break;
+    }
+}
+
+cudaError_t launch_field(const FieldArgs& a0, int T, int p, int loss, int phase, int kind, cudaStream_t s)
+{
+    const bool fast = kind == 1;
     FieldArgs a = a0;
     a.tiles_x = (a.L.w + TILE_X - 1) / TILE_X;
     a.tiles_per_task = a.tiles_x * ((a.L.h + (fast ? FAST_TY : TILE_Y) - 1) / (fast ? FAST_TY : TILE_Y));
     const bool pw = loss == 3;
+    if (kind == 2) {  // level 0, p = 3, 4: SF8 source, TF16 target tile (not PAIRWISE)
+        if (pw || a.src_fmt != SF8) return cudaErrorInvalidValue;
+        if (p == 3) { if (loss) launch_field_mid<3, true>(a, T, phase, s); else launch_field_mid<3, false>(a, T, phase, s); }
+        else if (p == 4) { if (loss) launch_field_mid<4, true>(a, T, phase, s); else launch_field_mid<4, false>(a, T, phase, s); }
+        else return cudaErrorInvalidValue;
+        return cudaGetLastError();
+    }
     if (fast && a.src_fmt == SF8F) {  // float-style level-0 sources (tree queries): GUIDE_STYLE only
         if (pw || !loss) return cudaErrorInvalidValue;
         if (p == 1) launch_field_fast<1, true, false, 1>(a, T, phase, s);
@@ -1229,16 +1358,14 @@ cudaError_t launch_field(const FieldArgs& a0, int T, int p, int loss, int phase,
             return cudaErrorInvalidValue;
         }
     } else if (a.src_fmt == SF16) {
-        if (p == 1) {
-            if (pw) launch_field_gen<1, true, SF16, true>(a, T, phase, s);
-            else if (loss) launch_field_gen<1, true, SF16>(a, T, phase, s);
-            else launch_field_gen<1, false, SF16>(a, T, phase, s);
-        } else if (p == 2) {
-            if (pw) launch_field_gen<2, true, SF16, true>(a, T, phase, s);
-            else if (loss) launch_field_gen<2, true, SF16>(a, T, phase, s);
-            else launch_field_gen<2, false, SF16>(a, T, phase, s);
+        if (pw) {
+            if (p == 1) launch_field_gen<1, true, SF16, true>(a, T, phase, s);
+            else if (p == 2) launch_field_gen<2, true, SF16, true>(a, T, phase, s);
+            else return cudaErrorInvalidValue;
+        } else if (loss) {
+            FB_DISPATCH_P(p, (launch_field_gen<PP, true, SF16>(a, T, phase, s)));
         } else {
-            return cudaErrorInvalidValue;
+            FB_DISPATCH_P(p, (launch_field_gen<PP, false, SF16>(a, T, phase, s)));
         }
     } else if (pw) {
         FB_DISPATCH_P(p, (launch_field_gen<PP, true, SF32, true>(a, T, phase, s)));

@@ -119,9 +119,10 @@ cudaError_t launch_aux_remap(const DTask* tasks, int T, const int2* F, long long
 cudaError_t launch_combine(const DOut* outs, int n_outs, const DMember* mem, const int2* F, long long fstride,
                            int h, int w, int p, int fmt, PLvl P, cudaStream_t s);
 // phase 0: E init + propagation (-1,0); 1: (+1,0); 2: (0,-1); 3: (0,+1) + all random-search steps.
-// fast = SF8/TF16 operands (target patch in registers); otherwise SF32/TF32 (target tile in smem).
+// kind: 0 general (SF16/SF32 source, TF32 target tile in smem), 1 fast (SF8/SF8F, TF16 target patch in
+// registers, p <= 2), 2 mid (level 0, p = 3..4: SF8 source, TF16 target tile in smem).
 // loss: fb_loss (0 BASE, 1 GUIDE_STYLE, 2 MEAN_ALIGN, 3 PAIRWISE).
-cudaError_t launch_field(const FieldArgs& a, int T, int p, int loss, int phase, bool fast, cudaStream_t s);
+cudaError_t launch_field(const FieldArgs& a, int T, int p, int loss, int phase, int kind, cudaStream_t s);
 // The whole updating sequence of one iteration (E init, four propagation fields, random search) in one
 // launch, fast operands only (SF8/TF16, p <= 2).  Fin -> Fout, E written.
 cudaError_t launch_iter_fast(const FieldArgs& a, int T, int p, int loss, cudaStream_t s);
