@@ -323,7 +323,8 @@ struct BatchOut {
 };
 
 BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& slots,
-                 const std::vector<TaskSpec>& tasks, const std::vector<GroupSpec>& groups, fb_stats* st)
+                 const std::vector<TaskSpec>& tasks, const std::vector<GroupSpec>& groups, fb_stats* st,
+                 bool want_E = false)
 {
     const int T = (int)tasks.size();
     const long long n0 = g.npx0();
@@ -335,6 +336,11 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
     out.fstride = n0;
     int2* F[2] = {ex.ar.take<int2>((size_t)T * n0), ex.ar.take<int2>((size_t)T * n0)};
     out.E = ex.ar.take<float>((size_t)T * n0);
+    // The fused fields-1-3 kernel must not overwrite E in place: its halo lanes read the field-0 E of pixels
+    // owned by neighbouring tiles.  Its final E goes to a second buffer, needed only when the caller asks
+    // for E (the next iteration recomputes E <- L(F) anyway, D17).
+    float* E_final = want_E ? ex.ar.take<float>((size_t)T * n0) : nullptr;
+    bool e_final_used = false;
     size_t tbytes = 0;  // one packed target operand, largest level
     for (int k = 0; k < g.Lv; ++k)
         tbytes = std::max(tbytes, (size_t)g.PL[k].rows * g.PL[k].pitch * ((k == 0 && fast0) ? 16 : 32));
@@ -422,7 +428,8 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
             if (Fsnap)  // freeze counterpart / tracking NNFs for this iteration (D39, D42)
                 ex.d2d(Fsnap, F[cur], sizeof(int2) * (size_t)T * n0);
             if (cfg.loss == FB_LOSS_GUIDE_STYLE) {  // S^ refresh (D17/D18)
-                ex.launch("aux", [&] { return fbk::launch_aux_remap(d_tasks, T, F[cur], n0, L, PL, g.p, tfmt, s); },
+                ex.launch("aux", [&] { return fbk::launch_aux_remap(d_tasks, T, F[cur], n0, L, PL, g.p, tfmt,
+                                                                       src_fmt(slots.fmt0, k), (long long)slots.off[k], s); },
                           (uint64_t)T * L.h * L.w);
                 if (st) st->remap_pixels += (uint64_t)T * L.h * L.w;
             } else if (per_group) {  // T-bar refresh (Eq. 7, D27)
@@ -461,6 +468,8 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
                     char nm[32];
                     snprintf(nm, sizeof nm, "field123.L%d", k);
                     a.Fin = F[cur]; a.Fout = F[cur ^ 1];
+                    a.Eout = E_final;
+                    e_final_used = k == 0 && it == cfg.iters_per_level - 1;
                     ex.launch(nm, [&] { return fbk::launch_iter13_fast(a, T, g.p, cfg.loss, s); },
                               (uint64_t)(3 + rk) * T * L.h * L.w);
                     cur ^= 1;
@@ -480,6 +489,7 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
         }
     }
     out.F = F[cur];
+    if (e_final_used) out.E = E_final;
     if (st) {
         st->nnf_pairs += (uint64_t)T;
         st->candidate_evals += (uint64_t)T * evals_per_pair(cfg, g);
@@ -498,6 +508,14 @@ struct CombineList {
     void add_remap(const float4* src_level_img, int task, float w)
     {
         mem.push_back(DMember{src_level_img, task, w, nullptr, -1});
+        ++outs.back().nm;
+    }
+    // Remap read from the same image held exactly in a packed u8 slot (4 B per tap instead of 16; the
+    // kernel's exact integer form gives identical values); other slot formats use the float image.
+    void add_remap(const float4* src_level_img, int task, float w, const Slots& S, long long slot)
+    {
+        const bool u8 = src_fmt(S.fmt0, 0) == fbk::SF8;
+        mem.push_back(DMember{src_level_img, task, w, u8 ? S.slot(slot) + S.off[0] : nullptr, u8 ? fbk::SF8 : -1});
         ++outs.back().nm;
     }
     void end(void* out, int fmt, float div) { outs.back().out = out; outs.back().fmt = fmt; outs.back().div = div; }
@@ -589,7 +607,7 @@ void blend_direct(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int N_total, 
             cl.begin();
             for (int j = lo; j <= hi; ++j) {
                 if (j == i) cl.add_img(S.frame(i - lo_b), 1.0f);
-                else cl.add_remap(S.frame(j - lo_b), t++, 1.0f);
+                else cl.add_remap(S.frame(j - lo_b), t++, 1.0f, FR, j - lo_b);
             }
             cl.end(out + 3LL * n0 * q, 1, (float)(hi - lo + 1));
             if (st) st->remap_pixels += (uint64_t)(hi - lo) * n0;
@@ -830,12 +848,12 @@ void interpolate(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N, const 
                     cl.add_img(KS.frame(t.key), 1.0f);  // keyframes are not modified
                 } else if (t.left < 0 || t.right < 0) {
                     const int k = t.left >= 0 ? t.left : t.right;
-                    cl.add_remap(KS.frame(k), t.left >= 0 ? tl[q - b0] : tr[q - b0], 1.0f);
+                    cl.add_remap(KS.frame(k), t.left >= 0 ? tl[q - b0] : tr[q - b0], 1.0f, KSl, k);
                 } else {
                     const int l = keys[t.left], r = keys[t.right], m = t.m;
                     const float wl = (float)(r - m) / (float)(r - l), wr = (float)(m - l) / (float)(r - l);
-                    cl.add_remap(KS.frame(t.right), tr[q - b0], wr);  // A = X_r * w_r, then fma(X_l, w_l, A)
-                    cl.add_remap(KS.frame(t.left), tl[q - b0], wl);
+                    cl.add_remap(KS.frame(t.right), tr[q - b0], wr, KSl, t.right);  // A = X_r w_r, fma(X_l, w_l, A)
+                    cl.add_remap(KS.frame(t.left), tl[q - b0], wl, KSl, t.left);
                 }
                 cl.end(out + 3LL * n0 * t.m, 1, 1.0f);
             }
@@ -885,7 +903,7 @@ void nnf_api(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int B, const uint8
             tasks.back().partner = group[b];
         }
     }
-    BatchOut bo = run_nnf(ex, cfg, g, SL, tasks, groups, st);
+    BatchOut bo = run_nnf(ex, cfg, g, SL, tasks, groups, st, err_out != nullptr);
     const long long n0 = g.npx0();
     ex.d2d(nnf_out, bo.F, sizeof(int2) * (size_t)B * n0);
     if (err_out) ex.d2d(err_out, bo.E, sizeof(float) * (size_t)B * n0);

@@ -231,52 +231,68 @@ __device__ __forceinline__ float3 remap_px(const float4* __restrict__ S, const i
     return make_float3(__fdiv_rn(ax, fn), __fdiv_rn(ay, fn), __fdiv_rn(az, fn));
 }
 
-// S^ refresh (GUIDE_STYLE, P:120, D17/D18): packed target = {G_tgt, remap(S_src, F)} over the padded grid.
 // Same remap reading the style channels from a packed source slot (SF8: u8 word, SF16: two u16 words),
-// converted exactly; identical values, a quarter / half of the bytes per tap.
+// a quarter / half of the bytes per tap of the float4 pyramid.  Exact integer form: a slot holds every
+// style value as n * 4^-k with integer n (k = 0: u8; k = 1..4: SF16, D6), and a sum of at most (2P+1)^2
+// such values has sum(n) < 2^24, so the FP32 chain of D19 is exact, order-free and equal to
+// (float)sum(n) * 4^-k; the sums are kept in integers (SF8: r|b and g in 16-bit lanes) and the one IEEE
+// division by the valid count is unchanged.  Branch-free: the zero border (>= P texels) makes every tap
+// address valid (F is in bounds, so F - d lies within P of the image), and invalid taps are masked to 0.
 template <int P, int SFMT>
 __device__ __forceinline__ float3 remap_px_slot(const char* __restrict__ slot, int pitch, const int2* __restrict__ F,
-                                                int h, int w, int r, int c, uint32_t ex)
+                                                int h, int w, int r, int c, int k)
 {
-    float ax = 0.0f, ay = 0.0f, az = 0.0f;
+    uint32_t a0 = 0u, a1 = 0u, a2 = 0u;
     int n = 0;
 #pragma unroll
     for (int dr = -P; dr <= P; ++dr) {
         const int tr = r + dr;
-        if ((unsigned)tr >= (unsigned)h) continue;
+        const bool rin = (unsigned)tr < (unsigned)h;
+        const int trc = clampi(tr, 0, h - 1);
 #pragma unroll
         for (int dc = -P; dc <= P; ++dc) {
             const int tc = c + dc;
-            if ((unsigned)tc >= (unsigned)w) continue;
-            const int2 f = __ldg(&F[tr * w + tc]);
+            const int2 f = __ldg(&F[trc * w + clampi(tc, 0, w - 1)]);
             const int sr = f.x - dr, sc = f.y - dc;
-            if ((unsigned)sr >= (unsigned)h || (unsigned)sc >= (unsigned)w) continue;
+            const bool v = rin && (unsigned)tc < (unsigned)w && (unsigned)sr < (unsigned)h && (unsigned)sc < (unsigned)w;
             const int idx = (sr + kBorder) * pitch + sc + kBorder;
-            float vx, vy, vz;
             if (SFMT == SF8) {
-                const uint32_t sv = __ldg(reinterpret_cast<const uint32_t*>(slot) + 2 * idx + 1);
-                vx = u8f(sv, 0); vy = u8f(sv, 1); vz = u8f(sv, 2);
+                uint32_t sv = __ldg(reinterpret_cast<const uint32_t*>(slot) + 2 * idx + 1);
+                sv = v ? sv : 0u;
+                a0 += __byte_perm(sv, 0u, 0x4240u);  // r | b << 16
+                a1 += __byte_perm(sv, 0u, 0x4441u);  // g
             } else {
-                const uint2 sv = __ldg(reinterpret_cast<const uint2*>(slot) + 2 * idx + 1);
-                vx = u16f(sv.x, 0x7410u, ex); vy = u16f(sv.x, 0x7432u, ex); vz = u16f(sv.y, 0x7410u, ex);
+                uint2 sv = __ldg(reinterpret_cast<const uint2*>(slot) + 2 * idx + 1);
+                if (!v) sv = make_uint2(0u, 0u);
+                a0 += sv.x & 0xffffu;
+                a1 += sv.x >> 16;
+                a2 += sv.y;
             }
-            ax = __fadd_rn(ax, vx);
-            ay = __fadd_rn(ay, vy);
-            az = __fadd_rn(az, vz);
-            ++n;
+            n += v ? 1 : 0;
         }
     }
+    float x, y, z;
+    if (SFMT == SF8) {
+        x = (float)(a0 & 0xffffu); y = (float)a1; z = (float)(a0 >> 16);
+    } else {
+        const float sc = __int_as_float((127 - 2 * k) << 23);  // 4^-k, exact
+        x = __fmul_rn((float)a0, sc); y = __fmul_rn((float)a1, sc); z = __fmul_rn((float)a2, sc);
+    }
     const float fn = (float)n;
-    return make_float3(__fdiv_rn(ax, fn), __fdiv_rn(ay, fn), __fdiv_rn(az, fn));
+    return make_float3(__fdiv_rn(x, fn), __fdiv_rn(y, fn), __fdiv_rn(z, fn));
 }
 
-template <int P>
+// S^ refresh (GUIDE_STYLE, P:120, D17/D18): packed target = {G_tgt, remap(S_src, F)} over the padded grid.
+// SFMT = SF8 / SF16 reads the source style from the task's packed slot (exact integer form above); -1
+// reads the float4 style pyramid (float-style sources such as blending-table cells).
+template <int P, int SFMT>
 __global__ void k_aux_remap(const DTask* __restrict__ tasks, const int2* __restrict__ F, long long fstride, Lvl L,
-                            PLvl PL, int tfmt)
+                            PLvl PL, int tfmt, long long src_off)
 {
     const int t = blockIdx.y;
     const DTask T = tasks[t];
     const float4* S = T.ss + L.off;
+    const char* slot = T.src + src_off;
     const int2* Ft = F + t * fstride;
     const int n = PL.rows * PL.pitch;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -285,15 +301,21 @@ __global__ void k_aux_remap(const DTask* __restrict__ tasks, const int2* __restr
         float3 v = make_float3(0.f, 0.f, 0.f);
         float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
         if (in) {
-            v = remap_px<P>(S, Ft, L.h, L.w, r, c);
+            if (SFMT == SF8 || SFMT == SF16) v = remap_px_slot<P, SFMT>(slot, PL.pitch, Ft, L.h, L.w, r, c, PL.k);
+            else v = remap_px<P>(S, Ft, L.h, L.w, r, c);
             g = __ldg(&T.tg[L.off + r * L.w + c]);
         }
         store_tgt(T.tgt, tfmt, i, in, g, v.x, v.y, v.z);
     }
 }
 
+// 5 CTAs/SM caps registers at 51: the unrolled 25-tap remap otherwise takes ~100 registers and halves the
+// resident warps of this latency-bound gather (tbar.L0 66 -> 42 ms at N=48; 8 CTAs spill and lose again).
+#ifndef COMBINE_MINB
+#define COMBINE_MINB 5
+#endif
 template <int P, int FMT>
-__global__ void k_combine(const DOut* __restrict__ outs, const DMember* __restrict__ mem, const int2* __restrict__ F,
+__global__ void __launch_bounds__(256, COMBINE_MINB) k_combine(const DOut* __restrict__ outs, const DMember* __restrict__ mem, const int2* __restrict__ F,
                           long long fstride, int h, int w, PLvl PL)
 {
     const DOut o = outs[blockIdx.y];
@@ -315,10 +337,9 @@ __global__ void k_combine(const DOut* __restrict__ outs, const DMember* __restri
                     y = make_float3(v.x, v.y, v.z);
                 } else {
                     if (mb.sfmt == SF8)
-                        y = remap_px_slot<P, SF8>(mb.slot, PL.pitch, F + mb.task * fstride, h, w, r, c, 0u);
+                        y = remap_px_slot<P, SF8>(mb.slot, PL.pitch, F + mb.task * fstride, h, w, r, c, 0);
                     else if (mb.sfmt == SF16)
-                        y = remap_px_slot<P, SF16>(mb.slot, PL.pitch, F + mb.task * fstride, h, w, r, c,
-                                                   (uint32_t)(75 - PL.k) << 24);
+                        y = remap_px_slot<P, SF16>(mb.slot, PL.pitch, F + mb.task * fstride, h, w, r, c, PL.k);
                     else
                         y = remap_px<P>(mb.img, F + mb.task * fstride, h, w, r, c);
                 }
@@ -894,7 +915,7 @@ __global__ void __launch_bounds__(32 * I13_TY, 3) k_iter13_fast(FieldArgs a)
         select(f, e, clampi(f.x + ox, 0, h - 1), clampi(f.y + oy, 0, w - 1));
     }
     a.Fout[t * a.fstride + i] = f;
-    a.E[t * a.fstride + i] = e;
+    if (a.Eout) a.Eout[t * a.fstride + i] = e;  // never a.E: halo lanes of other tiles read it
 }
 
 // ---- level-0 variant for p = 3, 4: SF8 source, TF16 target tile in shared memory -----------------
@@ -1215,11 +1236,20 @@ cudaError_t launch_upsample(const int2* Fc, int2* Ff, int T, long long fstride, 
     default: return cudaErrorInvalidValue;          \
     }
 
-cudaError_t launch_aux_remap(const DTask* tasks, int T, const int2* F, long long fstride, Lvl L, PLvl PL, int p,
-                             int tfmt, cudaStream_t s)
+template <int P>
+static void launch_aux_remap_t(const DTask* tasks, int T, const int2* F, long long fstride, Lvl L, PLvl PL, int tfmt,
+                               int sfmt, long long src_off, cudaStream_t s)
 {
-    FB_DISPATCH_P(p, (k_aux_remap<PP><<<grid1d((long long)PL.rows * PL.pitch, T), 256, 0, s>>>(tasks, F, fstride, L,
-                                                                                               PL, tfmt)));
+    const dim3 g = grid1d((long long)PL.rows * PL.pitch, T);
+    if (sfmt == SF8) k_aux_remap<P, SF8><<<g, 256, 0, s>>>(tasks, F, fstride, L, PL, tfmt, src_off);
+    else if (sfmt == SF16) k_aux_remap<P, SF16><<<g, 256, 0, s>>>(tasks, F, fstride, L, PL, tfmt, src_off);
+    else k_aux_remap<P, -1><<<g, 256, 0, s>>>(tasks, F, fstride, L, PL, tfmt, src_off);
+}
+
+cudaError_t launch_aux_remap(const DTask* tasks, int T, const int2* F, long long fstride, Lvl L, PLvl PL, int p,
+                             int tfmt, int sfmt, long long src_off, cudaStream_t s)
+{
+    FB_DISPATCH_P(p, (launch_aux_remap_t<PP>(tasks, T, F, fstride, L, PL, tfmt, sfmt, src_off, s)));
     return cudaGetLastError();
 }
 

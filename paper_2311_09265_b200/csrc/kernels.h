@@ -94,6 +94,7 @@ struct FieldArgs {
     int step;              // propagation step (jump flood scale, D41; 1 = P:72)
     int einit;             // phase 0 recomputes E <- L(F) (first field of the iteration)
     int do_rs;             // phase 3 runs the random search (last field of the iteration)
+    float* Eout;           // fused fields 1-3: final E (nullable); E itself is read-only there
 };
 
 // Packing jobs: one per (slot, level) for sources, one per task/group for BASE targets.
@@ -114,8 +115,10 @@ cudaError_t launch_pack_tgt_guide(const DTask* tasks, int T, Lvl L, PLvl P, int 
 cudaError_t launch_init(const DTask* tasks, int T, int2* F, long long fstride, Lvl L, int identity, Rng rng,
                         uint32_t level, cudaStream_t s);
 cudaError_t launch_upsample(const int2* Fc, int2* Ff, int T, long long fstride, Lvl Lc, Lvl Lf, cudaStream_t s);
+// sfmt: SF8 / SF16 remaps the style held in the task's packed source slot (level block at src_off), any
+// other value the float4 style pyramid.
 cudaError_t launch_aux_remap(const DTask* tasks, int T, const int2* F, long long fstride, Lvl L, PLvl P, int p,
-                             int tfmt, cudaStream_t s);
+                             int tfmt, int sfmt, long long src_off, cudaStream_t s);
 cudaError_t launch_combine(const DOut* outs, int n_outs, const DMember* mem, const int2* F, long long fstride,
                            int h, int w, int p, int fmt, PLvl P, cudaStream_t s);
 // phase 0: E init + propagation (-1,0); 1: (+1,0); 2: (0,-1); 3: (0,+1) + all random-search steps.

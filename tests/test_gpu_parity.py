@@ -325,3 +325,23 @@ def test_tracking_interpolation_parity(fb, ctx, keys, align):
     ref, pairs, evals = O.interpolate(ocfg(cfg), g, keys, s[keys])
     assert st["nnf_pairs"] == pairs and st["candidate_evals"] == evals
     assert_frames(out, ref)
+
+
+# ------------------------------------------------------------------------------ schedule invariance / races
+@pytest.mark.parametrize("mode", ["accurate", "fast"])
+def test_fused_fields_equal_per_field_launches(fb, mode, monkeypatch):
+    """k_iter13_fast (fields 1-3 + random search in one launch, halo lanes) must equal the per-field launches
+    (P:76 Jacobi fields) bit for bit, on every repetition: its halo lanes read the field-0 E of pixels owned
+    by other tiles, so it must never write E in place (a timing-dependent race that this test repeats)."""
+    g, s = moving_texture(6, 192, 160, seed=77)
+    loss = fb.MEAN_ALIGN if mode == "accurate" else fb.GUIDE_STYLE
+    sched = fb.TREE if mode == "fast" else fb.DIRECT
+    cfg = fb.MatchCfg(iters_per_level=3, loss=loss)
+    monkeypatch.setenv("FB_FUSE13", "0")
+    ref, _ = fb.Context(0).fb_blend_window(cfg, sched, dev(g), dev(s), 3)
+    monkeypatch.setenv("FB_FUSE13", "1")
+    c = fb.Context(0)
+    for _ in range(4):
+        out, _ = c.fb_blend_window(cfg, sched, dev(g), dev(s), 3)
+        assert torch.equal(out, ref)
+
