@@ -156,14 +156,20 @@ fbk::PLvl padded(int h, int w, int k)
 }
 
 // Packed source format of level k for a slot whose level-0 format is fmt0 (kernels.h): u8 styles use
-// SF8 at level 0 and the exact 16-bit integer form SF16 at levels 1..4 (values n / 4^k, n < 2^16).
+// SF8 at level 0, the exact 10-bit form SF10 at level 1 (n = 4v < 2^10, 8 bytes per texel) and the exact
+// 16-bit integer form SF16 at levels 2..4 (values n / 4^k, n < 2^16).
+static bool sf10_enabled = true;  // A/B knob (FB_SF10=0: level 1 as SF16, identical results)
 int src_fmt(int fmt0, int k)
 {
     if (fmt0 == fbk::SF8F) return k == 0 ? fbk::SF8F : fbk::SF32;  // float styles: u8 guide + f32 style
     if (fmt0 != fbk::SF8) return fbk::SF32;
+    if (k == 1 && sf10_enabled) return fbk::SF10;
     return k == 0 ? fbk::SF8 : (k <= 4 ? fbk::SF16 : fbk::SF32);
 }
-size_t src_bytes(int fmt) { return fmt == fbk::SF8 ? 8 : (fmt == fbk::SF16 || fmt == fbk::SF8F) ? 16 : 32; }
+size_t src_bytes(int fmt)
+{
+    return (fmt == fbk::SF8 || fmt == fbk::SF10) ? 8 : (fmt == fbk::SF16 || fmt == fbk::SF8F) ? 16 : 32;
+}
 
 int level_count(int H, int W, int p, int requested)  // D6, D32
 {
@@ -279,7 +285,7 @@ Slots pack_sources(Exec& ex, const Geo& g, int fmt0, const std::vector<SlotSpec>
     for (int k = 0; k < g.Lv; ++k) {
         S.off[k] = off;
         const int f = src_fmt(fmt0, k);
-        const size_t copies = f == fbk::SF8 ? fbk::kSF8Copies : 1;
+        const size_t copies = (f == fbk::SF8 || f == fbk::SF10) ? fbk::kSF8Copies : 1;
         off = (off + copies * g.PL[k].rows * g.PL[k].pitch * src_bytes(f) + 255) & ~size_t(255);
     }
     S.stride = off;
@@ -974,6 +980,8 @@ fb_status fb_ctx_create(int device, void* cuda_stream, fb_ctx* out)
     if (fused && fused[0] == '1') c->fused = true;
     const char* f13 = getenv("FB_FUSE13");
     if (f13 && f13[0] == '0') c->fuse13 = false;
+    const char* sf10 = getenv("FB_SF10");
+    sf10_enabled = !(sf10 && sf10[0] == '0');
     c->device = device;
     c->stream = static_cast<cudaStream_t>(cuda_stream);
     *out = c;

@@ -46,6 +46,12 @@ __device__ __forceinline__ float u16f(uint32_t word, uint32_t sel, uint32_t ex)
 {
     return __fsub_rn(__uint_as_float(__byte_perm(word, ex, sel)), __uint_as_float(ex));
 }
+// SF10 channel (level 1: v = n / 4, n < 2^10 in 10-bit fields at bits 0, 10, 20) as the exact float n / 4:
+// a field placed in the mantissa of 2^e with unit 2^-2 (e = 21 for bits 0-9, e = 11 for bits 10-19), then
+// 2^e subtracted.
+__device__ __forceinline__ float f10_0(uint32_t w) { return __fsub_rn(__uint_as_float((w & 0x3FFu) | 0x4A000000u), 2097152.0f); }
+__device__ __forceinline__ float f10_1(uint32_t w) { return __fsub_rn(__uint_as_float((w & 0xFFC00u) | 0x45000000u), 2048.0f); }
+__device__ __forceinline__ float f10_2(uint32_t w) { return __fsub_rn(__uint_as_float((w >> 20) | 0x4A000000u), 2097152.0f); }
 __device__ __forceinline__ uint32_t pack_rgb(float r, float g, float b)  // exact for integer 0..255
 {
     return (uint32_t)r | ((uint32_t)g << 8) | ((uint32_t)b << 16);
@@ -86,7 +92,7 @@ __global__ void k_pack_src(const PackSrc* __restrict__ jobs, int fmt, PLvl L)
 {
     const PackSrc J = jobs[blockIdx.y];
     const int n = L.rows * L.pitch;
-    const int copies = fmt == SF8 ? kSF8Copies : 1;
+    const int copies = (fmt == SF8 || fmt == SF10) ? kSF8Copies : 1;
     for (int ii = blockIdx.x * blockDim.x + threadIdx.x; ii < n * copies; ii += gridDim.x * blockDim.x) {
         const int cpy = ii / n, i = ii - cpy * n;  // copy cpy holds texel (pr, pc + cpy) at (pr, pc)
         const int pr = i / L.pitch, pc = i - pr * L.pitch;
@@ -112,6 +118,16 @@ __global__ void k_pack_src(const PackSrc* __restrict__ jobs, int fmt, PLvl L)
                                __float_as_uint(sv.z));
             }
             reinterpret_cast<uint4*>(J.out)[i] = v;
+        } else if (fmt == SF10) {
+            // level 1 of a u8 pyramid: v = n / 4 with n <= 1020; 10-bit fields {r, g, b} of G and of S
+            uint2 v = make_uint2(0u, 0u);
+            if (in) {
+                const float4 g = J.gp[r * L.w + c];
+                const float4 sv = J.sp ? J.sp[r * L.w + c] : make_float4(0.f, 0.f, 0.f, 0.f);
+                v.x = (uint32_t)(g.x * 4.0f) | ((uint32_t)(g.y * 4.0f) << 10) | ((uint32_t)(g.z * 4.0f) << 20);
+                v.y = (uint32_t)(sv.x * 4.0f) | ((uint32_t)(sv.y * 4.0f) << 10) | ((uint32_t)(sv.z * 4.0f) << 20);
+            }
+            reinterpret_cast<uint2*>(J.out)[(size_t)cpy * n + i] = v;
         } else if (fmt == SF16) {
             // level k of a u8 pyramid: v = n / 4^k with n < 2^16 (k <= 4); store n
             const float sc = (float)(1 << (2 * L.k));
@@ -231,7 +247,8 @@ __device__ __forceinline__ float3 remap_px(const float4* __restrict__ S, const i
     return make_float3(__fdiv_rn(ax, fn), __fdiv_rn(ay, fn), __fdiv_rn(az, fn));
 }
 
-// Same remap reading the style channels from a packed source slot (SF8: u8 word, SF16: two u16 words),
+// Same remap reading the style channels from a packed source slot (SF8: u8 word, SF10: 10-bit fields,
+// SF16: two u16 words),
 // a quarter / half of the bytes per tap of the float4 pyramid.  Exact integer form: a slot holds every
 // style value as n * 4^-k with integer n (k = 0: u8; k = 1..4: SF16, D6), and a sum of at most (2P+1)^2
 // such values has sum(n) < 2^24, so the FP32 chain of D19 is exact, order-free and equal to
@@ -261,6 +278,12 @@ __device__ __forceinline__ float3 remap_px_slot(const char* __restrict__ slot, i
                 sv = v ? sv : 0u;
                 a0 += __byte_perm(sv, 0u, 0x4240u);  // r | b << 16
                 a1 += __byte_perm(sv, 0u, 0x4441u);  // g
+            } else if (SFMT == SF10) {
+                uint32_t sv = __ldg(reinterpret_cast<const uint32_t*>(slot) + 2 * idx + 1);
+                sv = v ? sv : 0u;
+                a0 += sv & 0x3FFu;
+                a1 += (sv >> 10) & 0x3FFu;
+                a2 += sv >> 20;
             } else {
                 uint2 sv = __ldg(reinterpret_cast<const uint2*>(slot) + 2 * idx + 1);
                 if (!v) sv = make_uint2(0u, 0u);
@@ -301,7 +324,8 @@ __global__ void k_aux_remap(const DTask* __restrict__ tasks, const int2* __restr
         float3 v = make_float3(0.f, 0.f, 0.f);
         float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
         if (in) {
-            if (SFMT == SF8 || SFMT == SF16) v = remap_px_slot<P, SFMT>(slot, PL.pitch, Ft, L.h, L.w, r, c, PL.k);
+            if (SFMT == SF8 || SFMT == SF10 || SFMT == SF16)
+                v = remap_px_slot<P, SFMT>(slot, PL.pitch, Ft, L.h, L.w, r, c, PL.k);
             else v = remap_px<P>(S, Ft, L.h, L.w, r, c);
             g = __ldg(&T.tg[L.off + r * L.w + c]);
         }
@@ -338,6 +362,8 @@ __global__ void __launch_bounds__(256, COMBINE_MINB) k_combine(const DOut* __res
                 } else {
                     if (mb.sfmt == SF8)
                         y = remap_px_slot<P, SF8>(mb.slot, PL.pitch, F + mb.task * fstride, h, w, r, c, 0);
+                    else if (mb.sfmt == SF10)
+                        y = remap_px_slot<P, SF10>(mb.slot, PL.pitch, F + mb.task * fstride, h, w, r, c, PL.k);
                     else if (mb.sfmt == SF16)
                         y = remap_px_slot<P, SF16>(mb.slot, PL.pitch, F + mb.task * fstride, h, w, r, c, PL.k);
                     else
@@ -1069,7 +1095,12 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
 #pragma unroll
             for (int dc = 0; dc < D; ++dc) {
                 const int idx = (q.x + dr - P + B) * pitch + (q.y + dc - P + B);
-                if (SFMT == SF16) {
+                if (SFMT == SF10) {
+                    const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(T.psrc + a.src_off) + 2 * idx + 1);
+                    pa[PW ? dr : 0][PW ? dc : 0][0] = f10_0(v);
+                    pa[PW ? dr : 0][PW ? dc : 0][1] = f10_1(v);
+                    pa[PW ? dr : 0][PW ? dc : 0][2] = f10_2(v);
+                } else if (SFMT == SF16) {
                     const uint4 v = __ldg(reinterpret_cast<const uint4*>(T.psrc + a.src_off) + idx);
                     pa[PW ? dr : 0][PW ? dc : 0][0] = u16f(v.z, 0x7410u, ex);
                     pa[PW ? dr : 0][PW ? dc : 0][1] = u16f(v.z, 0x7432u, ex);
@@ -1086,10 +1117,27 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
     auto row = [&](int sr, int sc, int dr, float& dg, float& ds) {
         const int base = (sr + dr - P + B) * pitch + (sc - P + B);
         float rg = 0.0f, rs = 0.0f;
+        // SF10: the row's texel pairs from the copy in which it starts 16-byte aligned (as SF8)
+        constexpr int NCH = (D + 2) / 2;
+        uint32_t wd[SFMT == SF10 ? 4 * NCH : 1];
+        if (SFMT == SF10) {
+            const uint4* cp = reinterpret_cast<const uint4*>(
+                reinterpret_cast<const uint2*>(T.src + a.src_off) + (size_t)(base & 1) * (a.L.rows * pitch) + (base & ~1));
+#pragma unroll
+            for (int k = 0; k < NCH; ++k) {
+                const uint4 v = __ldg(cp + k);
+                wd[SFMT == SF10 ? 4 * k : 0] = v.x; wd[SFMT == SF10 ? 4 * k + 1 : 0] = v.y;
+                wd[SFMT == SF10 ? 4 * k + 2 : 0] = v.z; wd[SFMT == SF10 ? 4 * k + 3 : 0] = v.w;
+            }
+        }
 #pragma unroll
         for (int dc = 0; dc < D; ++dc) {
             float4 s0, s1;
-            if (SFMT == SF16) {
+            if (SFMT == SF10) {
+                const uint32_t gw = wd[SFMT == SF10 ? 2 * dc : 0], sw = wd[SFMT == SF10 ? 2 * dc + 1 : 0];
+                s0 = make_float4(f10_0(gw), f10_1(gw), f10_2(gw), TWO ? f10_0(sw) : 0.0f);
+                s1 = TWO ? make_float4(f10_1(sw), f10_2(sw), 0.0f, 0.0f) : s0;
+            } else if (SFMT == SF16) {
                 const uint4 v = __ldg(&S16[base + dc]);
                 s0 = make_float4(u16f(v.x, 0x7410u, ex), u16f(v.x, 0x7432u, ex), u16f(v.y, 0x7410u, ex),
                                  TWO ? u16f(v.z, 0x7410u, ex) : 0.0f);
@@ -1242,6 +1290,7 @@ static void launch_aux_remap_t(const DTask* tasks, int T, const int2* F, long lo
 {
     const dim3 g = grid1d((long long)PL.rows * PL.pitch, T);
     if (sfmt == SF8) k_aux_remap<P, SF8><<<g, 256, 0, s>>>(tasks, F, fstride, L, PL, tfmt, src_off);
+    else if (sfmt == SF10) k_aux_remap<P, SF10><<<g, 256, 0, s>>>(tasks, F, fstride, L, PL, tfmt, src_off);
     else if (sfmt == SF16) k_aux_remap<P, SF16><<<g, 256, 0, s>>>(tasks, F, fstride, L, PL, tfmt, src_off);
     else k_aux_remap<P, -1><<<g, 256, 0, s>>>(tasks, F, fstride, L, PL, tfmt, src_off);
 }
@@ -1386,6 +1435,16 @@ cudaError_t launch_field(const FieldArgs& a0, int T, int p, int loss, int phase,
             else launch_field_fast<2, false>(a, T, phase, s);
         } else {
             return cudaErrorInvalidValue;
+        }
+    } else if (a.src_fmt == SF10) {
+        if (pw) {
+            if (p == 1) launch_field_gen<1, true, SF10, true>(a, T, phase, s);
+            else if (p == 2) launch_field_gen<2, true, SF10, true>(a, T, phase, s);
+            else return cudaErrorInvalidValue;
+        } else if (loss) {
+            FB_DISPATCH_P(p, (launch_field_gen<PP, true, SF10>(a, T, phase, s)));
+        } else {
+            FB_DISPATCH_P(p, (launch_field_gen<PP, false, SF10>(a, T, phase, s)));
         }
     } else if (a.src_fmt == SF16) {
         if (pw) {

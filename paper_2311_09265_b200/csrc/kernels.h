@@ -9,7 +9,9 @@
 //  * packed PatchMatch operands with a zero border of kBorder texels on every side (so patch taps never
 //    need bounds checks: out-of-image taps read the border's zeros, reading D9) and an even pitch:
 //      source  SF8  (level 0, uint8 style): uint2 {G rgb u8, S rgb u8}                        8 B
-//              SF16 (levels 1..4, uint8 style): uint4 of u16 n = v * 4^k {G.r,G.g | G.b,0 |
+//              SF10 (level 1, uint8 style): uint2 {G, S} of 10-bit fields n = 4 v (r | g << 10 | b << 20),
+//                   exact because level-1 values are multiples of 1/4 (D6); two copies like SF8        8 B
+//              SF16 (levels 2..4, uint8 style): uint4 of u16 n = v * 4^k {G.r,G.g | G.b,0 |
 //                   S.r,S.g | S.b,0}; exact because level-k values are multiples of 4^-k (D6) 16 B
 //              SF8F (level 0, float style, e.g. blending-table cells): uint4 {G rgb u8, S.r, S.g, S.b
 //                   as f32}; the guide is still u8-exact at level 0                              16 B
@@ -28,7 +30,7 @@ constexpr int kBorder = 4;  // >= the largest compiled patch radius
 #endif                       // starts 16-byte aligned in copy (col & 1), so no parity selects are needed
 constexpr int kSF8Copies = FB_SF8_COPIES;
 
-enum SrcFmt { SF8 = 0, SF32 = 1, SF16 = 2, SF8F = 3 };
+enum SrcFmt { SF8 = 0, SF32 = 1, SF16 = 2, SF8F = 3, SF10 = 4 };
 enum TgtFmt { TF16 = 0, TF32 = 1 };
 
 // One NNF task (pair).
