@@ -31,6 +31,8 @@ struct fb_ctx_s {
     uint64_t launches = 0;
     bool fused = false;  // fused iteration kernel on the fast path (FB_FUSED=1; measured slower)
     bool fuse13 = true;  // fields 1-3 + random search fused on the fast path (FB_FUSE13=0 disables)
+    int tgt_reg_rows = 2;  // fused fields 1-3: target rows in registers, rest in shared memory (FB_HYROWS;
+                           // 0 = all in registers; accurate N=48: field123.L0 413 -> 397 ms)
     std::string err;
     // kernel timing (fb_profile_*)
     bool prof = false;
@@ -448,6 +450,7 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
             a.tasks = d_tasks; a.E = out.E; a.fstride = n0; a.L = PL; a.src_off = (long long)slots.off[k];
             a.alpha = cfg.alpha; a.rng = rng; a.level = (uint32_t)k; a.iter = (uint32_t)it; a.rs_r0 = r0; a.rs_k = rk;
             a.src_fmt = src_fmt(slots.fmt0, k);
+            a.tgt_reg_rows = ex.ctx->tgt_reg_rows;
             char names[4][32];
             for (int ph = 0; ph < 4; ++ph) snprintf(names[ph], sizeof names[ph], "field%d.L%d", ph, k);
             const int J = std::max(1, cfg.prop_scales);  // jump-flood scales (D41)
@@ -980,6 +983,8 @@ fb_status fb_ctx_create(int device, void* cuda_stream, fb_ctx* out)
     if (fused && fused[0] == '1') c->fused = true;
     const char* f13 = getenv("FB_FUSE13");
     if (f13 && f13[0] == '0') c->fuse13 = false;
+    const char* hy = getenv("FB_HYROWS");
+    if (hy) c->tgt_reg_rows = atoi(hy);
     const char* sf10 = getenv("FB_SF10");
     sf10_enabled = !(sf10 && sf10[0] == '0');
     c->device = device;

@@ -793,10 +793,15 @@ __global__ void __launch_bounds__(32 * (IT_TY + 1), IT_MINB) k_iter_fast(FieldAr
 // pixels see exactly the Jacobi inputs of the per-field launches.  No shared memory, no barrier.
 static constexpr int I13_TY = 4;
 
-template <int P, bool TWO, bool PW = false, int SFL = 0>
-__global__ void __launch_bounds__(32 * I13_TY, 3) k_iter13_fast(FieldArgs a)
+// NR < D (hybrid target): only the first NR rows of each lane's target patch live in registers -- row 0 is
+// read by every candidate, rows >= 1 only by candidates that survive row 0 -- and the rest is read from a
+// shared-memory copy of the CTA's target tile.  Registers drop from 168 to <= 128: 4 CTAs/SM instead of 3.
+template <int P, bool TWO, bool PW = false, int SFL = 0, int NR = 2 * P + 1>
+__global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? 4 : 3) k_iter13_fast(FieldArgs a)
 {
     constexpr int D = 2 * P + 1;
+    constexpr bool HY = NR < D;
+    static_assert(!(HY && PW), "the pairwise reference patch is per pixel: registers only");
     constexpr int NCH = (D + 2) / 2;
     const int t = blockIdx.x / a.tiles_per_task;
     const int tile = blockIdx.x - t * a.tiles_per_task;
@@ -808,21 +813,43 @@ __global__ void __launch_bounds__(32 * I13_TY, 3) k_iter13_fast(FieldArgs a)
     const DTask T = a.tasks[t];
     const uint2* S = reinterpret_cast<const uint2*>(T.src + a.src_off);
     const uint4* Tt = reinterpret_cast<const uint4*>(T.tgt);
-    uint32_t tgG[D][D];
-    float tgA[D][D][3];
+    constexpr int NRR = HY ? NR : D;
+    uint32_t tgG[NRR][D];
+    float tgA[NRR][D][3];
+    constexpr int TTY = HY ? I13_TY + 2 * P : 1, TTX = HY ? 32 + 2 * P : 1;
+    __shared__ uint4 tT[TTY][TTX];
+    if (HY) {  // the CTA's target tile (rows r0-P.., cols c0-P..), zero outside the padded plane
+        const int pr0 = ty * I13_TY - P + B, pc0 = tx * IT_TX - 1 - P + B;
+        for (int k = threadIdx.x; k < TTY * TTX; k += 32 * I13_TY) {
+            const int yy = k / TTX, xx = k - yy * TTX;
+            const int pr = pr0 + yy, pc = pc0 + xx;
+            tT[yy][xx] = (pr < a.L.rows && pc < pitch) ? __ldg(&Tt[pr * pitch + pc]) : make_uint4(0u, 0u, 0u, 0u);
+        }
+        __syncthreads();
+    }
     if (valid) {
 #pragma unroll
-        for (int dr = 0; dr < D; ++dr)
+        for (int dr = 0; dr < NRR; ++dr)
 #pragma unroll
             for (int dc = 0; dc < D; ++dc) {
-                const uint4 v = __ldg(&Tt[(r + dr - P + B) * pitch + (c + dc - P + B)]);
+                const uint4 v = HY ? tT[wy + dr][lane + dc] : __ldg(&Tt[(r + dr - P + B) * pitch + (c + dc - P + B)]);
                 tgG[dr][dc] = v.x;
                 tgA[dr][dc][0] = __uint_as_float(v.y);
                 tgA[dr][dc][1] = __uint_as_float(v.z);
                 tgA[dr][dc][2] = __uint_as_float(v.w);
             }
-        if (PW) load_pairwise_patch<P>(T, a, r * w + c, tgA);
+        if constexpr (PW && !HY) load_pairwise_patch<P>(T, a, r * w + c, tgA);
     }
+    // target texel (dr, j) of this lane's patch: registers for dr < NRR, else the shared tile
+    auto tgt = [&](int dr, int j, uint32_t& g, float& a0, float& a1, float& a2) {
+        if (dr < NRR) {
+            const int d = dr < NRR ? dr : 0;
+            g = tgG[d][j]; a0 = tgA[d][j][0]; a1 = tgA[d][j][1]; a2 = tgA[d][j][2];
+        } else {
+            const uint4 v = tT[HY ? wy + dr : 0][HY ? lane + j : 0];
+            g = v.x; a0 = __uint_as_float(v.y); a1 = __uint_as_float(v.z); a2 = __uint_as_float(v.w);
+        }
+    };
     // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
     auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
         const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
@@ -832,12 +859,14 @@ __global__ void __launch_bounds__(32 * I13_TY, 3) k_iter13_fast(FieldArgs a)
 #pragma unroll
             for (int j = 0; j < D; ++j) {
                 const uint4 v = __ldg(tp + j);
-                const uint32_t d = __vabsdiffu4(v.x, tgG[dr][j]);
+                uint32_t tg; float t0, t1, t2;
+                tgt(dr, j, tg, t0, t1, t2);
+                const uint32_t d = __vabsdiffu4(v.x, tg);
                 dg = __dp4a(d, d, dg);
                 if (TWO) {
-                    float dl = __fsub_rn(tgA[dr][j][0], __uint_as_float(v.y)); rs = __fmaf_rn(dl, dl, rs);
-                    dl = __fsub_rn(tgA[dr][j][1], __uint_as_float(v.z)); rs = __fmaf_rn(dl, dl, rs);
-                    dl = __fsub_rn(tgA[dr][j][2], __uint_as_float(v.w)); rs = __fmaf_rn(dl, dl, rs);
+                    float dl = __fsub_rn(t0, __uint_as_float(v.y)); rs = __fmaf_rn(dl, dl, rs);
+                    dl = __fsub_rn(t1, __uint_as_float(v.z)); rs = __fmaf_rn(dl, dl, rs);
+                    dl = __fsub_rn(t2, __uint_as_float(v.w)); rs = __fmaf_rn(dl, dl, rs);
                 }
             }
             if (TWO) ds = __fadd_rn(ds, rs);
@@ -856,13 +885,15 @@ __global__ void __launch_bounds__(32 * I13_TY, 3) k_iter13_fast(FieldArgs a)
 #pragma unroll
         for (int j = 0; j < D; ++j) {
             const uint32_t g = o ? wd[2 * j + 2] : wd[2 * j];
-            const uint32_t d = __vabsdiffu4(g, tgG[dr][j]);
+            uint32_t tg; float ta[3];
+            tgt(dr, j, tg, ta[0], ta[1], ta[2]);
+            const uint32_t d = __vabsdiffu4(g, tg);
             dg = __dp4a(d, d, dg);
             if (TWO) {
                 const uint32_t sv = o ? wd[2 * j + 3] : wd[2 * j + 1];
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
-                    const float dl = __fsub_rn(tgA[dr][j][ch], u8f(sv, ch));
+                    const float dl = __fsub_rn(ta[ch], u8f(sv, ch));
                     rs = __fmaf_rn(dl, dl, rs);
                 }
             }
@@ -1372,11 +1403,21 @@ cudaError_t launch_iter13_fast(const FieldArgs& a0, int T, int p, int loss, cuda
     a.tiles_x = (a.L.w + IT_TX - 1) / IT_TX;
     a.tiles_per_task = a.tiles_x * ((a.L.h + I13_TY - 1) / I13_TY);
     const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(32 * I13_TY);
+    const int hy = a.tgt_reg_rows;  // hybrid target (rows in registers; 0 = all)
     if (a.src_fmt == SF8F) {
         if (loss != 1 && loss != 2) return cudaErrorInvalidValue;
         if (p == 1) k_iter13_fast<1, true, false, 1><<<grid, block, 0, s>>>(a);
+        else if (p == 2 && hy == 1) k_iter13_fast<2, true, false, 1, 1><<<grid, block, 0, s>>>(a);
+        else if (p == 2 && hy == 2) k_iter13_fast<2, true, false, 1, 2><<<grid, block, 0, s>>>(a);
         else if (p == 2) k_iter13_fast<2, true, false, 1><<<grid, block, 0, s>>>(a);
         else return cudaErrorInvalidValue;
+        return cudaGetLastError();
+    }
+    if (p == 2 && loss != 3 && (hy == 1 || hy == 2)) {
+        if (loss && hy == 1) k_iter13_fast<2, true, false, 0, 1><<<grid, block, 0, s>>>(a);
+        else if (loss) k_iter13_fast<2, true, false, 0, 2><<<grid, block, 0, s>>>(a);
+        else if (hy == 1) k_iter13_fast<2, false, false, 0, 1><<<grid, block, 0, s>>>(a);
+        else k_iter13_fast<2, false, false, 0, 2><<<grid, block, 0, s>>>(a);
         return cudaGetLastError();
     }
     if (p == 1) {

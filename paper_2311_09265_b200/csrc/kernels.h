@@ -97,6 +97,7 @@ struct FieldArgs {
     int einit;             // phase 0 recomputes E <- L(F) (first field of the iteration)
     int do_rs;             // phase 3 runs the random search (last field of the iteration)
     float* Eout;           // fused fields 1-3: final E (nullable); E itself is read-only there
+    int tgt_reg_rows;      // fused fields 1-3 (p = 2): target patch rows held in registers (0 = all)
 };
 
 // Packing jobs: one per (slot, level) for sources, one per task/group for BASE targets.

@@ -1,6 +1,6 @@
 """A/B of an engine knob read at context creation (e.g. FB_LOCKSTEP): same inputs, both settings, outputs
 compared bit for bit, step times printed.  Development aid, not the bench.
-usage: python tools/ab_env.py VAR N mode [reps]"""
+usage: python tools/ab_env.py VAR N mode [reps] [v1,v2,...]   (values default 0,1)"""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -9,13 +9,14 @@ from synth import moving_texture
 
 var, N, mode = sys.argv[1], int(sys.argv[2]), sys.argv[3]
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 2
+values = sys.argv[5].split(",") if len(sys.argv) > 5 else ["0", "1"]
 g, s = moving_texture(N, 512, 512)
 gd, sd = torch.from_numpy(g).cuda(), torch.from_numpy(s).cuda()
 cfg = P.MatchCfg(loss=P.MEAN_ALIGN if mode == "accurate" else P.GUIDE_STYLE)
 sched = P.TREE if mode == "fast" else P.DIRECT
 M = 30 if mode == "fast" else 15
 outs = {}
-for val in ("0", "1"):
+for val in values:
     os.environ[var] = val
     ctx = P.Context(0)
     best = 1e9
@@ -31,5 +32,7 @@ for val in ("0", "1"):
     print("   ", ", ".join(f"{k} {v['ms']:.1f}" for k, v in top), flush=True)
     print(f"{var}={val}: {mode} N={N} best {best*1e3:.1f} ms, {st['candidate_evals']/best/1e9:.2f} G evals/s", flush=True)
     del ctx
-same = torch.equal(outs["0"], outs["1"])
-print("bit-identical outputs:", same, "max diff", float((outs["0"] - outs["1"]).abs().max()))
+ref = outs[values[0]]
+for val in values[1:]:
+    print(f"{var}={val} bit-identical to {var}={values[0]}:", torch.equal(outs[val], ref),
+          "max diff", float((outs[val] - ref).abs().max()))
