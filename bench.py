@@ -229,6 +229,10 @@ def main():
     def step(g_in, s_in):
         if world > 1:
             (g_loc, s_loc), f0 = shard.halo_exchange([g_in, s_in], plan, N, M, rank)
+            if sched == P.TREE:  # fast mode: owned blending-table cells built once, exchanged
+                _, st = shard.blend_tree_exchange(ctx, cfg, plan, N, M, rank, g_loc, s_loc, f0, out=out)
+                stats.update(st)
+                return
         else:
             g_loc, s_loc, f0 = g_in, s_in, 0
         _, st = ctx.fb_blend_window_range(cfg, sched, N, f0, g_loc, s_loc, M, t0, t1, out=out)

@@ -167,6 +167,32 @@ fb_status fb_blend_window_range(fb_ctx ctx, const fb_match_cfg* cfg, int schedul
                                 int H, int W, int M, const uint8_t* guide, const uint8_t* style, int t0, int t1,
                                 float* out, fb_stats* stats);
 
+/* ---- sharded tree schedule with blending-table cell exchange (Alg. 3-5) -------
+ * A shard's Alg. 5 queries visit cells BT(node, L) of nodes up to M frames outside its targets; instead of
+ * rebuilding those (fb_blend_window_range does), shards build the cells they own and exchange them.
+ * A cell is three int32 {orient, j, L}: orient 0 = forward, 1 = reversed frame order (D26); j is the node
+ * index in that order (frame j forward, frame N_total-1-j reversed); L >= 1 its table level.  Its value is
+ * the mean BT(j, L) of the 2^L frames [j-2^L+1, j] (orientation order) remapped into frame j (D25), stored
+ * as a float4 pyramid of fb_pyramid_elems(1, H, W, levels)/4 texels (the fb_build_pyramid layout, RGB + 0),
+ * `levels` = the configuration's pyramid depth.  Results are identical to fb_blend_window_range whoever
+ * builds a cell (pair-keyed RNG, D21).
+ *
+ * fb_tree_build_cells: builds the n_cells listed cells (HOST int32 [n_cells][3]) into cell_out (device,
+ *   n_cells pyramids back to back).  Every frame a cell reads must lie in the local frames [f0, f0+N).
+ * fb_tree_query: targets [t0, t1) from the local frames (which must cover [t0-M, t1+M) clipped) and the
+ *   given cells (cell_ptrs: HOST array of n_cells device pointers, one pyramid each); every cell the queries
+ *   visit must be listed (FB_ERR_INVALID_ARG otherwise).  out as in fb_blend_window_range.
+ * fb_tree_cell_texels: float4 texels of one cell pyramid for (cfg, H, W).
+ * ws_needed (nullable): when non-NULL, nothing runs; the workspace bytes the call needs are stored there. */
+size_t fb_tree_cell_texels(const fb_match_cfg* cfg, int H, int W);
+fb_status fb_tree_build_cells(fb_ctx ctx, const fb_match_cfg* cfg, int N_total, int f0, int N, int H, int W,
+                              const uint8_t* guide, const uint8_t* style, int n_cells, const int32_t* cells,
+                              float* cell_out, fb_stats* stats, size_t* ws_needed);
+fb_status fb_tree_query(fb_ctx ctx, const fb_match_cfg* cfg, int N_total, int f0, int N, int H, int W, int M,
+                        const uint8_t* guide, const uint8_t* style, int t0, int t1, int n_cells,
+                        const int32_t* cells, const float* const* cell_ptrs, float* out, fb_stats* stats,
+                        size_t* ws_needed);
+
 /* ---- keyframe interpolation (Eq. 9; D28) ----------------------------------------------
  * guide uint8 [N,H,W,3]; key_index HOST int32 [K], strictly increasing in [0,N); key_style uint8
  * [K,H,W,3]; out float [N,H,W,3].  Keys are copied verbatim; a frame m between consecutive keys

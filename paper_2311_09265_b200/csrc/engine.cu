@@ -644,6 +644,163 @@ std::vector<std::pair<int, int>> query_nodes(int l, int r)  // Alg. 5 with i <- 
     return v;
 }
 
+// Blending-table cells BT(j, L) (L >= 1) of one orientation, as float4 pyramids (g.pyr_texels each).
+using CellMap = std::map<std::pair<int, int>, const float4*>;
+
+// Alg. 3 + Alg. 4 for the cells (j, 1..top[j]) of orientation o (j in orientation order): RT sums of the
+// remaps X_{v->j}, v in [j-2^L+1, j-2^(L-1)] ascending, then BT(j,L) = (BT(j,L-1) + RT(j,L)*2^-(L-1))*0.5
+// level by level, then the BT pyramids.  The BT block stays in the arena (caller's mark).
+CellMap tree_build(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int N_total, int f0, const Pyr& G, const Pyr& S,
+                   const Slots& FR, int o, const std::vector<int>& top, fb_stats* st)
+{
+    const long long n0 = g.npx0();
+    auto orig = [&](int v) { return o == 0 ? v : N_total - 1 - v; };
+    const uint32_t tag_build = o == 0 ? 1u : 3u;
+    std::map<std::pair<int, int>, int> cell_id;  // (j, L) -> index
+    std::vector<std::pair<int, int>> cells;
+    int lmax = 0;
+    for (int j = 0; j < (int)top.size(); ++j)
+        for (int L = 1; L <= top[j]; ++L) { cell_id[{j, L}] = (int)cells.size(); cells.push_back({j, L}); lmax = std::max(lmax, L); }
+    const int nc = (int)cells.size();
+    float4* BT = ex.ar.take<float4>((size_t)nc * g.pyr_texels);  // BT cell pyramids (survive this call)
+    const size_t mark0 = ex.ar.off;
+    float4* RT = ex.ar.take<float4>((size_t)nc * n0);            // RT sums, level 0
+    auto bt_pyr = [&](int v, int L) -> const float4* {
+        return L == 0 ? S.frame(orig(v) - f0) : BT + (long long)cell_id.at({v, L}) * g.pyr_texels;
+    };
+    std::vector<int> cost(nc);
+    for (int c = 0; c < nc; ++c) cost[c] = 1 << (cells[c].second - 1);
+    const int cap = batch_pairs(ex.ctx, g, cfg.loss);
+    const size_t mark = ex.ar.off;
+    for (auto [c0, c1] : make_batches(cost, cap)) {
+        ex.ar.off = mark;
+        std::vector<TaskSpec> tasks;
+        for (int c = c0; c < c1; ++c) {
+            const auto [j, L] = cells[c];
+            for (int v = j - (1 << L) + 1; v <= j - (1 << (L - 1)); ++v)
+                tasks.push_back(TaskSpec{FR.slot(orig(v) - f0), S.frame(orig(v) - f0), G.frame(orig(j) - f0), -1,
+                                         (uint32_t)orig(v), (uint32_t)orig(j), tag_build});
+        }
+        BatchOut bo = run_nnf(ex, cfg, g, FR, tasks, {}, st);
+        CombineList cl;
+        int t = 0;
+        for (int c = c0; c < c1; ++c) {
+            const auto [j, L] = cells[c];
+            cl.begin();
+            for (int v = j - (1 << L) + 1; v <= j - (1 << (L - 1)); ++v) cl.add_remap(S.frame(orig(v) - f0), t++, 1.0f);
+            cl.end(RT + (long long)c * n0, 0, 1.0f);
+        }
+        if (st) st->remap_pixels += (uint64_t)tasks.size() * n0;
+        run_combine(ex, g, 0, cl, bo.F, bo.fstride);
+    }
+    ex.ar.off = mark;
+    for (int L = 1; L <= lmax; ++L) {
+        CombineList cl;
+        for (int c = 0; c < nc; ++c) {
+            if (cells[c].second != L) continue;
+            const int j = cells[c].first;
+            cl.begin();
+            cl.add_img(bt_pyr(j, L - 1), 1.0f);
+            cl.add_img(RT + (long long)c * n0, 1.0f / (float)(1 << (L - 1)));
+            cl.end(BT + (long long)c * g.pyr_texels, 0, 2.0f);
+        }
+        run_combine(ex, g, 0, cl, nullptr, 0);
+    }
+    if (nc) pyramid_levels_inplace(ex, g, BT, nc, g.pyr_texels);
+    ex.ar.off = mark0;  // RT is dead; BT stays
+    CellMap m;
+    for (int c = 0; c < nc; ++c) m[cells[c]] = BT + (long long)c * g.pyr_texels;
+    return m;
+}
+
+// Alg. 5 queries of targets [t0, t1) in orientation o into A (one float4 image per target):
+// A = sum over the visited nodes of 2^L * (BT(node, L) -> S_r); the self node is BT itself; L = 0 nodes are
+// frames.  Every visited (node, L >= 1) must be in `cells`.
+void tree_query(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int N_total, int f0, int M, const Pyr& G,
+                const Pyr& S, int o, int t0, int t1, const CellMap& cells, float4* A, fb_stats* st)
+{
+    const long long n0 = g.npx0();
+    auto orig = [&](int v) { return o == 0 ? v : N_total - 1 - v; };
+    const uint32_t tag_query = o == 0 ? 2u : 4u;
+    auto bt_pyr = [&](int v, int L) -> const float4* {
+        if (L == 0) return S.frame(orig(v) - f0);
+        auto it = cells.find({v, L});
+        if (it == cells.end()) throw Fail{FB_ERR_INVALID_ARG, "a query visits a blending-table cell that was not provided"};
+        return it->second;
+    };
+    std::vector<int> qcost;
+    std::vector<std::vector<std::pair<int, int>>> walks;
+    for (int i = t0; i < t1; ++i) {
+        const int v = o == 0 ? i : N_total - 1 - i;
+        walks.push_back(query_nodes(std::max(0, v - M), v));
+        qcost.push_back((int)walks.back().size() - 1);
+    }
+    const int cap = batch_pairs(ex.ctx, g, cfg.loss);
+    const size_t mark2 = ex.ar.off;
+    for (auto [q0, q1] : make_batches(qcost, cap)) {
+        ex.ar.off = mark2;
+        std::vector<TaskSpec> tasks;
+        std::vector<SlotSpec> qspecs;  // query sources: (G_i, BT(i,L)) packed as SF8F (float style)
+        for (int q = q0; q < q1; ++q) {
+            const int i = t0 + q, v = o == 0 ? i : N_total - 1 - i;
+            for (auto [node, L] : walks[q]) {
+                if (node == v) continue;
+                qspecs.push_back(SlotSpec{nullptr, nullptr, G.frame(orig(node) - f0), bt_pyr(node, L)});
+                tasks.push_back(TaskSpec{nullptr, bt_pyr(node, L), G.frame(i - f0), -1, (uint32_t)orig(node),
+                                         (uint32_t)i, tag_query});
+            }
+        }
+        const Slots QS = pack_sources(ex, g, fbk::SF8F, qspecs);
+        for (size_t t = 0; t < tasks.size(); ++t) tasks[t].src = QS.slot((long long)t);
+        BatchOut bo;
+        if (!tasks.empty()) bo = run_nnf(ex, cfg, g, QS, tasks, {}, st);
+        CombineList cl;
+        int t = 0;
+        for (int q = q0; q < q1; ++q) {
+            const int v = o == 0 ? t0 + q : N_total - 1 - (t0 + q);
+            cl.begin();
+            for (auto [node, L] : walks[q]) {
+                const float wgt = (float)(1 << L);
+                if (node == v) cl.add_img(bt_pyr(node, L), wgt);
+                else cl.add_remap(bt_pyr(node, L), t++, wgt);
+            }
+            cl.end(A + (long long)q * n0, 0, 1.0f);
+        }
+        if (st) st->remap_pixels += (uint64_t)tasks.size() * n0;
+        run_combine(ex, g, 0, cl, bo.F, bo.fstride);
+    }
+    ex.ar.off = mark2;
+}
+
+// Levels of the cells the queries of targets [t0, t1) visit, per node of orientation o.
+std::vector<int> tree_top(int N_total, int M, int o, int t0, int t1)
+{
+    std::vector<int> top(N_total, 0);
+    for (int i = t0; i < t1; ++i) {
+        const int v = o == 0 ? i : N_total - 1 - i;
+        for (auto [node, L] : query_nodes(std::max(0, v - M), v)) top[node] = std::max(top[node], L);
+    }
+    return top;
+}
+
+// Eq. 6: out_i = ((A_f + A_r) - S_i) / |W_i|
+void tree_merge(Exec& ex, const Geo& g, int N_total, int f0, int M, const Pyr& S, int t0, int t1, float4* const A[2],
+                float* out)
+{
+    const long long n0 = g.npx0();
+    CombineList cl;
+    for (int q = 0; q < t1 - t0; ++q) {
+        const int i = t0 + q, lo = std::max(0, i - M), hi = std::min(N_total - 1, i + M);
+        cl.begin();
+        cl.add_img(A[0] + (long long)q * n0, 1.0f);
+        cl.add_img(A[1] + (long long)q * n0, 1.0f);
+        cl.add_img(S.frame(i - f0), -1.0f);
+        cl.end(out + 3LL * n0 * q, 1, (float)(hi - lo + 1));
+    }
+    run_combine(ex, g, 0, cl, nullptr, 0);
+}
+
+// Whole tree schedule for targets [t0, t1), building every cell its queries visit locally.
 void blend_tree(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N_total, int f0, int N, int M,
                 const uint8_t* guide, const uint8_t* style, int t0, int t1, float* out, fb_stats* st)
 {
@@ -655,124 +812,67 @@ void blend_tree(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N_total, i
     std::vector<SlotSpec> specs;
     for (int j = 0; j < N; ++j) specs.push_back(SlotSpec{guide + 3 * n0 * j, style + 3 * n0 * j, G.frame(j), S.frame(j)});
     const Slots FR = pack_sources(ex, g, fbk::SF8, specs);
-    const int lcap = floor_log2(M + 1);
-    const int cap = batch_pairs(ex.ctx, g, cfg.loss);
     const int nt = t1 - t0;
     float4* A[2] = {ex.ar.take<float4>((size_t)nt * n0), ex.ar.take<float4>((size_t)nt * n0)};
     for (int o = 0; o < 2; ++o) {
         const size_t omark = ex.ar.off;  // this orientation's tables die once its A is written
-        auto orig = [&](int v) { return o == 0 ? v : N_total - 1 - v; };
-        const uint32_t tag_build = o == 0 ? 1u : 3u, tag_query = o == 0 ? 2u : 4u;
-        // cells needed by the queries: (j, L) for 1 <= L <= level of a visited node
-        std::map<std::pair<int, int>, int> cell_id;  // (j, L) -> index
-        std::vector<std::pair<int, int>> cells;
-        std::vector<int> top(N_total, 0);
-        for (int i = t0; i < t1; ++i) {
-            const int v = o == 0 ? i : N_total - 1 - i;
-            for (auto [node, L] : query_nodes(std::max(0, v - M), v)) top[node] = std::max(top[node], L);
-        }
-        for (int j = 0; j < N_total; ++j)
-            for (int L = 1; L <= top[j]; ++L) { cell_id[{j, L}] = (int)cells.size(); cells.push_back({j, L}); }
-        const int nc = (int)cells.size();
-        float4* RT = ex.ar.take<float4>((size_t)nc * n0);           // RT sums, level 0
-        float4* BT = ex.ar.take<float4>((size_t)nc * g.pyr_texels);  // BT cell pyramids
-        auto bt_pyr = [&](int v, int L) -> const float4* {
-            return L == 0 ? S.frame(orig(v) - f0) : BT + (long long)cell_id.at({v, L}) * g.pyr_texels;
-        };
-        // Alg. 3: RT(j,L) receives X_{i->j} for i in [j-2^L+1, j-2^(L-1)], summed ascending.
-        std::vector<int> cost(nc);
-        for (int c = 0; c < nc; ++c) cost[c] = 1 << (cells[c].second - 1);
-        const size_t mark = ex.ar.off;
-        for (auto [c0, c1] : make_batches(cost, cap)) {
-            ex.ar.off = mark;
-            std::vector<TaskSpec> tasks;
-            for (int c = c0; c < c1; ++c) {
-                const auto [j, L] = cells[c];
-                for (int v = j - (1 << L) + 1; v <= j - (1 << (L - 1)); ++v)
-                    tasks.push_back(TaskSpec{FR.slot(orig(v) - f0), S.frame(orig(v) - f0), G.frame(orig(j) - f0), -1,
-                                             (uint32_t)orig(v), (uint32_t)orig(j), tag_build});
-            }
-            BatchOut bo = run_nnf(ex, cfg, g, FR, tasks, {}, st);
-            CombineList cl;
-            int t = 0;
-            for (int c = c0; c < c1; ++c) {
-                const auto [j, L] = cells[c];
-                cl.begin();
-                for (int v = j - (1 << L) + 1; v <= j - (1 << (L - 1)); ++v) cl.add_remap(S.frame(orig(v) - f0), t++, 1.0f);
-                cl.end(RT + (long long)c * n0, 0, 1.0f);
-            }
-            if (st) st->remap_pixels += (uint64_t)tasks.size() * n0;
-            run_combine(ex, g, 0, cl, bo.F, bo.fstride);
-        }
-        ex.ar.off = mark;
-        // Alg. 4: BT(j,L) = (BT(j,L-1) + RT(j,L) * 2^-(L-1)) * 0.5, level by level
-        for (int L = 1; L <= lcap; ++L) {
-            CombineList cl;
-            for (int c = 0; c < nc; ++c) {
-                if (cells[c].second != L) continue;
-                const int j = cells[c].first;
-                cl.begin();
-                cl.add_img(bt_pyr(j, L - 1), 1.0f);
-                cl.add_img(RT + (long long)c * n0, 1.0f / (float)(1 << (L - 1)));
-                cl.end(BT + (long long)c * g.pyr_texels, 0, 2.0f);
-            }
-            run_combine(ex, g, 0, cl, nullptr, 0);
-        }
-        if (nc) pyramid_levels_inplace(ex, g, BT, nc, g.pyr_texels);
-        // Alg. 5 queries: A = sum over visited nodes of 2^L * (BT(i,L) -> S_r); the self node is BT itself.
-        std::vector<int> qcost;
-        std::vector<std::vector<std::pair<int, int>>> walks;
-        for (int i = t0; i < t1; ++i) {
-            const int v = o == 0 ? i : N_total - 1 - i;
-            walks.push_back(query_nodes(std::max(0, v - M), v));
-            qcost.push_back((int)walks.back().size() - 1);
-        }
-        const size_t mark2 = ex.ar.off;
-        for (auto [q0, q1] : make_batches(qcost, cap)) {
-            ex.ar.off = mark2;
-            std::vector<TaskSpec> tasks;
-            std::vector<SlotSpec> qspecs;  // query sources: (G_i, BT(i,L)) packed as SF32 (float style)
-            for (int q = q0; q < q1; ++q) {
-                const int i = t0 + q, v = o == 0 ? i : N_total - 1 - i;
-                for (auto [node, L] : walks[q]) {
-                    if (node == v) continue;
-                    qspecs.push_back(SlotSpec{nullptr, nullptr, G.frame(orig(node) - f0), bt_pyr(node, L)});
-                    tasks.push_back(TaskSpec{nullptr, bt_pyr(node, L), G.frame(i - f0), -1, (uint32_t)orig(node),
-                                             (uint32_t)i, tag_query});
-                }
-            }
-            const Slots QS = pack_sources(ex, g, fbk::SF8F, qspecs);
-            for (size_t t = 0; t < tasks.size(); ++t) tasks[t].src = QS.slot((long long)t);
-            BatchOut bo;
-            if (!tasks.empty()) bo = run_nnf(ex, cfg, g, QS, tasks, {}, st);
-            CombineList cl;
-            int t = 0;
-            for (int q = q0; q < q1; ++q) {
-                const int v = o == 0 ? t0 + q : N_total - 1 - (t0 + q);
-                cl.begin();
-                for (auto [node, L] : walks[q]) {
-                    const float wgt = (float)(1 << L);
-                    if (node == v) cl.add_img(bt_pyr(node, L), wgt);
-                    else cl.add_remap(bt_pyr(node, L), t++, wgt);
-                }
-                cl.end(A[o] + (long long)q * n0, 0, 1.0f);
-            }
-            if (st) st->remap_pixels += (uint64_t)tasks.size() * n0;
-            run_combine(ex, g, 0, cl, bo.F, bo.fstride);
-        }
+        const CellMap cells = tree_build(ex, cfg, g, N_total, f0, G, S, FR, o, tree_top(N_total, M, o, t0, t1), st);
+        tree_query(ex, cfg, g, N_total, f0, M, G, S, o, t0, t1, cells, A[o], st);
         ex.ar.off = omark;
     }
-    // Eq. 6: out_i = ((A_f + A_r) - S_i) / |W_i|
-    CombineList cl;
-    for (int q = 0; q < nt; ++q) {
-        const int i = t0 + q, lo = std::max(0, i - M), hi = std::min(N_total - 1, i + M);
-        cl.begin();
-        cl.add_img(A[0] + (long long)q * n0, 1.0f);
-        cl.add_img(A[1] + (long long)q * n0, 1.0f);
-        cl.add_img(S.frame(i - f0), -1.0f);
-        cl.end(out + 3LL * n0 * q, 1, (float)(hi - lo + 1));
+    tree_merge(ex, g, N_total, f0, M, S, t0, t1, A, out);
+}
+
+// Sharded tree schedule with cell exchange, phase 1: build the listed cells {o, j, L}
+// (orientation order) into cell_out, one pyramid of g.pyr_texels float4 texels per listed cell.
+void tree_build_cells(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N_total, int f0, int N,
+                      const uint8_t* guide, const uint8_t* style, int n_cells, const int32_t* cl, float* cell_out,
+                      fb_stats* st)
+{
+    fb_match_cfg cfg = cfg0;
+    cfg.loss = FB_LOSS_GUIDE_STYLE;
+    const Pyr G = pyramid_u8(ex, g, guide, N);
+    const Pyr S = pyramid_u8(ex, g, style, N);
+    const long long n0 = g.npx0();
+    std::vector<SlotSpec> specs;
+    for (int j = 0; j < N; ++j) specs.push_back(SlotSpec{guide + 3 * n0 * j, style + 3 * n0 * j, G.frame(j), S.frame(j)});
+    const Slots FR = pack_sources(ex, g, fbk::SF8, specs);
+    for (int o = 0; o < 2; ++o) {
+        std::vector<int> top(N_total, 0);
+        bool any = false;
+        for (int c = 0; c < n_cells; ++c)
+            if (cl[3 * c] == o) { top[cl[3 * c + 1]] = std::max(top[cl[3 * c + 1]], cl[3 * c + 2]); any = true; }
+        if (!any) continue;
+        const size_t omark = ex.ar.off;
+        const CellMap cells = tree_build(ex, cfg, g, N_total, f0, G, S, FR, o, top, st);
+        for (int c = 0; c < n_cells; ++c)
+            if (cl[3 * c] == o)
+                ex.d2d(cell_out + (size_t)c * 4 * g.pyr_texels, cells.at({cl[3 * c + 1], cl[3 * c + 2]}),
+                       sizeof(float4) * (size_t)g.pyr_texels);
+        ex.ar.off = omark;
     }
-    run_combine(ex, g, 0, cl, nullptr, 0);
+}
+
+// Phase 2: the queries of targets [t0, t1) from local frames plus the given cells, then Eq. 6.
+void tree_query_cells(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N_total, int f0, int N, int M,
+                      const uint8_t* guide, const uint8_t* style, int t0, int t1, int n_cells, const int32_t* cl,
+                      const float* const* cell_ptrs, float* out, fb_stats* st)
+{
+    fb_match_cfg cfg = cfg0;
+    cfg.loss = FB_LOSS_GUIDE_STYLE;
+    const Pyr G = pyramid_u8(ex, g, guide, N);
+    const Pyr S = pyramid_u8(ex, g, style, N);
+    const long long n0 = g.npx0();
+    const int nt = t1 - t0;
+    float4* A[2] = {ex.ar.take<float4>((size_t)nt * n0), ex.ar.take<float4>((size_t)nt * n0)};
+    for (int o = 0; o < 2; ++o) {
+        CellMap cells;
+        for (int c = 0; c < n_cells; ++c)
+            if (cl[3 * c] == o)
+                cells[{cl[3 * c + 1], cl[3 * c + 2]}] = cell_ptrs ? reinterpret_cast<const float4*>(cell_ptrs[c]) : nullptr;
+        tree_query(ex, cfg, g, N_total, f0, M, G, S, o, t0, t1, cells, A[o], st);
+    }
+    tree_merge(ex, g, N_total, f0, M, S, t0, t1, A, out);
 }
 
 // ------------------------------------------------------------------------------------ interpolation
@@ -1131,6 +1231,68 @@ fb_status fb_blend_window_range(fb_ctx ctx, const fb_match_cfg* cfg, int schedul
     return guarded(ctx, stats, [&](Exec& ex, fb_stats* st) {
         blend_range_body(ex, st, cfg, schedule, N_total, f0, N, H, W, M, guide, style, t0, t1, out);
     });
+}
+
+size_t fb_tree_cell_texels(const fb_match_cfg* cfg, int H, int W)
+{
+    try {
+        if (!cfg) return 0;
+        validate_cfg(cfg);
+        return (size_t)make_geo(*cfg, H, W).pyr_texels;
+    } catch (...) {
+        return 0;
+    }
+}
+
+static void tree_common_checks(const fb_match_cfg* cfg, int N_total, int f0, int N, int H, int W,
+                               const uint8_t* guide, const uint8_t* style, int n_cells, const int32_t* cells)
+{
+    validate_cfg(cfg);
+    check_frames(N_total, H, W);
+    if (cfg->loss != FB_LOSS_GUIDE_STYLE) throw Fail{FB_ERR_INVALID_ARG, "the tree schedule uses GUIDE_STYLE"};
+    if (!guide || !style) throw Fail{FB_ERR_INVALID_ARG, "NULL frames"};
+    if (f0 < 0 || N < 1 || f0 + N > N_total) throw Fail{FB_ERR_INVALID_ARG, "bad local frame range"};
+    if (n_cells < 0 || (n_cells > 0 && !cells)) throw Fail{FB_ERR_INVALID_ARG, "bad cell list"};
+    for (int c = 0; c < n_cells; ++c) {
+        const int o = cells[3 * c], j = cells[3 * c + 1], L = cells[3 * c + 2];
+        if ((o != 0 && o != 1) || j < 0 || j >= N_total || L < 1 || L > 30 || j - (1 << L) + 1 < 0)
+            throw Fail{FB_ERR_INVALID_ARG, "bad cell {orient, j, L}"};
+    }
+}
+
+fb_status fb_tree_build_cells(fb_ctx ctx, const fb_match_cfg* cfg, int N_total, int f0, int N, int H, int W,
+                              const uint8_t* guide, const uint8_t* style, int n_cells, const int32_t* cells,
+                              float* cell_out, fb_stats* stats, size_t* ws_needed)
+{
+    return guarded(ctx, stats, [&](Exec& ex, fb_stats* st) {
+        tree_common_checks(cfg, N_total, f0, N, H, W, guide, style, n_cells, cells);
+        if (n_cells > 0 && !cell_out && !ex.dry) throw Fail{FB_ERR_INVALID_ARG, "NULL cell_out"};
+        for (int c = 0; c < n_cells; ++c) {  // every frame a cell reads is local
+            const int o = cells[3 * c], j = cells[3 * c + 1], L = cells[3 * c + 2];
+            const int a = j - (1 << L) + 1, b = j;
+            const int lo = o == 0 ? a : N_total - 1 - b, hi = o == 0 ? b : N_total - 1 - a;
+            if (lo < f0 || hi >= f0 + N) throw Fail{FB_ERR_INVALID_ARG, "a cell reads frames outside the local range"};
+        }
+        const Geo g = make_geo(*cfg, H, W);
+        tree_build_cells(ex, *cfg, g, N_total, f0, N, guide, style, n_cells, cells, cell_out, st);
+    }, ws_needed);
+}
+
+fb_status fb_tree_query(fb_ctx ctx, const fb_match_cfg* cfg, int N_total, int f0, int N, int H, int W, int M,
+                        const uint8_t* guide, const uint8_t* style, int t0, int t1, int n_cells,
+                        const int32_t* cells, const float* const* cell_ptrs, float* out, fb_stats* stats,
+                        size_t* ws_needed)
+{
+    return guarded(ctx, stats, [&](Exec& ex, fb_stats* st) {
+        tree_common_checks(cfg, N_total, f0, N, H, W, guide, style, n_cells, cells);
+        if (M < 0) throw Fail{FB_ERR_INVALID_ARG, "M < 0"};
+        if (t0 < 0 || t1 > N_total || t0 >= t1) throw Fail{FB_ERR_INVALID_ARG, "bad target range"};
+        if (f0 > std::max(0, t0 - M) || f0 + N < std::min(N_total, t1 + M))
+            throw Fail{FB_ERR_INVALID_ARG, "local frames must cover the targets plus a halo of M"};
+        if (!ex.dry && (!out || (n_cells > 0 && !cell_ptrs))) throw Fail{FB_ERR_INVALID_ARG, "NULL pointer"};
+        const Geo g = make_geo(*cfg, H, W);
+        tree_query_cells(ex, *cfg, g, N_total, f0, N, M, guide, style, t0, t1, n_cells, cells, cell_ptrs, out, st);
+    }, ws_needed);
 }
 
 fb_status fb_blend_window(fb_ctx ctx, const fb_match_cfg* cfg, int schedule, int N, int H, int W, int M,

@@ -27,7 +27,7 @@ STATUS = {0: "FB_OK", 1: "FB_ERR_INVALID_ARG", 2: "FB_ERR_SHAPE", 3: "FB_ERR_CUD
 SYMBOLS = ["fb_ctx_create", "fb_ctx_destroy", "fb_last_error", "fb_set_workspace", "fb_set_max_batch_pairs",
            "fb_workspace_size", "fb_workspace_size_range", "fb_launch_count", "fb_pyramid_elems", "fb_build_pyramid", "fb_nnf_estimate",
            "fb_remap", "fb_blend_window", "fb_blend_window_range", "fb_interpolate_keyframes", "fb_profile_enable",
-           "fb_profile_read", "fb_profile_reset"]
+           "fb_profile_read", "fb_profile_reset", "fb_tree_cell_texels", "fb_tree_build_cells", "fb_tree_query"]
 
 
 class FBError(RuntimeError):
@@ -117,6 +117,11 @@ def load_library(build_if_missing: bool = True):
     lib.fb_blend_window_range.argtypes = [V, P(_Cfg), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                           V, V, C.c_int, C.c_int, V, P(_Stats)]
     lib.fb_interpolate_keyframes.argtypes = [V, P(_Cfg), C.c_int, C.c_int, C.c_int, V, C.c_int, V, V, V, P(_Stats)]
+    lib.fb_tree_cell_texels.argtypes = [P(_Cfg), C.c_int, C.c_int]
+    lib.fb_tree_cell_texels.restype = C.c_size_t
+    lib.fb_tree_build_cells.argtypes = [V, P(_Cfg)] + [C.c_int] * 5 + [V, V, C.c_int, V, V, P(_Stats), P(C.c_size_t)]
+    lib.fb_tree_query.argtypes = [V, P(_Cfg)] + [C.c_int] * 6 + [V, V, C.c_int, C.c_int, C.c_int, V, V, V, P(_Stats),
+                                                                P(C.c_size_t)]
     lib.fb_profile_enable.argtypes = [V, C.c_int]
     lib.fb_profile_read.argtypes = [V, P(_Prof), C.c_int]
     lib.fb_profile_read.restype = C.c_int
@@ -259,6 +264,61 @@ class Context:
         c = cfg.c()
         self._check(self.lib.fb_blend_window(self.h, C.byref(c), schedule, N, H, W, M, _ptr(g), _ptr(s), _ptr(out),
                                              C.byref(st)))
+        return out, st.as_dict()
+
+    # ---- sharded tree schedule with cell exchange (include/fb.h) -------------------------
+    def tree_cell_texels(self, cfg: MatchCfg, H: int, W: int) -> int:
+        c = cfg.c()
+        n = int(self.lib.fb_tree_cell_texels(C.byref(c), H, W))
+        if n == 0:
+            raise FBError(1, "invalid configuration for the frame size")
+        return n
+
+    @staticmethod
+    def _cells(cells):
+        flat = [int(x) for cell in cells for x in cell]
+        return (C.c_int32 * max(len(flat), 1))(*flat), len(cells)
+
+    def fb_tree_build_cells(self, cfg: MatchCfg, N_total: int, f0: int, guide, style, cells):
+        """Builds the cells [(orient, j, L), ...] from local frames f0..f0+N-1: (float32 [n, texels, 4], stats)."""
+        g = _dev(guide, self.device, torch.uint8)
+        s = _dev(style, self.device, torch.uint8)
+        N, H, W, _ = g.shape
+        arr, n = self._cells(cells)
+        c = cfg.c()
+        need = C.c_size_t(0)
+        self._check(self.lib.fb_tree_build_cells(self.h, C.byref(c), N_total, f0, N, H, W, _ptr(g), _ptr(s), n, arr,
+                                                  None, None, C.byref(need)))
+        self.ensure_workspace(int(need.value))
+        out = torch.empty((n, self.tree_cell_texels(cfg, H, W), 4), dtype=torch.float32, device=self.device)
+        st = _Stats()
+        self._check(self.lib.fb_tree_build_cells(self.h, C.byref(c), N_total, f0, N, H, W, _ptr(g), _ptr(s), n, arr,
+                                                  _ptr(out), C.byref(st), None))
+        return out, st.as_dict()
+
+    def fb_tree_query(self, cfg: MatchCfg, N_total: int, f0: int, guide, style, M: int, t0: int, t1: int, cells,
+                      cell_tensors, out: torch.Tensor | None = None):
+        """Targets [t0, t1) from local frames plus cells (list of (orient, j, L)) whose pyramids are the
+        matching entries of cell_tensors (a list of [texels, 4] tensors or one [n, texels, 4] tensor)."""
+        g = _dev(guide, self.device, torch.uint8)
+        s = _dev(style, self.device, torch.uint8)
+        N, H, W, _ = g.shape
+        arr, n = self._cells(cells)
+        tens = [t.contiguous() for t in cell_tensors] if n else []
+        for t in tens:
+            if t.device != self.device or t.dtype != torch.float32:
+                raise ValueError("cell tensors must be float32 on the context device")
+        ptrs = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in tens])
+        c = cfg.c()
+        need = C.c_size_t(0)
+        self._check(self.lib.fb_tree_query(self.h, C.byref(c), N_total, f0, N, H, W, M, _ptr(g), _ptr(s), t0, t1, n,
+                                            arr, ptrs, None, None, C.byref(need)))
+        self.ensure_workspace(int(need.value))
+        if out is None:
+            out = torch.empty((t1 - t0, H, W, 3), dtype=torch.float32, device=self.device)
+        st = _Stats()
+        self._check(self.lib.fb_tree_query(self.h, C.byref(c), N_total, f0, N, H, W, M, _ptr(g), _ptr(s), t0, t1, n,
+                                            arr, ptrs, _ptr(out), C.byref(st), None))
         return out, st.as_dict()
 
     def fb_blend_window_range(self, cfg: MatchCfg, schedule: int, N_total: int, f0: int, guide, style, M: int,

@@ -106,3 +106,99 @@ def halo_exchange(owned: list[torch.Tensor], plan: list[tuple[int, int]], N: int
         for r in dist.batch_isend_irecv(ops):
             r.wait()
     return locals_, f0
+
+
+# ---------------------------------------------------------------------------------------------- tree
+# Tree schedule (Alg. 3-5): a shard's Alg. 5 queries visit blending-table cells BT(node, L) of nodes up to
+# M frames outside its targets.  Rebuilding them (fb_blend_window_range) costs ~20 % extra NNFs per GPU at
+# G = 8; instead every cell has one owner (the rank owning the node's frame), owners build the
+# cells any rank needs, and the cells move point-to-point once, before the queries (include/fb.h).
+
+def query_nodes(l: int, r: int) -> list[tuple[int, int]]:
+    """Alg. 5's walk over [l, r] (D23: i <- i - 2^L): the (node, L) pairs it visits."""
+    out, i = [], r
+    while i >= l:
+        L = 0
+        while (i >> L) & 1 and i - (1 << (L + 1)) + 1 >= l:
+            L += 1
+        out.append((i, L))
+        i -= 1 << L
+    return out
+
+
+def tree_cells_needed(N: int, M: int, t0: int, t1: int) -> list[tuple[int, int, int]]:
+    """Cells (orient, node, L >= 1) the queries of targets [t0, t1) visit, in a canonical order."""
+    need = set()
+    for o in (0, 1):
+        for i in range(t0, t1):
+            v = i if o == 0 else N - 1 - i
+            for node, L in query_nodes(max(0, v - M), v):
+                if L >= 1:
+                    need.add((o, node, L))
+    return sorted(need)
+
+
+def cell_frame(N: int, cell: tuple[int, int, int]) -> int:
+    """Original frame id of a cell's node (its owner is the rank owning that frame)."""
+    o, j, _ = cell
+    return j if o == 0 else N - 1 - j
+
+
+def exchange_cells(plan: list[tuple[int, int]], N: int, M: int, rank: int, built: dict, texels: int,
+                   device, group=None) -> dict:
+    """built: {cell: tensor [texels, 4]} of the cells this rank owns and some rank needs.  Sends each peer
+    the cells it needs from this rank (one message per peer, cells in canonical order) and receives the
+    cells this rank needs from their owners.  Returns {cell: tensor} for every cell this rank's queries
+    visit (its own built ones plus the received ones)."""
+    world = len(plan)
+    t0, t1 = plan[rank]
+    mine = tree_cells_needed(N, M, t0, t1) if t1 > t0 else []
+    owner = {c: owner_of(plan, cell_frame(N, c)) for c in mine}
+    ops, recv = [], {}
+    for g in range(world):
+        if g == rank:
+            continue
+        a, b = plan[g]
+        theirs = [c for c in tree_cells_needed(N, M, a, b) if owner_of(plan, cell_frame(N, c)) == rank] if b > a else []
+        if theirs:
+            ops.append(dist.P2POp(dist.isend, torch.stack([built[c] for c in theirs]).contiguous(), g, group))
+        from_g = [c for c in mine if owner[c] == g]
+        if from_g:
+            buf = torch.empty((len(from_g), texels, 4), dtype=torch.float32, device=device)
+            ops.append(dist.P2POp(dist.irecv, buf, g, group))
+            recv[g] = (from_g, buf)
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    cells = {c: built[c] for c in mine if owner[c] == rank}
+    for from_g, buf in recv.values():
+        for k, c in enumerate(from_g):
+            cells[c] = buf[k]
+    return cells
+
+
+def cells_to_build(plan: list[tuple[int, int]], N: int, M: int, rank: int) -> list[tuple[int, int, int]]:
+    """Cells this rank owns that some rank's queries visit (canonical order)."""
+    need = set()
+    for a, b in plan:
+        if b > a:
+            need.update(tree_cells_needed(N, M, a, b))
+    return sorted(c for c in need if owner_of(plan, cell_frame(N, c)) == rank)
+
+
+def blend_tree_exchange(ctx, cfg, plan: list[tuple[int, int]], N: int, M: int, rank: int, guide_loc, style_loc,
+                        f0: int, out=None, group=None):
+    """Fast-mode blend of this rank's targets with cell exchange: build owned cells, exchange, query."""
+    t0, t1 = plan[rank]
+    H, W = int(guide_loc.shape[1]), int(guide_loc.shape[2])
+    texels = ctx.tree_cell_texels(cfg, H, W)
+    build = cells_to_build(plan, N, M, rank)
+    built, st_b = {}, {}
+    if build:
+        T, st_b = ctx.fb_tree_build_cells(cfg, N, f0, guide_loc, style_loc, build)
+        built = {c: T[k] for k, c in enumerate(build)}
+    cells = exchange_cells(plan, N, M, rank, built, texels, guide_loc.device, group)
+    order = sorted(cells)
+    out, st_q = ctx.fb_tree_query(cfg, N, f0, guide_loc, style_loc, M, t0, t1, order, [cells[c] for c in order],
+                                  out=out)
+    return out, {k: st_q.get(k, 0) + st_b.get(k, 0) for k in st_q}

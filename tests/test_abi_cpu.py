@@ -71,3 +71,23 @@ def test_context_creation_fails_loudly_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         fb.Context(0)
+
+
+def declared_param_counts():
+    """{function: number of parameters} from include/fb.h prototypes."""
+    text = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    out = {}
+    for name, params in re.findall(r"\b(fb_\w+)\s*\(([^;{]*?)\)\s*;", text, flags=re.S):
+        params = params.strip()
+        out[name] = 0 if params in ("", "void") else params.count(",") + 1
+    return out
+
+
+def test_binding_argtypes_match_header_arity():
+    """Every ctypes prototype of the binding passes exactly the parameters the header declares."""
+    lib = fb.load_library()
+    counts = declared_param_counts()
+    assert set(counts) == set(fb.SYMBOLS)
+    for name, n in counts.items():
+        at = getattr(lib, name).argtypes
+        assert at is not None and len(at) == n, (name, n, at and len(at))

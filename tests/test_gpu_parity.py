@@ -345,3 +345,33 @@ def test_fused_fields_equal_per_field_launches(fb, mode, monkeypatch):
         out, _ = c.fb_blend_window(cfg, sched, dev(g), dev(s), 3)
         assert torch.equal(out, ref)
 
+
+
+@pytest.mark.parametrize("N,M,world", [(12, 5, 3), (10, 3, 2), (9, 8, 3)])
+def test_tree_cell_exchange_matches_full_blend(fb, N, M, world):
+    """Sharded fast mode with blending-table cell exchange: every rank builds only the cells
+    it owns, the cells move between ranks (here: within one process), and each rank's queries reproduce its
+    targets of the single-call tree blend bit for bit."""
+    from paper_2311_09265_b200 import shard
+    g, s = moving_texture(N, 40, 48, seed=13)
+    cfg = fb.MatchCfg(iters_per_level=1, loss=fb.GUIDE_STYLE)
+    full, _ = fb.Context(0).fb_blend_window(cfg, fb.TREE, dev(g), dev(s), M)
+    plan = shard.plan_shards(N, M, world, "tree")
+    ctx = fb.Context(0)
+    pool = {}
+    for r in range(world):
+        f0, f1 = shard.halo_range(N, M, *plan[r])
+        build = shard.cells_to_build(plan, N, M, r)
+        if build:
+            T, _ = ctx.fb_tree_build_cells(cfg, N, f0, dev(g[f0:f1]), dev(s[f0:f1]), build)
+            pool.update({c: T[k] for k, c in enumerate(build)})
+    for r in range(world):
+        t0, t1 = plan[r]
+        f0, f1 = shard.halo_range(N, M, t0, t1)
+        need = shard.tree_cells_needed(N, M, t0, t1)
+        out, _ = ctx.fb_tree_query(cfg, N, f0, dev(g[f0:f1]), dev(s[f0:f1]), M, t0, t1, need, [pool[c] for c in need])
+        assert torch.equal(out, full[t0:t1])
+        if need:  # a query whose cells are incomplete is rejected, not silently wrong
+            with pytest.raises(fb.FBError):
+                ctx.fb_tree_query(cfg, N, f0, dev(g[f0:f1]), dev(s[f0:f1]), M, t0, t1, need[1:],
+                                  [pool[c] for c in need[1:]])

@@ -78,3 +78,78 @@ def test_halo_exchange_gloo(world, N, M):
     res = dict(q.get(timeout=5) for _ in range(world))
     assert all(p.exitcode == 0 for p in procs)
     assert all(res[r] for r in range(world)), res
+
+
+# ------------------------------------------------------------------------------ tree cell exchange
+def _brute_query_nodes(l, r):
+    """Alg. 5 written out (D23): from i = r, take the largest aligned block [i-2^L+1, i] inside [l, r]."""
+    out, i = [], r
+    while i >= l:
+        L = 0
+        while (i + 1) % (1 << (L + 1)) == 0 and i - (1 << (L + 1)) + 1 >= l:
+            L += 1
+        out.append((i, L))
+        i -= 1 << L
+    return out
+
+
+@pytest.mark.parametrize("N,M", [(200, 30), (50, 7), (9, 0), (16, 15)])
+def test_query_walk_partitions_window(N, M):
+    for v in range(N):
+        l = max(0, v - M)
+        walk = shard.query_nodes(l, v)
+        assert walk == _brute_query_nodes(l, v)
+        covered = sorted(x for node, L in walk for x in range(node - (1 << L) + 1, node + 1))
+        assert covered == list(range(l, v + 1))
+
+
+@pytest.mark.parametrize("N,M,world", [(200, 30, 8), (200, 30, 3), (50, 7, 4), (12, 6, 3), (5, 9, 2), (7, 3, 8)])
+def test_tree_cells_built_once_and_cover_every_need(N, M, world):
+    """Across ranks the owned builds partition the cells the whole video's queries visit (no cell is built
+    twice, none is missing), and every cell a rank builds reads only frames in its halo range."""
+    plan = shard.plan_shards(N, M, world, "tree")
+    builds = [shard.cells_to_build(plan, N, M, r) for r in range(world)]
+    flat = [c for b in builds for c in b]
+    assert len(flat) == len(set(flat))
+    assert set(flat) == set(shard.tree_cells_needed(N, M, 0, N))
+    for r, b in enumerate(builds):
+        f0, f1 = shard.halo_range(N, M, *plan[r])
+        for o, j, L in b:
+            lo, hi = (j - (1 << L) + 1, j) if o == 0 else (N - 1 - j, N - 1 - j + (1 << L) - 1)
+            assert f0 <= lo and hi < f1
+
+
+def _cell_value(c, texels):
+    o, j, L = c
+    return torch.full((texels, 4), float(o * 100000 + j * 100 + L))
+
+
+def _tree_worker(rank, world, port, N, M, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        texels = 5
+        plan = shard.plan_shards(N, M, world, "tree")
+        built = {c: _cell_value(c, texels) for c in shard.cells_to_build(plan, N, M, rank)}
+        got = shard.exchange_cells(plan, N, M, rank, built, texels, torch.device("cpu"))
+        t0, t1 = plan[rank]
+        need = shard.tree_cells_needed(N, M, t0, t1) if t1 > t0 else []
+        ok = sorted(got) == need and all(torch.equal(got[c], _cell_value(c, texels)) for c in need)
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,N,M", [(2, 24, 7), (3, 40, 12), (3, 10, 9)])
+def test_tree_cell_exchange_gloo(world, N, M):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tree_worker, args=(r, world, port, N, M, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    res = dict(q.get(timeout=5) for _ in range(world))
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(res[r] for r in range(world)), res
