@@ -37,6 +37,9 @@ WORKLOADS = {
     # configs[2]: fast mode (tree), window 30
     "config3": dict(desc="blending mode fast (tree-combined window), 200 frames 512x512, window 30 "
                          "(BASELINE.json configs[2])", N=200, H=512, W=512, M=30, p=2, mode="fast"),
+    # configs[3]: keyframe interpolation (Eq. 9), keys 0 and 101, 100 in-between frames at 768x768
+    "config4": dict(desc="interpolation mode, 2 keyframes rendering 100 in-between frames 768x768, patch 5 "
+                         "(BASELINE.json configs[3])", N=102, H=768, W=768, M=0, p=2, mode="interp", keys=[0, 101]),
     # balanced mode at the metric's size (not a BASELINE config; for comparison)
     "balanced512": dict(desc="blending mode balanced, 200 frames 512x512, patch 5, window 15", N=200, H=512, W=512,
                         M=15, p=2, mode="balanced"),
@@ -114,7 +117,7 @@ class ClockSampler:
 
 
 def make_cfg(P, wl):
-    loss = {"accurate": P.MEAN_ALIGN, "balanced": P.GUIDE_STYLE, "fast": P.GUIDE_STYLE}[wl["mode"]]
+    loss = {"accurate": P.MEAN_ALIGN, "balanced": P.GUIDE_STYLE, "fast": P.GUIDE_STYLE, "interp": P.GUIDE_STYLE}[wl["mode"]]
     sched = P.TREE if wl["mode"] == "fast" else P.DIRECT
     return P.MatchCfg(patch_radius=wl["p"], iters_per_level=5, alpha=10.0, loss=loss, seed=1), sched
 
@@ -144,6 +147,9 @@ def oracle_sample(wl, n_pairs: int, threads: int | None = None):
 
 def workload_pairs(wl) -> int:
     N, M = wl["N"], wl["M"]
+    if wl["mode"] == "interp":
+        keys = wl["keys"]
+        return sum(int(any(k < m for k in keys)) + int(any(k > m for k in keys)) for m in range(N) if m not in keys)
     if wl["mode"] == "fast":
         return 2242 if (N, M) == (200, 30) else N * 10  # exact count for config 3
     return sum(min(N - 1, i + M) - max(0, i - M) for i in range(N))
@@ -213,9 +219,15 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     N, H, W, M = wl["N"], wl["H"], wl["W"], wl["M"]
     cfg, sched = make_cfg(P, wl)
-    plan = shard.plan_shards(N, M, world, "tree" if sched == P.TREE else "direct")
+    interp = wl["mode"] == "interp"
+    keys = wl.get("keys", [])
+    plan = shard.plan_interp_shards(N, keys, world) if interp else \
+        shard.plan_shards(N, M, world, "tree" if sched == P.TREE else "direct")
     t0, t1 = plan[rank]
     g_all, s_all = moving_texture(N, H, W)  # deterministic: every rank would load only its own frames
+    if interp:  # the key styles live on rank 0 (broadcast inside the step); s_own is unused
+        ks_all = torch.from_numpy(s_all[keys]).to(dev) if rank == 0 else None
+        ks_host = torch.from_numpy(s_all[keys]).pin_memory() if rank == 0 else None
     g_own = torch.from_numpy(g_all[t0:t1]).to(dev)
     s_own = torch.from_numpy(s_all[t0:t1]).to(dev)
     g_host = torch.from_numpy(g_all[t0:t1]).pin_memory()
@@ -226,7 +238,15 @@ def main():
     out = torch.empty((t1 - t0, H, W, 3), dtype=torch.float32, device=dev)
     stats = {}
 
-    def step(g_in, s_in):
+    def step(g_in, s_in, ks_in=None):
+        if interp:
+            ks = ks_in if ks_in is not None else ks_all
+            if world > 1:
+                _, st = shard.interpolate_sharded(ctx, cfg, plan, N, keys, rank, g_in, ks, out=out)
+            else:
+                _, st = ctx.fb_interpolate_keyframes(cfg, g_in, keys, ks, out=out)
+            stats.update(st)
+            return
         if world > 1:
             (g_loc, s_loc), f0 = shard.halo_exchange([g_in, s_in], plan, N, M, rank)
             if sched == P.TREE:  # fast mode: owned blending-table cells built once, exchanged
@@ -283,8 +303,10 @@ def main():
         e0.record(stream)
         for _ in range(args.steps):
             g_d = g_host.to(dev, non_blocking=True)
-            s_d = s_host.to(dev, non_blocking=True)
-            step(g_d, s_d)
+            if interp:
+                step(g_d, None, ks_host.to(dev, non_blocking=True) if rank == 0 else None)
+            else:
+                step(g_d, s_host.to(dev, non_blocking=True))
             out_host.copy_(out, non_blocking=True)
         e1.record(stream)
         barrier()
@@ -292,7 +314,8 @@ def main():
         if world > 1:
             dist.all_reduce(t2, op=dist.ReduceOp.MAX)
         ms_e2e = float(t2.item()) / args.steps
-        e2e = {"value": N / (ms_e2e / 1e3), "unit": "frames/s", "h2d_bytes_per_step": int(2 * N * H * W * 3),
+        h2d = (N + len(keys)) * H * W * 3 if interp else 2 * N * H * W * 3
+        e2e = {"value": N / (ms_e2e / 1e3), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(N * H * W * 3 * 4), "ms_per_step": ms_e2e}
 
     if rank != 0:
@@ -340,7 +363,7 @@ def main():
         import oracle as O
         cores = len(os.sched_getaffinity(0))
         O.set_threads(cores)
-        dt, npairs, ev = oracle_sample(wl, args.cpu_pairs)
+        dt, npairs, ev = oracle_sample(wl, min(args.cpu_pairs, 8) if wl["mode"] == "interp" else args.cpu_pairs)
         pairs_total = workload_pairs(wl)
         cpu = {"value": N / (dt / npairs * pairs_total), "unit": "frames/s", "cores": cores, "kind": "oracle",
                "sample": f"{npairs} of the {pairs_total} NNF pairs (target 0's window, full resolution, same loss, "

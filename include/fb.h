@@ -206,6 +206,16 @@ fb_status fb_interpolate_keyframes(fb_ctx ctx, const fb_match_cfg* cfg, int N, i
                                    int K, const int32_t* key_index, const uint8_t* key_style, float* out,
                                    fb_stats* stats);
 
+/* Same, restricted to output frames [t0, t1) (sharded interpolation): guide holds frames
+ * t0..t1-1 only, key_guide [K,H,W,3] the keyframes' guide frames (broadcast to every shard with the key
+ * styles), out [t1-t0,H,W,3].  Frame ids in RNG keys are original ids, so the rows equal the full call's.
+ * cfg.tracking couples all frames of a key span (D42): FB_ERR_UNSUPPORTED unless [t0,t1) = [0,N).
+ * ws_needed (nullable): when non-NULL, nothing runs; the workspace bytes the call needs are stored there. */
+fb_status fb_interpolate_keyframes_range(fb_ctx ctx, const fb_match_cfg* cfg, int N, int H, int W, int t0, int t1,
+                                         const uint8_t* guide, int K, const int32_t* key_index,
+                                         const uint8_t* key_guide, const uint8_t* key_style, float* out,
+                                         fb_stats* stats, size_t* ws_needed);
+
 #ifdef __cplusplus
 }
 #endif

@@ -877,22 +877,28 @@ void tree_query_cells(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N_to
 
 // ------------------------------------------------------------------------------------ interpolation
 // Eq. 9 (D28).
-void interpolate(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N, const uint8_t* guide, int K,
-                 const int32_t* keys, const uint8_t* key_style, float* out, fb_stats* st)
+// Targets [t0, t1) of an N-frame video: guide holds frames t0..t1-1; key_guide the K keyframes' guides
+// (nullptr: taken from guide, which then must hold every keyframe, i.e. the full call).
+void interpolate(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N, int t0, int t1, const uint8_t* guide,
+                 int K, const int32_t* keys, const uint8_t* key_guide, const uint8_t* key_style, float* out,
+                 fb_stats* st)
 {
     // cfg.loss == PAIRWISE: frames between two keys estimate both NNFs jointly with the alignment loss
     // of Eq. 10 (D38-D40); single-key frames and all other losses use Eq. 3 (GUIDE_STYLE).
     const bool align = cfg0.loss == FB_LOSS_PAIRWISE;
-    const Pyr G = pyramid_u8(ex, g, guide, N);
+    const Pyr G = pyramid_u8(ex, g, guide, t1 - t0);
     const Pyr KS = pyramid_u8(ex, g, key_style, K);
     const long long n0 = g.npx0();
+    Pyr GK;
+    if (key_guide) GK = pyramid_u8(ex, g, key_guide, K);
+    auto kg8 = [&](int k) { return key_guide ? key_guide + 3 * n0 * k : guide + 3 * n0 * (keys[k] - t0); };
+    auto kgp = [&](int k) { return key_guide ? GK.frame(k) : G.frame(keys[k] - t0); };
     std::vector<SlotSpec> specs;
-    for (int k = 0; k < K; ++k)
-        specs.push_back(SlotSpec{guide + 3 * n0 * keys[k], key_style + 3 * n0 * k, G.frame(keys[k]), KS.frame(k)});
+    for (int k = 0; k < K; ++k) specs.push_back(SlotSpec{kg8(k), key_style + 3 * n0 * k, kgp(k), KS.frame(k)});
     const Slots KSl = pack_sources(ex, g, (align && g.p > 2) ? fbk::SF32 : fbk::SF8, specs);
     struct Tgt { int m, left, right, key; };  // key indices (or -1)
     std::vector<Tgt> tg[2];  // [0]: keys and GUIDE_STYLE targets, [1]: aligned (two-key) targets
-    for (int m = 0; m < N; ++m) {
+    for (int m = t0; m < t1; ++m) {
         Tgt t{m, -1, -1, -1};
         for (int k = 0; k < K; ++k) {
             if (keys[k] == m) t.key = k;
@@ -924,12 +930,12 @@ void interpolate(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N, const 
                 if (t.key >= 0) continue;
                 if (t.left >= 0) {
                     tl[q - b0] = (int)tasks.size();
-                    tasks.push_back(TaskSpec{KSl.slot(t.left), KS.frame(t.left), G.frame(t.m), -1,
+                    tasks.push_back(TaskSpec{KSl.slot(t.left), KS.frame(t.left), G.frame(t.m - t0), -1,
                                              (uint32_t)keys[t.left], (uint32_t)t.m, 5u});
                 }
                 if (t.right >= 0) {
                     tr[q - b0] = (int)tasks.size();
-                    tasks.push_back(TaskSpec{KSl.slot(t.right), KS.frame(t.right), G.frame(t.m), -1,
+                    tasks.push_back(TaskSpec{KSl.slot(t.right), KS.frame(t.right), G.frame(t.m - t0), -1,
                                              (uint32_t)keys[t.right], (uint32_t)t.m, 5u});
                 }
                 if (pass == 1) {  // counterparts (Eq. 10)
@@ -964,7 +970,7 @@ void interpolate(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N, const 
                     cl.add_remap(KS.frame(t.right), tr[q - b0], wr, KSl, t.right);  // A = X_r w_r, fma(X_l, w_l, A)
                     cl.add_remap(KS.frame(t.left), tl[q - b0], wl, KSl, t.left);
                 }
-                cl.end(out + 3LL * n0 * t.m, 1, 1.0f);
+                cl.end(out + 3LL * n0 * (t.m - t0), 1, 1.0f);
             }
             if (st) st->remap_pixels += (uint64_t)tasks.size() * n0;
             run_combine(ex, g, 0, cl, bo.F, bo.fstride);
@@ -1313,8 +1319,29 @@ fb_status fb_interpolate_keyframes(fb_ctx ctx, const fb_match_cfg* cfg, int N, i
             if (key_index[k] < 0 || key_index[k] >= N || (k && key_index[k] <= key_index[k - 1]))
                 throw Fail{FB_ERR_INVALID_ARG, "key_index must be strictly increasing in [0, N)"};
         const Geo g = make_geo(*cfg, H, W);
-        interpolate(ex, *cfg, g, N, guide, K, key_index, key_style, out, st);
+        interpolate(ex, *cfg, g, N, 0, N, guide, K, key_index, nullptr, key_style, out, st);
     });
+}
+
+fb_status fb_interpolate_keyframes_range(fb_ctx ctx, const fb_match_cfg* cfg, int N, int H, int W, int t0, int t1,
+                                         const uint8_t* guide, int K, const int32_t* key_index,
+                                         const uint8_t* key_guide, const uint8_t* key_style, float* out,
+                                         fb_stats* stats, size_t* ws_needed)
+{
+    return guarded(ctx, stats, [&](Exec& ex, fb_stats* st) {
+        validate_cfg(cfg);
+        check_frames(N, H, W);
+        if (!guide || !key_index || !key_guide || !key_style || (!out && !ex.dry) || K < 1)
+            throw Fail{FB_ERR_INVALID_ARG, "NULL pointer or K < 1"};
+        if (t0 < 0 || t1 > N || t0 >= t1) throw Fail{FB_ERR_INVALID_ARG, "bad target range"};
+        for (int k = 0; k < K; ++k)
+            if (key_index[k] < 0 || key_index[k] >= N || (k && key_index[k] <= key_index[k - 1]))
+                throw Fail{FB_ERR_INVALID_ARG, "key_index must be strictly increasing in [0, N)"};
+        if (cfg->tracking && (t0 > 0 || t1 < N))
+            throw Fail{FB_ERR_UNSUPPORTED, "tracking couples every frame of a key span (D42): use the full call"};
+        const Geo g = make_geo(*cfg, H, W);
+        interpolate(ex, *cfg, g, N, t0, t1, guide, K, key_index, key_guide, key_style, out, st);
+    }, ws_needed);
 }
 
 size_t fb_workspace_size_range(fb_ctx ctx, int schedule, const fb_match_cfg* cfg, int N_total, int f0, int N, int H,
@@ -1365,7 +1392,7 @@ size_t fb_workspace_size(fb_ctx ctx, int op, const fb_match_cfg* cfg, int n, int
         s = guarded(ctx, nullptr, [&](Exec& ex, fb_stats* st) {
             validate_cfg(cfg);
             const Geo g = make_geo(*cfg, H, W);
-            interpolate(ex, *cfg, g, n, fake, (int)keys.size(), keys.data(), fake, fout, st);
+            interpolate(ex, *cfg, g, n, 0, n, fake, (int)keys.size(), keys.data(), nullptr, fake, fout, st);
         }, &need);
     } else {
         return 0;

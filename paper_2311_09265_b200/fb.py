@@ -27,7 +27,8 @@ STATUS = {0: "FB_OK", 1: "FB_ERR_INVALID_ARG", 2: "FB_ERR_SHAPE", 3: "FB_ERR_CUD
 SYMBOLS = ["fb_ctx_create", "fb_ctx_destroy", "fb_last_error", "fb_set_workspace", "fb_set_max_batch_pairs",
            "fb_workspace_size", "fb_workspace_size_range", "fb_launch_count", "fb_pyramid_elems", "fb_build_pyramid", "fb_nnf_estimate",
            "fb_remap", "fb_blend_window", "fb_blend_window_range", "fb_interpolate_keyframes", "fb_profile_enable",
-           "fb_profile_read", "fb_profile_reset", "fb_tree_cell_texels", "fb_tree_build_cells", "fb_tree_query"]
+           "fb_profile_read", "fb_profile_reset", "fb_tree_cell_texels", "fb_tree_build_cells", "fb_tree_query",
+           "fb_interpolate_keyframes_range"]
 
 
 class FBError(RuntimeError):
@@ -117,6 +118,8 @@ def load_library(build_if_missing: bool = True):
     lib.fb_blend_window_range.argtypes = [V, P(_Cfg), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                           V, V, C.c_int, C.c_int, V, P(_Stats)]
     lib.fb_interpolate_keyframes.argtypes = [V, P(_Cfg), C.c_int, C.c_int, C.c_int, V, C.c_int, V, V, V, P(_Stats)]
+    lib.fb_interpolate_keyframes_range.argtypes = [V, P(_Cfg)] + [C.c_int] * 5 + [V, C.c_int, V, V, V, V, P(_Stats),
+                                                                                P(C.c_size_t)]
     lib.fb_tree_cell_texels.argtypes = [P(_Cfg), C.c_int, C.c_int]
     lib.fb_tree_cell_texels.restype = C.c_size_t
     lib.fb_tree_build_cells.argtypes = [V, P(_Cfg)] + [C.c_int] * 5 + [V, V, C.c_int, V, V, P(_Stats), P(C.c_size_t)]
@@ -352,6 +355,29 @@ class Context:
         c = cfg.c()
         self._check(self.lib.fb_interpolate_keyframes(self.h, C.byref(c), N, H, W, _ptr(g), K, ki, _ptr(ks), _ptr(out),
                                                       C.byref(st)))
+        return out, st.as_dict()
+
+
+    def fb_interpolate_keyframes_range(self, cfg: MatchCfg, N: int, t0: int, t1: int, guide, key_index, key_guide,
+                                       key_style, out: torch.Tensor | None = None):
+        """Frames [t0, t1) of the interpolation (guide holds frames t0..t1-1; key_guide/key_style the K keys)."""
+        g = _dev(guide, self.device, torch.uint8)
+        kg = _dev(key_guide, self.device, torch.uint8)
+        ks = _dev(key_style, self.device, torch.uint8)
+        _, H, W, _ = g.shape
+        keys = [int(k) for k in key_index]
+        K = len(keys)
+        ki = (C.c_int32 * max(K, 1))(*keys)
+        c = cfg.c()
+        need = C.c_size_t(0)
+        self._check(self.lib.fb_interpolate_keyframes_range(self.h, C.byref(c), N, H, W, t0, t1, _ptr(g), K, ki, _ptr(kg),
+                                                            _ptr(ks), None, None, C.byref(need)))
+        self.ensure_workspace(int(need.value))
+        if out is None:
+            out = torch.empty((t1 - t0, H, W, 3), dtype=torch.float32, device=self.device)
+        st = _Stats()
+        self._check(self.lib.fb_interpolate_keyframes_range(self.h, C.byref(c), N, H, W, t0, t1, _ptr(g), K, ki, _ptr(kg),
+                                                            _ptr(ks), _ptr(out), C.byref(st), None))
         return out, st.as_dict()
 
 

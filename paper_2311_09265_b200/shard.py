@@ -39,7 +39,14 @@ def plan_shards(N: int, M: int, world: int, schedule: str = "direct") -> list[tu
     least one target when N >= world (ranks beyond N get empty ranges)."""
     if world <= 1:
         return [(0, N)]
-    cost = [(direct_pairs if schedule == "direct" else tree_pairs)(N, M, i) + 1 for i in range(N)]
+    return plan_by_cost([(direct_pairs if schedule == "direct" else tree_pairs)(N, M, i) + 1 for i in range(N)], world)
+
+
+def plan_by_cost(cost: list[int], world: int) -> list[tuple[int, int]]:
+    """Contiguous ranges of len(cost) items, one per rank, with near-equal cost sums."""
+    N = len(cost)
+    if world <= 1:
+        return [(0, N)]
     prefix = [0]
     for c in cost:
         prefix.append(prefix[-1] + c)
@@ -202,3 +209,48 @@ def blend_tree_exchange(ctx, cfg, plan: list[tuple[int, int]], N: int, M: int, r
     out, st_q = ctx.fb_tree_query(cfg, N, f0, guide_loc, style_loc, M, t0, t1, order, [cells[c] for c in order],
                                   out=out)
     return out, {k: st_q.get(k, 0) + st_b.get(k, 0) for k in st_q}
+
+
+# ---------------------------------------------------------------------------------------- interpolation
+# Eq. 9: every frame's NNFs read only its own guide frame and the keyframes, so the frames
+# shard with no data-path exchange beyond the keyframes themselves, which are broadcast once: the key
+# styles from the rank that holds them (rank 0), each key's guide frame from the rank owning that frame.
+
+def interp_pairs(N: int, keys: list[int], m: int) -> int:
+    """NNF pairs of frame m: 0 for a keyframe, else the number of keys on its sides (1 or 2)."""
+    if m in keys:
+        return 0
+    return int(any(k < m for k in keys)) + int(any(k > m for k in keys))
+
+
+def plan_interp_shards(N: int, keys: list[int], world: int) -> list[tuple[int, int]]:
+    return plan_by_cost([interp_pairs(N, keys, m) + 1 for m in range(N)], world)
+
+
+def broadcast_keyframes(plan: list[tuple[int, int]], keys: list[int], rank: int, guide_own: torch.Tensor,
+                        key_style: torch.Tensor | None, group=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Returns (key_guide [K,H,W,3], key_style [K,H,W,3]) on every rank: key styles broadcast from rank 0
+    (key_style is read there only), each key's guide frame from the rank owning that frame."""
+    t0, _ = plan[rank]
+    shape = tuple(guide_own.shape[1:])
+    K = len(keys)
+    kg = torch.empty((K,) + shape, dtype=guide_own.dtype, device=guide_own.device)
+    for k, f in enumerate(keys):
+        src = owner_of(plan, f)
+        if src == rank:
+            kg[k].copy_(guide_own[f - t0])
+        dist.broadcast(kg[k], src, group)
+    ks = key_style.contiguous() if rank == 0 else torch.empty((K,) + shape, dtype=guide_own.dtype,
+                                                              device=guide_own.device)
+    dist.broadcast(ks, 0, group)
+    return kg, ks
+
+
+def interpolate_sharded(ctx, cfg, plan: list[tuple[int, int]], N: int, keys: list[int], rank: int,
+                        guide_own: torch.Tensor, key_style: torch.Tensor | None, out=None, group=None):
+    """This rank's frames [t0, t1) of the keyframe interpolation (fb_interpolate_keyframes_range)."""
+    t0, t1 = plan[rank]
+    kg, ks = broadcast_keyframes(plan, keys, rank, guide_own, key_style, group)
+    if t1 <= t0:
+        return None, {}
+    return ctx.fb_interpolate_keyframes_range(cfg, N, t0, t1, guide_own, keys, kg, ks, out=out)

@@ -375,3 +375,22 @@ def test_tree_cell_exchange_matches_full_blend(fb, N, M, world):
             with pytest.raises(fb.FBError):
                 ctx.fb_tree_query(cfg, N, f0, dev(g[f0:f1]), dev(s[f0:f1]), M, t0, t1, need[1:],
                                   [pool[c] for c in need[1:]])
+
+
+@pytest.mark.parametrize("loss", ["GUIDE_STYLE", "PAIRWISE"])
+def test_interpolation_range_equals_full_call(fb, loss):
+    """Sharded interpolation: frames [t0, t1) from their own guides plus the broadcast keyframes
+    equal the full call's rows bit for bit; tracking (D42) needs the full call."""
+    from paper_2311_09265_b200 import shard
+    N, keys = 11, [0, 5, 10]
+    g, s = moving_texture(N, 36, 44, seed=21)
+    ks = s[keys]
+    cfg = fb.MatchCfg(iters_per_level=2, loss=getattr(fb, loss))
+    ctx = fb.Context(0)
+    full, _ = ctx.fb_interpolate_keyframes(cfg, dev(g), keys, dev(ks))
+    for t0, t1 in shard.plan_interp_shards(N, keys, 3) + [(2, 3), (5, 6)]:
+        part, _ = ctx.fb_interpolate_keyframes_range(cfg, N, t0, t1, dev(g[t0:t1]), keys, dev(g[keys]), dev(ks))
+        assert torch.equal(part, full[t0:t1])
+    cfg_t = fb.MatchCfg(iters_per_level=2, loss=fb.GUIDE_STYLE, tracking=1)
+    with pytest.raises(fb.FBError):
+        ctx.fb_interpolate_keyframes_range(cfg_t, N, 0, 4, dev(g[0:4]), keys, dev(g[keys]), dev(ks))

@@ -153,3 +153,47 @@ def test_tree_cell_exchange_gloo(world, N, M):
     res = dict(q.get(timeout=5) for _ in range(world))
     assert all(p.exitcode == 0 for p in procs)
     assert all(res[r] for r in range(world)), res
+
+
+# ------------------------------------------------------------------------------ interpolation sharding
+@pytest.mark.parametrize("N,keys,world", [(102, [0, 101], 8), (10, [0, 4, 9], 3), (7, [3], 2), (5, [0, 4], 8)])
+def test_interp_plan_covers_and_balances(N, keys, world):
+    plan = shard.plan_interp_shards(N, keys, world)
+    assert plan[0][0] == 0 and plan[-1][1] == N
+    for (a, b), (c, d) in zip(plan, plan[1:]):
+        assert b == c and a <= b
+    if N >= 8 * world:
+        costs = [sum(shard.interp_pairs(N, keys, m) + 1 for m in range(a, b)) for a, b in plan]
+        assert min(costs) / max(costs) >= 0.85, costs
+
+
+def _interp_worker(rank, world, port, N, keys, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(9)
+        full_g = torch.from_numpy(rng.integers(0, 256, size=(N, 4, 5, 3), dtype=np.uint8))
+        full_ks = torch.from_numpy(rng.integers(0, 256, size=(len(keys), 4, 5, 3), dtype=np.uint8))
+        plan = shard.plan_interp_shards(N, keys, world)
+        t0, t1 = plan[rank]
+        kg, ks = shard.broadcast_keyframes(plan, keys, rank, full_g[t0:t1].clone(),
+                                           full_ks.clone() if rank == 0 else None)
+        ok = torch.equal(kg, full_g[keys]) and torch.equal(ks, full_ks)
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,N,keys", [(2, 12, [0, 11]), (3, 15, [0, 7, 14])])
+def test_keyframe_broadcast_gloo(world, N, keys):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_interp_worker, args=(r, world, port, N, keys, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    res = dict(q.get(timeout=5) for _ in range(world))
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(res[r] for r in range(world)), res
