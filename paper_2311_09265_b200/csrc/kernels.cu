@@ -440,6 +440,8 @@ __global__ void k_remap_f3(const float* __restrict__ src, const int2* __restrict
 // checks after rows 1 and 3 (profiles/r01_pde_tuning.txt).
 #define PDE_FAST_S1(P) 1
 #define PDE_FAST_S2(P) (2 * (P) + 1)
+#define PDE_I13_S2(P) ((P) == 2 ? 3 : 2 * (P) + 1)  // fused fields 1-3 with the hybrid target: second check
+                                                     // before the shared-memory rows (N=48: 397 -> 387 ms)
 #define PDE_GEN_S1(P) 1
 #define PDE_GEN_S2(P) 3
 __device__ __forceinline__ float partial_loss(float alpha, float dg, float ds, bool two)
@@ -907,7 +909,7 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? 4 : 3) k_iter13_
     auto loss = [&](int sr, int sc, float bound) -> float {
         uint32_t dg = 0u;
         float ds = 0.0f;
-        constexpr int S1 = PDE_FAST_S1(P), S2 = PDE_FAST_S2(P);
+        constexpr int S1 = PDE_FAST_S1(P), S2 = PDE_I13_S2(P);
 #pragma unroll
         for (int dr = 0; dr < S1; ++dr) row(sr, sc, dr, dg, ds);
         if (partial_loss(a.alpha, __uint2float_rn(dg), ds, TWO) >= bound) return __int_as_float(0x7f800000);
