@@ -1,6 +1,6 @@
 """Summarise an ncu report (or a launch-list CSV) into the plain-text files kept under profiles/.
 
-    python tools/ncu_summary.py full  <report.ncu-rep> <out.txt> [evals_per_launch]
+    python tools/ncu_summary.py full  <report.ncu-rep | raw.csv> <out.txt> [evals_per_launch]
     python tools/ncu_summary.py list  <launches.csv>   <out.txt>
 """
 import csv
@@ -18,7 +18,8 @@ KEYS = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elap
         "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "sm__inst_executed.sum",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
-        "launch__occupancy_limit_registers", "sm__cycles_elapsed.avg.per_second"]
+        "launch__occupancy_limit_registers", "sm__cycles_elapsed.avg.per_second",
+        "smsp__thread_inst_executed_per_inst_executed.ratio"]
 
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
@@ -28,7 +29,10 @@ def _num(s):
 
 
 def full(rep, out, evals=None):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # `ncu -i <rep> --page raw --csv` already exported on the GPU box
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     lines = [f"ncu --set full summary of {rep}"]
