@@ -629,7 +629,6 @@ void blend_direct(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int N_total, 
 // Alg. 3 (remapping table), Alg. 4 (blending table), Alg. 5 (query) on the forward and the reversed
 // frame order (D26), merged by Eq. 6.  Tables hold means (D25); levels capped at floor(log2(M+1))
 // (D24); only the cells the requested targets' queries visit are built (the "task manager").
-int floor_log2(int x) { int l = 0; while ((2 << l) <= x) ++l; return l; }
 
 std::vector<std::pair<int, int>> query_nodes(int l, int r)  // Alg. 5 with i <- i - 2^L (D23)
 {
