@@ -18,6 +18,19 @@ static constexpr int TILE_X = 32, TILE_Y = 8;  // 256-thread 2D tiles: a warp is
 static constexpr int FAST_TY = 4;              // fast kernel: 128-thread tiles, 3 CTAs/SM at <= 168 regs
 static constexpr int B = kBorder;
 
+// Debug bounds checks (build with -DFB_DEBUG_BOUNDS: tools/build_variant.sh dbg -DFB_DEBUG_BOUNDS): every
+// gather's texel range is checked against its padded level block and a violation traps the kernel (the
+// launch then fails with an error instead of reading a neighbour's data).  No-ops in the product build.
+#ifdef FB_DEBUG_BOUNDS
+#define FB_ASSERT(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define FB_ASSERT(cond) do { } while (0)
+#endif
+// a patch row of D texels starting at padded texel idx (rounded down to even, NCH texel pairs) lies in
+// the level block and in the row band the zero border provides
+#define FB_ROW_OK(idx, L, D) ((idx) >= 0 && ((idx) & ~1) + 2 * (((D) + 2) / 2) <= (L).rows * (L).pitch && \
+                              (idx) / (L).pitch >= 0 && (idx) / (L).pitch < (L).rows)
+
 // ------------------------------------------------------------------------------------ Philox4x32-10
 // Salmon et al. (SC'11).  Counter layout of D21: c0 = pixel, c1 = purpose<<28 | level<<22 | iter<<12 |
 // step, c2 = source frame id, c3 = tag<<28 | target frame id.
@@ -273,6 +286,7 @@ __device__ __forceinline__ float3 remap_px_slot(const char* __restrict__ slot, i
             const int sr = f.x - dr, sc = f.y - dc;
             const bool v = rin && (unsigned)tc < (unsigned)w && (unsigned)sr < (unsigned)h && (unsigned)sc < (unsigned)w;
             const int idx = (sr + kBorder) * pitch + sc + kBorder;
+            FB_ASSERT(sr >= -kBorder && sc >= -kBorder && sr < h + kBorder && sc < w + kBorder);
             if (SFMT == SF8) {
                 uint32_t sv = __ldg(reinterpret_cast<const uint32_t*>(slot) + 2 * idx + 1);
                 sv = v ? sv : 0u;
@@ -457,6 +471,7 @@ __device__ __forceinline__ void load_pairwise_patch(const DTask& T, const FieldA
                                                     float (&pa)[2 * P + 1][2 * P + 1][3])
 {
     const int2 q = __ldg(&T.pF[i]);
+    FB_ASSERT((unsigned)q.x < (unsigned)a.L.h && (unsigned)q.y < (unsigned)a.L.w);
     const uint32_t* PS = reinterpret_cast<const uint32_t*>(T.psrc + a.src_off);
 #pragma unroll
     for (int dr = 0; dr < 2 * P + 1; ++dr)
@@ -505,6 +520,7 @@ __global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
     // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
     auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
         const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
+        FB_ASSERT((unsigned)sr < (unsigned)h && (unsigned)sc < (unsigned)w && FB_ROW_OK(idx, a.L, D));
         if (SFL == 1) {  // SF8F float style (blending-table cells): one 16-byte texel per tap
             const uint4* tp = reinterpret_cast<const uint4*>(S) + idx;
             float rs = 0.0f;
@@ -608,6 +624,7 @@ __global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
             }
         }
     }
+    FB_ASSERT((unsigned)f.x < (unsigned)h && (unsigned)f.y < (unsigned)w);
     a.Fout[t * a.fstride + i] = f;
     a.E[t * a.fstride + i] = e;
 }
@@ -661,6 +678,7 @@ __global__ void __launch_bounds__(32 * (IT_TY + 1), IT_MINB) k_iter_fast(FieldAr
     // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
     auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
         const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
+        FB_ASSERT((unsigned)sr < (unsigned)h && (unsigned)sc < (unsigned)w && FB_ROW_OK(idx, a.L, D));
         if (SFL == 1) {  // SF8F float style (blending-table cells): one 16-byte texel per tap
             const uint4* tp = reinterpret_cast<const uint4*>(S) + idx;
             float rs = 0.0f;
@@ -783,6 +801,7 @@ __global__ void __launch_bounds__(32 * (IT_TY + 1), IT_MINB) k_iter_fast(FieldAr
         const int ox = (int)__umulhi(u.x, span) - R, oy = (int)__umulhi(u.y, span) - R;
         select(f, e, clampi(f.x + ox, 0, h - 1), clampi(f.y + oy, 0, w - 1));
     }
+    FB_ASSERT((unsigned)f.x < (unsigned)h && (unsigned)f.y < (unsigned)w);
     a.Fout[t * a.fstride + i] = f;
     a.E[t * a.fstride + i] = e;
 }
@@ -855,6 +874,7 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? 4 : 3) k_iter13_
     // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
     auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
         const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
+        FB_ASSERT((unsigned)sr < (unsigned)h && (unsigned)sc < (unsigned)w && FB_ROW_OK(idx, a.L, D));
         if (SFL == 1) {  // SF8F float style (blending-table cells): one 16-byte texel per tap
             const uint4* tp = reinterpret_cast<const uint4*>(S) + idx;
             float rs = 0.0f;
@@ -973,6 +993,7 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? 4 : 3) k_iter13_
         const int ox = (int)__umulhi(u.x, span) - R, oy = (int)__umulhi(u.y, span) - R;
         select(f, e, clampi(f.x + ox, 0, h - 1), clampi(f.y + oy, 0, w - 1));
     }
+    FB_ASSERT((unsigned)f.x < (unsigned)h && (unsigned)f.y < (unsigned)w);
     a.Fout[t * a.fstride + i] = f;
     if (a.Eout) a.Eout[t * a.fstride + i] = e;  // never a.E: halo lanes of other tiles read it
 }
@@ -1007,6 +1028,7 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_mid(FieldArgs a)
     const int plane = a.L.rows * pitch;
     auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
         const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
+        FB_ASSERT((unsigned)sr < (unsigned)h && (unsigned)sc < (unsigned)w && FB_ROW_OK(idx, a.L, D));
         const uint4* cp = reinterpret_cast<const uint4*>(
             S + (kSF8Copies == 2 ? (size_t)(idx & 1) * plane + (idx & ~1) : (size_t)(idx & ~1)));
         const int o = kSF8Copies == 2 ? 0 : (idx & 1);
@@ -1082,6 +1104,7 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_mid(FieldArgs a)
             select(f, e, clampi(f.x + ox, 0, h - 1), clampi(f.y + oy, 0, w - 1));
         }
     }
+    FB_ASSERT((unsigned)f.x < (unsigned)h && (unsigned)f.y < (unsigned)w);
     a.Fout[t * a.fstride + i] = f;
     a.E[t * a.fstride + i] = e;
 }
@@ -1128,6 +1151,7 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
 #pragma unroll
             for (int dc = 0; dc < D; ++dc) {
                 const int idx = (q.x + dr - P + B) * pitch + (q.y + dc - P + B);
+                FB_ASSERT((unsigned)q.x < (unsigned)h && (unsigned)q.y < (unsigned)w);
                 if (SFMT == SF10) {
                     const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(T.psrc + a.src_off) + 2 * idx + 1);
                     pa[PW ? dr : 0][PW ? dc : 0][0] = f10_0(v);
@@ -1149,6 +1173,7 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
     }
     auto row = [&](int sr, int sc, int dr, float& dg, float& ds) {
         const int base = (sr + dr - P + B) * pitch + (sc - P + B);
+        FB_ASSERT((unsigned)sr < (unsigned)h && (unsigned)sc < (unsigned)w && FB_ROW_OK(base, a.L, D));
         float rg = 0.0f, rs = 0.0f;
         // SF10: the row's texel pairs from the copy in which it starts 16-byte aligned (as SF8)
         constexpr int NCH = (D + 2) / 2;
@@ -1256,6 +1281,7 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
             }
         }
     }
+    FB_ASSERT((unsigned)f.x < (unsigned)h && (unsigned)f.y < (unsigned)w);
     a.Fout[t * a.fstride + i] = f;
     a.E[t * a.fstride + i] = e;
 }
