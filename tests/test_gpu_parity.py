@@ -394,3 +394,16 @@ def test_interpolation_range_equals_full_call(fb, loss):
     cfg_t = fb.MatchCfg(iters_per_level=2, loss=fb.GUIDE_STYLE, tracking=1)
     with pytest.raises(fb.FBError):
         ctx.fb_interpolate_keyframes_range(cfg_t, N, 0, 4, dev(g[0:4]), keys, dev(g[keys]), dev(ks))
+
+
+def test_context_on_a_side_stream(fb):
+    """Results do not depend on the stream the context enqueues on (stream choice invariance)."""
+    g, s = moving_texture(6, 48, 40, seed=8)
+    cfg = fb.MatchCfg(iters_per_level=2, loss=fb.MEAN_ALIGN)
+    ref, _ = fb.Context(0).fb_blend_window(cfg, fb.DIRECT, dev(g), dev(s), 2)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        c = fb.Context(0, stream=side)
+        out, _ = c.fb_blend_window(cfg, fb.DIRECT, dev(g), dev(s), 2)
+    side.synchronize()
+    assert torch.equal(out, ref)
