@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/fb.h"
 #include "kernels.h"
 
@@ -102,6 +104,20 @@ struct Arena {
         peak = std::max(peak, off);
         return p;
     }
+};
+
+// NVTX range for profilers (nsys / ncu --nvtx): schedule phases, pyramid levels and iterations.  The
+// calls are no-ops unless a tool is attached; dry (planning) runs emit nothing.
+struct Nvtx {
+    bool on;
+    Nvtx(bool dry, const char* fmt, int a = 0, int b = 0) : on(!dry)
+    {
+        if (!on) return;
+        char buf[64];
+        snprintf(buf, sizeof buf, fmt, a, b);
+        nvtxRangePushA(buf);
+    }
+    ~Nvtx() { if (on) nvtxRangePop(); }
 };
 
 struct Exec {
@@ -415,7 +431,9 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
     }
     const fbk::Rng rng{(uint32_t)(cfg.seed & 0xFFFFFFFFu), (uint32_t)(cfg.seed >> 32)};
     int cur = 0;
+    Nvtx nv_nnf(ex.dry, "nnf batch (%d pairs)", T);
     for (int k = g.Lv - 1; k >= 0; --k) {
+        Nvtx nv_level(ex.dry, "level %d", k);
         const Lvl L = g.L[k];
         const fbk::PLvl PL = g.PL[k];
         const bool tf16 = k == 0 && fast0;
@@ -433,6 +451,7 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
             ex.launch("pack_tgt", [&] { return fbk::launch_pack_tgt_guide(d_tasks, T, L, PL, tfmt, s); });
         const int rk = rs_count(cfg, L), r0 = rs_r0(cfg, L);
         for (int it = 0; it < cfg.iters_per_level; ++it) {
+            Nvtx nv_iter(ex.dry, "iteration %d", it);
             if (Fsnap)  // freeze counterpart / tracking NNFs for this iteration (D39, D42)
                 ex.d2d(Fsnap, F[cur], sizeof(int2) * (size_t)T * n0);
             if (cfg.loss == FB_LOSS_GUIDE_STYLE) {  // S^ refresh (D17/D18)
@@ -583,6 +602,7 @@ void blend_direct(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int N_total, 
     const auto batches = make_batches(cost, batch_pairs(ex.ctx, g, cfg.loss));
     const size_t mark = ex.ar.off;
     for (auto [b0, b1] : batches) {
+        Nvtx nv(ex.dry, "direct batch targets [%d, %d)", t0 + b0, t0 + b1);
         ex.ar.off = mark;
         // frames this batch reads (original ids), then their local (input) and batch indices
         const int lo_b = std::max(0, t0 + b0 - M), hi_b = std::min(N_total - 1, t0 + b1 - 1 + M);
@@ -652,6 +672,7 @@ using CellMap = std::map<std::pair<int, int>, const float4*>;
 CellMap tree_build(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int N_total, int f0, const Pyr& G, const Pyr& S,
                    const Slots& FR, int o, const std::vector<int>& top, fb_stats* st)
 {
+    Nvtx nv(ex.dry, "tree build (orientation %d)", o);
     const long long n0 = g.npx0();
     auto orig = [&](int v) { return o == 0 ? v : N_total - 1 - v; };
     const uint32_t tag_build = o == 0 ? 1u : 3u;
@@ -718,6 +739,7 @@ CellMap tree_build(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int N_total,
 void tree_query(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int N_total, int f0, int M, const Pyr& G,
                 const Pyr& S, int o, int t0, int t1, const CellMap& cells, float4* A, fb_stats* st)
 {
+    Nvtx nv(ex.dry, "tree queries (orientation %d)", o);
     const long long n0 = g.npx0();
     auto orig = [&](int v) { return o == 0 ? v : N_total - 1 - v; };
     const uint32_t tag_query = o == 0 ? 2u : 4u;
@@ -908,6 +930,7 @@ void interpolate(Exec& ex, const fb_match_cfg& cfg0, const Geo& g, int N, int t0
     }
     const size_t mark = ex.ar.off;
     for (int pass = 0; pass < 2; ++pass) {
+        Nvtx nv(ex.dry, "interpolation pass %d", pass);
         fb_match_cfg cfg = cfg0;
         cfg.loss = pass == 1 ? FB_LOSS_PAIRWISE : FB_LOSS_GUIDE_STYLE;
         std::vector<int> cost;

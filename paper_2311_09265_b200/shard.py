@@ -9,8 +9,23 @@ Pair-keyed RNG (D21) makes the result identical for every world size.
 """
 from __future__ import annotations
 
+import contextlib
+
 import torch
 import torch.distributed as dist
+
+
+@contextlib.contextmanager
+def _nvtx(name: str):
+    """NVTX range around an exchange step (no-op without CUDA, e.g. in the gloo CPU tests)."""
+    if torch.cuda.is_available():
+        torch.cuda.nvtx.range_push(name)
+        try:
+            yield
+        finally:
+            torch.cuda.nvtx.range_pop()
+    else:
+        yield
 
 
 def direct_pairs(N: int, M: int, i: int) -> int:
@@ -110,8 +125,9 @@ def halo_exchange(owned: list[torch.Tensor], plan: list[tuple[int, int]], N: int
             for x in owned:
                 ops.append(dist.P2POp(dist.isend, x[lo - t0:hi - t0].contiguous(), g, group))
     if ops:
-        for r in dist.batch_isend_irecv(ops):
-            r.wait()
+        with _nvtx("halo exchange"):
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
     return locals_, f0
 
 
@@ -175,8 +191,9 @@ def exchange_cells(plan: list[tuple[int, int]], N: int, M: int, rank: int, built
             ops.append(dist.P2POp(dist.irecv, buf, g, group))
             recv[g] = (from_g, buf)
     if ops:
-        for r in dist.batch_isend_irecv(ops):
-            r.wait()
+        with _nvtx("tree cell exchange"):
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
     cells = {c: built[c] for c in mine if owner[c] == rank}
     for from_g, buf in recv.values():
         for k, c in enumerate(from_g):
@@ -231,6 +248,11 @@ def broadcast_keyframes(plan: list[tuple[int, int]], keys: list[int], rank: int,
                         key_style: torch.Tensor | None, group=None) -> tuple[torch.Tensor, torch.Tensor]:
     """Returns (key_guide [K,H,W,3], key_style [K,H,W,3]) on every rank: key styles broadcast from rank 0
     (key_style is read there only), each key's guide frame from the rank owning that frame."""
+    with _nvtx("keyframe broadcast"):
+        return _broadcast_keyframes(plan, keys, rank, guide_own, key_style, group)
+
+
+def _broadcast_keyframes(plan, keys, rank, guide_own, key_style, group):
     t0, _ = plan[rank]
     shape = tuple(guide_own.shape[1:])
     K = len(keys)
