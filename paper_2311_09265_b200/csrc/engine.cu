@@ -33,6 +33,8 @@ struct fb_ctx_s {
     uint64_t launches = 0;
     bool fused = false;  // fused iteration kernel on the fast path (FB_FUSED=1; measured slower)
     bool fuse13 = true;  // fields 1-3 + random search fused on the fast path (FB_FUSE13=0 disables)
+    bool phase0_mid = true;  // E init + field 0 at level 0 through the shared-memory-target kernel (FB_P0MID=0:
+                             // register target; 44 vs 163 registers: field0.L0 95 -> 76 ms at N=48)
     int tgt_reg_rows = 2;  // fused fields 1-3: target rows in registers, rest in shared memory (FB_HYROWS;
                            // 0 = all in registers; accurate N=48: field123.L0 413 -> 397 ms)
     std::string err;
@@ -490,7 +492,9 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
                 const bool last = j == 0;
                 if (last && fast && ex.ctx->fuse13) {  // field 0, then fields 1-3 + random search in one launch
                     a.Fin = F[cur]; a.Fout = F[cur ^ 1];
-                    ex.launch(names[0], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, 0, kind, s); },
+                    const int kind0 = (ex.ctx->phase0_mid && !pairwise && g.p == 2 &&
+                                       (a.src_fmt == fbk::SF8 || a.src_fmt == fbk::SF8F)) ? 2 : kind;
+                    ex.launch(names[0], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, 0, kind0, s); },
                               (1ull + (uint64_t)a.einit) * T * L.h * L.w);
                     cur ^= 1;
                     char nm[32];
@@ -1111,6 +1115,8 @@ fb_status fb_ctx_create(int device, void* cuda_stream, fb_ctx* out)
     if (fused && fused[0] == '1') c->fused = true;
     const char* f13 = getenv("FB_FUSE13");
     if (f13 && f13[0] == '0') c->fuse13 = false;
+    const char* p0 = getenv("FB_P0MID");
+    if (p0) c->phase0_mid = p0[0] == '1';
     const char* hy = getenv("FB_HYROWS");
     if (hy) c->tgt_reg_rows = atoi(hy);
     const char* sf10 = getenv("FB_SF10");

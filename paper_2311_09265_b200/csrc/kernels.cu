@@ -1001,7 +1001,7 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? 4 : 3) k_iter13_
 // ---- level-0 variant for p = 3, 4: SF8 source, TF16 target tile in shared memory -----------------
 // The target patch of p >= 3 does not fit in registers, so it is staged per tile; the source rows and the
 // exact integer guide term (every partial < 2^24 for p <= 4 at level 0) are those of k_field_fast.
-template <int P, bool TWO, int PHASE>
+template <int P, bool TWO, int PHASE, int SFL = 0>
 __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_mid(FieldArgs a)
 {
     constexpr int D = 2 * P + 1, SX = TILE_X + 2 * P, SY = TILE_Y + 2 * P;
@@ -1029,6 +1029,24 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_mid(FieldArgs a)
     auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
         const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
         FB_ASSERT((unsigned)sr < (unsigned)h && (unsigned)sc < (unsigned)w && FB_ROW_OK(idx, a.L, D));
+        if (SFL == 1) {  // SF8F float style (blending-table cells): one 16-byte texel per tap
+            const uint4* tp = reinterpret_cast<const uint4*>(T.src + a.src_off) + idx;
+            float rs = 0.0f;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const uint4 v = __ldg(tp + j);
+                const uint4 tv = tT[ly + dr][lx + j];
+                const uint32_t d = __vabsdiffu4(v.x, tv.x);
+                dg = __dp4a(d, d, dg);
+                if (TWO) {
+                    float dl = __fsub_rn(__uint_as_float(tv.y), __uint_as_float(v.y)); rs = __fmaf_rn(dl, dl, rs);
+                    dl = __fsub_rn(__uint_as_float(tv.z), __uint_as_float(v.z)); rs = __fmaf_rn(dl, dl, rs);
+                    dl = __fsub_rn(__uint_as_float(tv.w), __uint_as_float(v.w)); rs = __fmaf_rn(dl, dl, rs);
+                }
+            }
+            if (TWO) ds = __fadd_rn(ds, rs);
+            return;
+        }
         const uint4* cp = reinterpret_cast<const uint4*>(
             S + (kSF8Copies == 2 ? (size_t)(idx & 1) * plane + (idx & ~1) : (size_t)(idx & ~1)));
         const int o = kSF8Copies == 2 ? 0 : (idx & 1);
@@ -1462,15 +1480,15 @@ cudaError_t launch_iter13_fast(const FieldArgs& a0, int T, int p, int loss, cuda
     return cudaGetLastError();
 }
 
-template <int P, bool TWO>
+template <int P, bool TWO, int SFL = 0>
 static void launch_field_mid(const FieldArgs& a, int T, int phase, cudaStream_t s)
 {
     const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(TILE_X * TILE_Y);
     switch (phase) {
-    case 0: k_field_mid<P, TWO, 0><<<grid, block, 0, s>>>(a); break;
-    case 1: k_field_mid<P, TWO, 1><<<grid, block, 0, s>>>(a); break;
-    case 2: k_field_mid<P, TWO, 2><<<grid, block, 0, s>>>(a); break;
-    default: k_field_mid<P, TWO, 3><<<grid, block, 0, s>>>(a); break;
+    case 0: k_field_mid<P, TWO, 0, SFL><<<grid, block, 0, s>>>(a); break;
+    case 1: k_field_mid<P, TWO, 1, SFL><<<grid, block, 0, s>>>(a); break;
+    case 2: k_field_mid<P, TWO, 2, SFL><<<grid, block, 0, s>>>(a); break;
+    default: k_field_mid<P, TWO, 3, SFL><<<grid, block, 0, s>>>(a); break;
     }
 }
 
@@ -1481,9 +1499,16 @@ cudaError_t launch_field(const FieldArgs& a0, int T, int p, int loss, int phase,
     a.tiles_x = (a.L.w + TILE_X - 1) / TILE_X;
     a.tiles_per_task = a.tiles_x * ((a.L.h + (fast ? FAST_TY : TILE_Y) - 1) / (fast ? FAST_TY : TILE_Y));
     const bool pw = loss == 3;
-    if (kind == 2) {  // level 0, p = 3, 4: SF8 source, TF16 target tile (not PAIRWISE)
-        if (pw || a.src_fmt != SF8) return cudaErrorInvalidValue;
-        if (p == 3) { if (loss) launch_field_mid<3, true>(a, T, phase, s); else launch_field_mid<3, false>(a, T, phase, s); }
+    if (kind == 2) {  // level 0: SF8 (or, p = 2, SF8F) source, TF16 target tile (not PAIRWISE)
+        if (pw) return cudaErrorInvalidValue;
+        if (a.src_fmt == SF8F) {
+            if (p != 2 || !loss) return cudaErrorInvalidValue;
+            launch_field_mid<2, true, 1>(a, T, phase, s);
+            return cudaGetLastError();
+        }
+        if (a.src_fmt != SF8) return cudaErrorInvalidValue;
+        if (p == 2) { if (loss) launch_field_mid<2, true>(a, T, phase, s); else launch_field_mid<2, false>(a, T, phase, s); }
+        else if (p == 3) { if (loss) launch_field_mid<3, true>(a, T, phase, s); else launch_field_mid<3, false>(a, T, phase, s); }
         else if (p == 4) { if (loss) launch_field_mid<4, true>(a, T, phase, s); else launch_field_mid<4, false>(a, T, phase, s); }
         else return cudaErrorInvalidValue;
         return cudaGetLastError();
