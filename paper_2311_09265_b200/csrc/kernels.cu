@@ -818,7 +818,10 @@ static constexpr int I13_TY = 4;
 // read by every candidate, rows >= 1 only by candidates that survive row 0 -- and the rest is read from a
 // shared-memory copy of the CTA's target tile.  Registers drop from 168 to <= 128: 4 CTAs/SM instead of 3.
 template <int P, bool TWO, bool PW = false, int SFL = 0, int NR = 2 * P + 1>
-__global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? 4 : 3) k_iter13_fast(FieldArgs a)
+#ifndef I13_HY_MINB
+#define I13_HY_MINB 5  // 96 registers, no spills: 5 CTAs/SM (N=48: 388 -> 357 ms; 6 and 7 spill and lose)
+#endif
+__global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? I13_HY_MINB : 3) k_iter13_fast(FieldArgs a)
 {
     constexpr int D = 2 * P + 1;
     constexpr bool HY = NR < D;
