@@ -322,8 +322,11 @@ __device__ __forceinline__ float3 remap_px_slot(const char* __restrict__ slot, i
 // S^ refresh (GUIDE_STYLE, D17/D18): packed target = {G_tgt, remap(S_src, F)} over the padded grid.
 // SFMT = SF8 / SF16 reads the source style from the task's packed slot (exact integer form above); -1
 // reads the float4 style pyramid (float-style sources such as blending-table cells).
+#ifndef AUX_MINB
+#define AUX_MINB 5  // p = 2: 48 registers (balanced N=48: aux 62.5 -> 60.1 ms; 8 CTAs spill and lose)
+#endif
 template <int P, int SFMT>
-__global__ void k_aux_remap(const DTask* __restrict__ tasks, const int2* __restrict__ F, long long fstride, Lvl L,
+__global__ void __launch_bounds__(256, P == 2 ? AUX_MINB : 1) k_aux_remap(const DTask* __restrict__ tasks, const int2* __restrict__ F, long long fstride, Lvl L,
                             PLvl PL, int tfmt, long long src_off)
 {
     const int t = blockIdx.y;
@@ -1005,7 +1008,10 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? I13_HY_MINB : 3)
 // The target patch of p >= 3 does not fit in registers, so it is staged per tile; the source rows and the
 // exact integer guide term (every partial < 2^24 for p <= 4 at level 0) are those of k_field_fast.
 template <int P, bool TWO, int PHASE, int SFL = 0>
-__global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_mid(FieldArgs a)
+#ifndef MID_MINB
+#define MID_MINB 8  // p = 2 (phase 0): 8 CTAs/SM at 32 registers beats 5 at 44 (balanced N=48: 68 -> 62 ms)
+#endif
+__global__ void __launch_bounds__(TILE_X* TILE_Y, P == 2 ? MID_MINB : 1) k_field_mid(FieldArgs a)
 {
     constexpr int D = 2 * P + 1, SX = TILE_X + 2 * P, SY = TILE_Y + 2 * P;
     constexpr int NCH = (D + 2) / 2;  // 16-byte chunks covering D texels from an even start
