@@ -268,13 +268,15 @@ __device__ __forceinline__ float3 remap_px(const float4* __restrict__ S, const i
 // (float)sum(n) * 4^-k; the sums are kept in integers (SF8: r|b and g in 16-bit lanes) and the one IEEE
 // division by the valid count is unchanged.  Branch-free: the zero border (>= P texels) makes every tap
 // address valid (F is in bounds, so F - d lies within P of the image), and invalid taps are masked to 0.
-template <int P, int SFMT>
+// RU: patch rows unrolled (and their loads hoisted) at once: all for the single-member S^ refresh, one in
+// the many-member combine, where hoisting every row's loads spills at the register cap (tbar.L0 44 -> 41 ms).
+template <int P, int SFMT, int RU = 2 * P + 1>
 __device__ __forceinline__ float3 remap_px_slot(const char* __restrict__ slot, int pitch, const int2* __restrict__ F,
                                                 int h, int w, int r, int c, int k)
 {
     uint32_t a0 = 0u, a1 = 0u, a2 = 0u;
     int n = 0;
-#pragma unroll
+#pragma unroll RU
     for (int dr = -P; dr <= P; ++dr) {
         const int tr = r + dr;
         const bool rin = (unsigned)tr < (unsigned)h;
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(256, P == 2 ? AUX_MINB : 1) k_aux_remap(const 
 #define COMBINE_MINB 5
 #endif
 template <int P, int FMT>
-__global__ void __launch_bounds__(256, COMBINE_MINB) k_combine(const DOut* __restrict__ outs, const DMember* __restrict__ mem, const int2* __restrict__ F,
+__global__ void __launch_bounds__(256, P <= 2 ? COMBINE_MINB : 1) k_combine(const DOut* __restrict__ outs, const DMember* __restrict__ mem, const int2* __restrict__ F,
                           long long fstride, int h, int w, PLvl PL)
 {
     const DOut o = outs[blockIdx.y];
@@ -378,11 +380,11 @@ __global__ void __launch_bounds__(256, COMBINE_MINB) k_combine(const DOut* __res
                     y = make_float3(v.x, v.y, v.z);
                 } else {
                     if (mb.sfmt == SF8)
-                        y = remap_px_slot<P, SF8>(mb.slot, PL.pitch, F + mb.task * fstride, h, w, r, c, 0);
+                        y = remap_px_slot<P, SF8, 1>(mb.slot, PL.pitch, F + mb.task * fstride, h, w, r, c, 0);
                     else if (mb.sfmt == SF10)
-                        y = remap_px_slot<P, SF10>(mb.slot, PL.pitch, F + mb.task * fstride, h, w, r, c, PL.k);
+                        y = remap_px_slot<P, SF10, 1>(mb.slot, PL.pitch, F + mb.task * fstride, h, w, r, c, PL.k);
                     else if (mb.sfmt == SF16)
-                        y = remap_px_slot<P, SF16>(mb.slot, PL.pitch, F + mb.task * fstride, h, w, r, c, PL.k);
+                        y = remap_px_slot<P, SF16, 1>(mb.slot, PL.pitch, F + mb.task * fstride, h, w, r, c, PL.k);
                     else
                         y = remap_px<P>(mb.img, F + mb.task * fstride, h, w, r, c);
                 }
