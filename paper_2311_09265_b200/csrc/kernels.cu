@@ -827,7 +827,10 @@ template <int P, bool TWO, bool PW = false, int SFL = 0, int NR = 2 * P + 1>
 #ifndef I13_HY_MINB
 #define I13_HY_MINB 5  // 96 registers, no spills: 5 CTAs/SM (N=48: 388 -> 357 ms; 6 and 7 spill and lose)
 #endif
-__global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? I13_HY_MINB : 3) k_iter13_fast(FieldArgs a)
+#ifndef I13_SFL_MINB
+#define I13_SFL_MINB 4  // SF8F (16-byte texel) queries spill at 5 CTAs/SM: fast N=48 field123.L0 126 -> 124 ms
+#endif
+__global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (SFL ? I13_SFL_MINB : I13_HY_MINB) : 3) k_iter13_fast(FieldArgs a)
 {
     constexpr int D = 2 * P + 1;
     constexpr bool HY = NR < D;
