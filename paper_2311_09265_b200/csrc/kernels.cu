@@ -325,11 +325,17 @@ __device__ __forceinline__ float3 remap_px_slot(const char* __restrict__ slot, i
 // S^ refresh (GUIDE_STYLE, D17/D18): packed target = {G_tgt, remap(S_src, F)} over the padded grid.
 // SFMT = SF8 / SF16 reads the source style from the task's packed slot (exact integer form above); -1
 // reads the float4 style pyramid (float-style sources such as blending-table cells).
+#ifndef AUX_RU1
+#define AUX_RU1 1    // p >= 3: remap one patch row at a time (config-5 shard: aux 204 ms -> < 120 ms)
+#endif
+#ifndef AUX3_MINB
+#define AUX3_MINB 1
+#endif
 #ifndef AUX_MINB
 #define AUX_MINB 5  // p = 2: 48 registers (balanced N=48: aux 62.5 -> 60.1 ms; 8 CTAs spill and lose)
 #endif
 template <int P, int SFMT>
-__global__ void __launch_bounds__(256, P == 2 ? AUX_MINB : 1) k_aux_remap(const DTask* __restrict__ tasks, const int2* __restrict__ F, long long fstride, Lvl L,
+__global__ void __launch_bounds__(256, P == 2 ? AUX_MINB : AUX3_MINB) k_aux_remap(const DTask* __restrict__ tasks, const int2* __restrict__ F, long long fstride, Lvl L,
                             PLvl PL, int tfmt, long long src_off)
 {
     const int t = blockIdx.y;
@@ -345,7 +351,7 @@ __global__ void __launch_bounds__(256, P == 2 ? AUX_MINB : 1) k_aux_remap(const 
         float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
         if (in) {
             if (SFMT == SF8 || SFMT == SF10 || SFMT == SF16)
-                v = remap_px_slot<P, SFMT>(slot, PL.pitch, Ft, L.h, L.w, r, c, PL.k);
+                v = remap_px_slot<P, SFMT, (P <= 2 || !AUX_RU1) ? 2 * P + 1 : 1>(slot, PL.pitch, Ft, L.h, L.w, r, c, PL.k);
             else v = remap_px<P>(S, Ft, L.h, L.w, r, c);
             g = __ldg(&T.tg[L.off + r * L.w + c]);
         }
@@ -1017,7 +1023,10 @@ template <int P, bool TWO, int PHASE, int SFL = 0>
 #ifndef MID_MINB
 #define MID_MINB 8  // p = 2 (phase 0): 8 CTAs/SM at 32 registers beats 5 at 44 (balanced N=48: 68 -> 62 ms)
 #endif
-__global__ void __launch_bounds__(TILE_X* TILE_Y, P == 2 ? MID_MINB : 1) k_field_mid(FieldArgs a)
+#ifndef MID3_MINB
+#define MID3_MINB 4  // p = 3: 64 registers, 4 CTAs/SM (config-5 shard 27.3 -> 30.6 G evals/s)
+#endif
+__global__ void __launch_bounds__(TILE_X* TILE_Y, P == 2 ? MID_MINB : (P == 3 ? MID3_MINB : 1)) k_field_mid(FieldArgs a)
 {
     constexpr int D = 2 * P + 1, SX = TILE_X + 2 * P, SY = TILE_Y + 2 * P;
     constexpr int NCH = (D + 2) / 2;  // 16-byte chunks covering D texels from an even start
