@@ -352,6 +352,8 @@ def main():
                 if dom in tr and "bytes_per_work" in tr[dom]:
                     roof["traffic"] = tr[dom]["bytes_per_work"] * d["work"] / max(d["launches"], 1)
                     roof["traffic_source"] = tr[dom].get("source")
+                if dom in tr and "ncu_util" in tr[dom]:  # measured pipe / data-path utilisation (same capture)
+                    roof["ncu_util"] = tr[dom]["ncu_util"]
             except (OSError, ValueError):
                 pass
     kernels = {k: {"launches": v["launches"], "ms_per_step": v["ms"] / args.steps,
