@@ -4,14 +4,19 @@
 Default workload = BASELINE.json configs[1], the configuration its metric is quoted on:
 accurate-mode window blend (Eq. 7/8, direct O(N*M) schedule) of 200 synthetic 512x512 frames,
 "patch 5" (p=2), "window 15" (M=15), auto pyramid (5 levels), n=5 iterations, alpha=10.
-One step = one fb_blend_window call over the whole video (pyramids, all 5760 NNF estimations with
-their per-iteration T-bar refresh, the final remaps and the window means), inputs resident in HBM.
+One step = one blend of the whole video (pyramids, all 5760 NNF estimations with their per-iteration
+T-bar refresh, the final remaps and the window means), inputs resident in HBM.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fb|reference] [--workload config2|...]
 
-N>1 runs under torchrun: targets are sharded by pair count, halo frames move over NCCL inside the
-timed step, the time is the max over ranks.  --impl reference times the CPU oracle (the reference arm
-of this tier) on a bounded sample of the same workload.  Prints ONE JSON line on rank 0.
+--gpus N > 1 runs N ranks: under torchrun when WORLD_SIZE is set (the driver's launch), else bench.py
+re-launches itself under torch.distributed.run with N local ranks.  Targets are sharded by pair count, the
+halo frames (and, in fast mode, blending-table cells; in interpolation mode, the keyframes) move between
+ranks inside the timed step, and the time is the max over ranks.  One rank per GPU over NCCL; when the
+box has fewer GPUs than ranks (the one-GPU pool), the ranks share a GPU and exchange over gloo with host
+staging -- a correctness run, flagged "oversubscribed" in the JSON line, not a scaling number.
+--impl reference times the CPU oracle (the reference arm of this tier) on a bounded sample of the same
+workload.  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -19,6 +24,7 @@ import argparse
 import json
 import os
 import platform
+import socket
 import statistics
 import subprocess
 import sys
@@ -31,6 +37,10 @@ sys.path.insert(0, ROOT)
 METRIC = "frames/sec blended (512×512, window 15, patch 5) at 1/2/4/8 B200; NNF evals/s"
 
 WORKLOADS = {
+    # BASELINE.json configs[0]: the small case the oracle finishes in seconds (parity size)
+    "config1": dict(desc="blending mode (balanced), 8 synthetic frames 64x64 RGB, patch 5, window 3, 2 pyramid "
+                         "levels, 2 PatchMatch iterations (BASELINE.json configs[0])", N=8, H=64, W=64, M=3, p=2,
+                    mode="balanced", iters=2, levels=2),
     # BASELINE.json configs[1] — the metric's configuration (default)
     "config2": dict(desc="blending mode accurate, 200 frames 512x512, patch 5, window 15, single B200 "
                          "(BASELINE.json configs[1])", N=200, H=512, W=512, M=15, p=2, mode="accurate"),
@@ -40,14 +50,20 @@ WORKLOADS = {
     # configs[3]: keyframe interpolation (Eq. 9), keys 0 and 101, 100 in-between frames at 768x768
     "config4": dict(desc="interpolation mode, 2 keyframes rendering 100 in-between frames 768x768, patch 5 "
                          "(BASELINE.json configs[3])", N=102, H=768, W=768, M=0, p=2, mode="interp", keys=[0, 101]),
+    # configs[4]: 1000 frames at 1080p, patch 7, window 15, balanced, frame-sharded over 8 GPUs
+    "config5": dict(desc="blending mode (balanced), 1000 frames 1920x1080, patch 7, window 15, frame-sharded with "
+                         "halo exchange (BASELINE.json configs[4]; 8xB200)", N=1000, H=1080, W=1920, M=15, p=3,
+                    mode="balanced"),
     # balanced mode at the metric's size (not a BASELINE config; for comparison)
     "balanced512": dict(desc="blending mode balanced, 200 frames 512x512, patch 5, window 15", N=200, H=512, W=512,
                         M=15, p=2, mode="balanced"),
 }
 
-FP32_LANES_PER_SM = 128   # Blackwell SM: 4 SMSPs x 32 FP32 lanes (blackwell_cuda_programming.md)
 SMS = 148
 SM_MAX_MHZ = 1965.0       # MEASURED_PEAKS.json sm_max_mhz (B200_PROFILING.md: clocks.max.sm)
+FP32_LANES_PER_SM = 128   # Blackwell SM: 4 SMSPs x 32 FP32 lanes (blackwell_cuda_programming.md)
+L1_BYTES_PER_CLK = 128    # L1/shared data path per SM (B300_MICROARCH.md: 128 B/cyc/SM)
+L1_PEAK_FILE = os.path.join(ROOT, "profiles", "l1_peak.json")  # tools/l1_peak_bench.cu, measured on a B200
 
 
 def dist_env():
@@ -60,9 +76,6 @@ def flops_per_eval(p: int, loss: int) -> int:
     flops) per loss term; two terms (guide, style/aux) for GUIDE_STYLE / MEAN_ALIGN."""
     terms = 1 if loss == 0 else 2
     return terms * (2 * p + 1) ** 2 * 3 * 3
-
-
-L1_BYTES_PER_CLK = 128    # L1/shared data path per SM (B300_MICROARCH.md: smem crossbar 128 B/cyc/SM)
 
 
 def gathered_bytes_per_eval(p: int, loss: int) -> int:
@@ -119,30 +132,51 @@ class ClockSampler:
 def make_cfg(P, wl):
     loss = {"accurate": P.MEAN_ALIGN, "balanced": P.GUIDE_STYLE, "fast": P.GUIDE_STYLE, "interp": P.GUIDE_STYLE}[wl["mode"]]
     sched = P.TREE if wl["mode"] == "fast" else P.DIRECT
-    return P.MatchCfg(patch_radius=wl["p"], iters_per_level=5, alpha=10.0, loss=loss, seed=1), sched
+    return P.MatchCfg(patch_radius=wl["p"], iters_per_level=wl.get("iters", 5), levels=wl.get("levels", 0), alpha=10.0,
+                      loss=loss, seed=1), sched
+
+
+def config_dict(wl, world: int) -> dict:
+    """The workload description both arms print (identical dicts: the driver compares them)."""
+    N = wl["N"]
+    state = "inputs and per-step NNF state exceed the 126 MB L2; no flush needed" if N * wl["H"] * wl["W"] >= 2 ** 24 \
+        else "small parity case: fits in L2 (not a bandwidth measurement)"
+    return {"workload": wl["desc"], "N": N, "H": wl["H"], "W": wl["W"], "M": wl["M"], "p": wl["p"], "mode": wl["mode"],
+            "levels": wl.get("levels", 0) or "auto", "iters_per_level": wl.get("iters", 5), "alpha": 10.0,
+            "global_batch": N, "parallelism": f"dp{world} (frame shards + halo exchange)" if world > 1 else "dp1",
+            "l2": state}
 
 
 # ------------------------------------------------------------------------------------------ oracle arm
-def oracle_sample(wl, n_pairs: int, threads: int | None = None):
-    """Times the CPU oracle (as it stands) on a bounded sample of the workload: n_pairs NNF estimations
-    of target 0's window, with the workload's loss (MEAN_ALIGN pairs coupled through T-bar, Eq. 8), at
-    full resolution.  Returns (seconds, pairs, evals)."""
+def oracle_sample(wl, n_pairs: int | None = None):
+    """Times the CPU oracle (as it stands) on a bounded sample of the workload at full resolution, with the
+    workload's loss, levels and iterations.  Direct modes: the pairs j -> 0 of target 0's window W_0 =
+    [0, M] (all M of them by default; MEAN_ALIGN pairs coupled through T-bar, Eq. 8).  Fast mode: GUIDE_STYLE
+    pairs j -> 0 for j = 1..n.  Interpolation: key 0 -> frames 1..n.  Returns (seconds, pairs, evals, label)."""
     import numpy as np
 
     import oracle as O
     from synth import moving_texture
-    if threads:
-        O.set_threads(threads)
-    g, s = moving_texture(n_pairs + 1, wl["H"], wl["W"])
+    interp = wl["mode"] == "interp"
+    if n_pairs is None:
+        n_pairs = 8 if interp else max(1, min(wl["M"], wl["N"] - 1))
+    g, s = moving_texture(wl["N"], wl["H"], wl["W"], t0=0, t1=n_pairs + 1)
     loss = O.MEAN_ALIGN if wl["mode"] == "accurate" else O.GUIDE_STYLE
-    cfg = O.Cfg(patch_radius=wl["p"], iters_per_level=5, alpha=10.0, loss=loss, seed=1)
+    cfg = O.Cfg(patch_radius=wl["p"], iters_per_level=wl.get("iters", 5), levels=wl.get("levels", 0), alpha=10.0,
+                loss=loss, seed=1)
     n1 = n_pairs + 1
     frames = np.concatenate([g, s]).astype(np.float32)
-    tasks = [dict(src_guide=j, tgt_guide=0, src_style=n1 + j, tgt_style=n1, group=0, src_id=j, tgt_id=0, tag=0)
-             for j in range(1, n1)]
+    if interp:  # NNF(key 0 -> frame m), m = 1..n (Eq. 9's single-key pairs)
+        tasks = [dict(src_guide=0, tgt_guide=m, src_style=n1, group=m, src_id=0, tgt_id=m, tag=5) for m in range(1, n1)]
+        label = f"{n_pairs} interpolation pairs key 0 -> frames 1..{n_pairs}"
+    else:
+        tasks = [dict(src_guide=j, tgt_guide=0, src_style=n1 + j, tgt_style=n1, group=0, src_id=j, tgt_id=0, tag=0)
+                 for j in range(1, n1)]
+        label = (f"the {n_pairs} pairs j -> 0 (j = 1..{n_pairs}) of target 0's window" if wl["mode"] != "fast" else
+                 f"{n_pairs} GUIDE_STYLE pairs j -> 0 (j = 1..{n_pairs})")
     t = time.perf_counter()
     _, _, _, evals = O.nnf(cfg, frames, tasks, want_x=True)
-    return time.perf_counter() - t, n_pairs, evals
+    return time.perf_counter() - t, n_pairs, evals, label
 
 
 def workload_pairs(wl) -> int:
@@ -151,11 +185,44 @@ def workload_pairs(wl) -> int:
         keys = wl["keys"]
         return sum(int(any(k < m for k in keys)) + int(any(k > m for k in keys)) for m in range(N) if m not in keys)
     if wl["mode"] == "fast":
-        return 2242 if (N, M) == (200, 30) else N * 10  # exact count for config 3
+        import oracle as O
+        lcap = 0
+        while (2 << lcap) <= M + 1:
+            lcap += 1
+        builds = len(O.tree_build_tasks(N, lcap)) if N > 1 and M > 0 else 0
+        queries = 0
+        for o in (0, 1):
+            for i in range(N):
+                v = i if o == 0 else N - 1 - i
+                queries += len(O.tree_query_nodes(max(0, v - M), v)) - 1
+        return 2 * builds + queries if M > 0 else 0
     return sum(min(N - 1, i + M) - max(0, i - M) for i in range(N))
 
 
+def cpu_sample_record(wl, n_pairs):
+    import oracle as O
+    cores = len(os.sched_getaffinity(0))
+    O.set_threads(cores)
+    dt, npairs, ev, label = oracle_sample(wl, n_pairs)
+    pairs_total = workload_pairs(wl)
+    return {"value": wl["N"] / (dt / npairs * pairs_total), "unit": "frames/s", "cores": cores, "kind": "oracle",
+            "sample": f"{label}: {npairs} of the workload's {pairs_total} NNF pairs at full resolution "
+                      f"(same loss, levels, iterations), {dt:.1f} s, whole workload extrapolated by pair count",
+            "evals_per_s": ev / dt, "cpu": platform.processor() or platform.machine()}
+
+
 def run_reference(args, wl, rank, world):
+    """The reference arm (the oracle, on the host cores).  Under torchrun only rank 0 works; every rank joins
+    a gloo group first so the line can state how many ranks were started."""
+    started = world
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        one = torch.ones(1)
+        dist.all_reduce(one)
+        started = int(one.item())
+        dist.destroy_process_group()
     if rank != 0:
         return
     import oracle as O
@@ -164,27 +231,94 @@ def run_reference(args, wl, rank, world):
     pairs_total = workload_pairs(wl)
     for _ in range(args.warmup):
         oracle_sample(wl, args.cpu_pairs)
-    times = []
-    evals = 0
+    times, evals, label, npairs = [], 0, "", 1
     for _ in range(args.steps):
-        dt, npairs, ev = oracle_sample(wl, args.cpu_pairs)
+        dt, npairs, ev, label = oracle_sample(wl, args.cpu_pairs)
         times.append(dt)
         evals = ev
-    per_pair = statistics.mean(times) / args.cpu_pairs
+    per_pair = statistics.mean(times) / npairs
     step_s = per_pair * pairs_total  # the whole workload, extrapolated by exact pair count
-    fps = wl["N"] / step_s
-    sample = (f"{args.cpu_pairs} of the {pairs_total} NNF pairs of the workload (target 0's window, full "
-              f"{wl['H']}x{wl['W']}, same loss/levels/iterations), extrapolated by pair count")
+    fps = wl["N"] / step_s if step_s > 0 else float("inf")
+    sample = (f"{label}: {npairs} of the workload's {pairs_total} NNF pairs per step at full resolution (same loss, "
+              f"levels, iterations); ms_per_step = the whole workload extrapolated by pair count")
     line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": wl["desc"], "N": wl["N"], "H": wl["H"], "W": wl["W"], "M": wl["M"], "p": wl["p"],
-                       "mode": wl["mode"], "iters_per_level": 5, "alpha": 10.0, "parallelism": f"dp{world}"},
-            "evals_per_s": evals / statistics.mean(times),
+            "ranks_started": started, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+            "ms_per_step_measured": statistics.mean(times) * 1e3, "extrapolated": True,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(wl, world), "evals_per_s": evals / statistics.mean(times),
             "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": sample,
                              "cpu": platform.processor() or platform.machine()},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------ multi-rank launch
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    """`python bench.py --gpus N` without WORLD_SIZE: run the same command as N local ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+# ------------------------------------------------------------------------------------------ roofline
+def roofline(prof, wl, cfg, steps):
+    """Roofline of the dominant kernel class.  SURVEY 8(d): the PatchMatch evaluation is bound by
+    the L1/shared data path (gathered patch rows), so `roofline` reports algorithmic gathered bytes (600 B per
+    evaluation at p = 2, FP32) per second against the L1 peak measured on a B200 by
+    tools/l1_peak_bench.cu (profiles/l1_peak.json; the nominal 148 x 128 B x 1965 MHz if absent), with the
+    hardware counters of the committed ncu capture (ncu_traffic.json) beside it.  The FP32-pipe figure is
+    `roofline_alu`."""
+    if not prof:
+        return None, None
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    d = prof[dom]
+    sec = d["ms"] / 1e3
+    total_ms = sum(v["ms"] for v in prof.values())
+    if not (dom.startswith("field") or dom.startswith("iter")):
+        return {"kernel": dom, "bound": "l1", "achieved": None, "peak": None, "unit": "GB/s", "frac": None,
+                "traffic": None, "share_of_kernel_time": d["ms"] / total_ms}, None
+    bpe = gathered_bytes_per_eval(wl["p"], cfg.loss)
+    fpe = flops_per_eval(wl["p"], cfg.loss)
+    nominal = SMS * L1_BYTES_PER_CLK * SM_MAX_MHZ * 1e6 / 1e9
+    peak, peak_src = nominal, "nominal: 148 SMs x 128 B/clk x 1965 MHz (no measured L1 peak file)"
+    if os.path.exists(L1_PEAK_FILE):
+        try:
+            lp = json.load(open(L1_PEAK_FILE))
+            peak = float(lp["l1_peak_gbs"])
+            peak_src = f"measured: {lp.get('how', 'tools/l1_peak_bench.cu')} ({lp.get('when', '')})"
+        except (OSError, ValueError, KeyError):
+            pass
+    achieved = d["work"] * bpe / sec / 1e9
+    roof = {"kernel": f"pm_{dom}", "bound": "l1", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "frac_of_nominal": achieved / nominal, "traffic": None, "peak_basis": peak_src,
+            "bytes_per_eval": bpe, "evals_per_launch": d["work"] / max(d["launches"], 1),
+            "avg_launch_ms": d["ms"] / max(d["launches"], 1), "share_of_kernel_time": d["ms"] / total_ms,
+            "note": "algorithmic bytes: partial-distance elimination and the 8-byte exact texels load fewer; the "
+                    "hardware L1 utilisation of the same kernel is ncu_util.l1tex_lsu_wavefronts_pct"}
+    traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(traffic_file):
+        try:
+            tr = json.load(open(traffic_file))
+            if dom in tr and "bytes_per_work" in tr[dom]:
+                roof["traffic"] = tr[dom]["bytes_per_work"] * d["work"] / max(d["launches"], 1)
+                roof["traffic_source"] = tr[dom].get("source")
+            if dom in tr and "ncu_util" in tr[dom]:
+                roof["ncu_util"] = tr[dom]["ncu_util"]
+        except (OSError, ValueError):
+            pass
+    fp32_peak = SMS * FP32_LANES_PER_SM * 2 * SM_MAX_MHZ * 1e6 / 1e12
+    alu = {"kernel": f"pm_{dom}", "bound": "alu", "achieved": d["work"] * fpe / sec / 1e12, "peak": fp32_peak,
+           "unit": "TFLOP/s", "frac": d["work"] * fpe / sec / 1e12 / fp32_peak, "flops_per_eval": fpe,
+           "peak_basis": "nominal FP32: 148 SMs x 128 lanes x 2 flop x 1965 MHz (guide unit counts)"}
+    return roof, alu
 
 
 # ------------------------------------------------------------------------------------------ GPU arm
@@ -195,17 +329,22 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fb", choices=["fb", "reference"])
     ap.add_argument("--workload", default="config2", choices=sorted(WORKLOADS))
-    ap.add_argument("--cpu-pairs", type=int, default=16, help="oracle sample size (NNF pairs)")
+    ap.add_argument("--cpu-pairs", type=int, default=None, help="oracle sample size (NNF pairs; default: target 0's window)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--check-single", action="store_true",
+                    help="N>1: after timing, compare every rank's rows with the single-call blend of its targets")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args.gpus))
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args, wl, rank, world)
     args.warmup = max(args.warmup, 3)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -213,10 +352,21 @@ def main():
     from paper_2311_09265_b200 import shard
     from synth import moving_texture
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    if ndev < 1:
+        raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    oversub = world > 1 and ndev < local_world
+    dev_idx = local % ndev
+    torch.cuda.set_device(dev_idx)
+    dev = torch.device("cuda", dev_idx)
+    backend = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = "gloo" if oversub else "nccl"
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     N, H, W, M = wl["N"], wl["H"], wl["W"], wl["M"]
     cfg, sched = make_cfg(P, wl)
     interp = wl["mode"] == "interp"
@@ -224,18 +374,21 @@ def main():
     plan = shard.plan_interp_shards(N, keys, world) if interp else \
         shard.plan_shards(N, M, world, "tree" if sched == P.TREE else "direct")
     t0, t1 = plan[rank]
-    g_all, s_all = moving_texture(N, H, W)  # deterministic: every rank would load only its own frames
-    if interp:  # the key styles live on rank 0 (broadcast inside the step); s_own is unused
-        ks_all = torch.from_numpy(s_all[keys]).to(dev) if rank == 0 else None
-        ks_host = torch.from_numpy(s_all[keys]).pin_memory() if rank == 0 else None
-    g_own = torch.from_numpy(g_all[t0:t1]).to(dev)
-    s_own = torch.from_numpy(s_all[t0:t1]).to(dev)
-    g_host = torch.from_numpy(g_all[t0:t1]).pin_memory()
-    s_host = torch.from_numpy(s_all[t0:t1]).pin_memory()
-    del g_all, s_all
-    ctx = P.Context(local)
+    g_np, s_np = moving_texture(N, H, W, t0=t0, t1=t1)  # each rank generates only its own frames
+    if interp and rank == 0:  # the key styles live on rank 0 (broadcast inside the step)
+        import numpy as np
+        ks_np = np.concatenate([moving_texture(N, H, W, t0=k, t1=k + 1)[1] for k in keys])
+        ks_all = torch.from_numpy(ks_np).to(dev)
+        ks_host = torch.from_numpy(ks_np).pin_memory()
+    else:
+        ks_all = ks_host = None
+    g_own = torch.from_numpy(g_np).to(dev)
+    s_own = torch.from_numpy(s_np).to(dev)
+    g_host = torch.from_numpy(g_np).pin_memory()
+    s_host = torch.from_numpy(s_np).pin_memory()
+    ctx = P.Context(dev_idx)
     stream = ctx.stream
-    out = torch.empty((t1 - t0, H, W, 3), dtype=torch.float32, device=dev)
+    out = torch.empty((max(t1 - t0, 1), H, W, 3), dtype=torch.float32, device=dev)
     stats = {}
 
     def step(g_in, s_in, ks_in=None):
@@ -245,17 +398,13 @@ def main():
                 _, st = shard.interpolate_sharded(ctx, cfg, plan, N, keys, rank, g_in, ks, out=out)
             else:
                 _, st = ctx.fb_interpolate_keyframes(cfg, g_in, keys, ks, out=out)
-            stats.update(st)
-            return
-        if world > 1:
+        elif world == 1:
+            _, st = ctx.fb_blend_window_range(cfg, sched, N, 0, g_in, s_in, M, 0, N, out=out)
+        elif sched == P.TREE:  # fast mode: owned blending-table cells built once, exchanged
             (g_loc, s_loc), f0 = shard.halo_exchange([g_in, s_in], plan, N, M, rank)
-            if sched == P.TREE:  # fast mode: owned blending-table cells built once, exchanged
-                _, st = shard.blend_tree_exchange(ctx, cfg, plan, N, M, rank, g_loc, s_loc, f0, out=out)
-                stats.update(st)
-                return
+            _, st = shard.blend_tree_exchange(ctx, cfg, plan, N, M, rank, g_loc, s_loc, f0, out=out)
         else:
-            g_loc, s_loc, f0 = g_in, s_in, 0
-        _, st = ctx.fb_blend_window_range(cfg, sched, N, f0, g_loc, s_loc, M, t0, t1, out=out)
+            _, st = shard.blend_direct_sharded(ctx, cfg, plan, N, M, rank, g_in, s_in, out=out)
         stats.update(st)
 
     def barrier():
@@ -269,7 +418,7 @@ def main():
     barrier()
 
     # ---- timed region: K steps, inputs resident in HBM
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev_idx)
     clocks.start()
     ctx.profile_reset()
     ctx.profile_enable(True)
@@ -286,106 +435,93 @@ def main():
     prof = ctx.profile_read()
     ctx.profile_enable(False)
     clk = clocks.stop()
-    t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
-    work = torch.tensor([stats.get("candidate_evals", 0), stats.get("nnf_pairs", 0)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(work, op=dist.ReduceOp.SUM)
-    ms = float(t.item()) / args.steps
-    evals_step, pairs_step = float(work[0].item()), int(work[1].item())
+
+    def allreduce(vals, op):
+        t = torch.tensor(vals, dtype=torch.float64)
+        if world > 1:
+            t = t.to(dev) if backend == "nccl" else t
+            dist.all_reduce(t, op=op)
+        return [float(x) for x in t.cpu()]
+
+    ms = allreduce([ms_local], dist.ReduceOp.MAX if world > 1 else None)[0] / args.steps
+    evals_step, pairs_step, launches_all = allreduce(
+        [stats.get("candidate_evals", 0), stats.get("nnf_pairs", 0), launches],
+        dist.ReduceOp.SUM if world > 1 else None)
     fps = N / (ms / 1e3)
 
     # ---- e2e: the public call on pinned HOST frames; H2D + blend + D2H every step
     e2e = None
     if not args.no_e2e:
-        out_host = torch.empty((t1 - t0, H, W, 3), dtype=torch.float32, pin_memory=True)
+        out_host = torch.empty(out.shape, dtype=torch.float32, pin_memory=True)
+        own = t1 - t0
+        h2d_rank = own * H * W * 3 * (1 if interp else 2) + (len(keys) * H * W * 3 if interp and rank == 0 else 0)
+        d2h_rank = own * H * W * 3 * 4
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
             g_d = g_host.to(dev, non_blocking=True)
             if interp:
-                step(g_d, None, ks_host.to(dev, non_blocking=True) if rank == 0 else None)
+                step(g_d, None, ks_host.to(dev, non_blocking=True) if ks_host is not None else None)
             else:
                 step(g_d, s_host.to(dev, non_blocking=True))
             out_host.copy_(out, non_blocking=True)
         e1.record(stream)
         barrier()
-        t2 = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t2.item()) / args.steps
-        h2d = (N + len(keys)) * H * W * 3 if interp else 2 * N * H * W * 3
+        ms_e2e = allreduce([e0.elapsed_time(e1)], dist.ReduceOp.MAX if world > 1 else None)[0] / args.steps
+        h2d, d2h = allreduce([h2d_rank, d2h_rank], dist.ReduceOp.SUM if world > 1 else None)
         e2e = {"value": N / (ms_e2e / 1e3), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(N * H * W * 3 * 4), "ms_per_step": ms_e2e}
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e,
+               "bytes": "summed over ranks; each rank copies only its own frames (and rank 0 the keyframes)"}
+
+    # ---- optional: every rank's sharded rows == the single-call blend of its targets (all frames local)
+    check = None
+    if args.check_single and world > 1:
+        if t1 > t0:
+            ga, sa = moving_texture(N, H, W)
+            if interp:
+                ref, _ = ctx.fb_interpolate_keyframes(cfg, torch.from_numpy(ga).to(dev), keys,
+                                                      torch.from_numpy(sa[keys]).to(dev))
+                ref = ref[t0:t1]
+            else:
+                ref, _ = P.Context(dev_idx).fb_blend_window_range(cfg, sched, N, 0, torch.from_numpy(ga).to(dev),
+                                                                  torch.from_numpy(sa).to(dev), M, t0, t1)
+            same = float(torch.equal(out[:t1 - t0], ref))
+        else:
+            same = 1.0
+        check = allreduce([same], dist.ReduceOp.MIN)[0] == 1.0
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel class
-    dom = max(prof, key=lambda k: prof[k]["ms"]) if prof else None
-    roof = roof_l1 = None
-    if dom:
-        d = prof[dom]
-        sec = d["ms"] / 1e3
-        total_ms = sum(v["ms"] for v in prof.values())
-        if dom.startswith("field") or dom.startswith("iter"):
-            fpe = flops_per_eval(wl["p"], cfg.loss)
-            bpe = gathered_bytes_per_eval(wl["p"], cfg.loss)
-            achieved = d["work"] * fpe / sec / 1e12
-            peak = SMS * FP32_LANES_PER_SM * 2 * SM_MAX_MHZ * 1e6 / 1e12
-            roof = {"kernel": f"pm_{dom}", "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": None,
-                    "peak_basis": "FP32: 148 SMs x 128 lanes x 2 flop x 1965 MHz (guide unit counts, max clock)",
-                    "flops_per_eval": fpe, "evals_per_launch": d["work"] / max(d["launches"], 1),
-                    "avg_launch_ms": d["ms"] / max(d["launches"], 1), "share_of_kernel_time": d["ms"] / total_ms}
-            achieved_l1 = d["work"] * bpe / sec / 1e9
-            peak_l1 = SMS * L1_BYTES_PER_CLK * SM_MAX_MHZ * 1e6 / 1e9
-            roof_l1 = {"kernel": f"pm_{dom}", "bound": "l1", "achieved": achieved_l1, "peak": peak_l1, "unit": "GB/s",
-                       "frac": achieved_l1 / peak_l1, "bytes_per_eval": bpe,
-                       "peak_basis": "L1/shared data path: 148 SMs x 128 B/clk x 1965 MHz (SURVEY 8(d) binding ceiling)"}
-        traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if roof and os.path.exists(traffic_file):
-            try:
-                tr = json.load(open(traffic_file))
-                if dom in tr and "bytes_per_work" in tr[dom]:
-                    roof["traffic"] = tr[dom]["bytes_per_work"] * d["work"] / max(d["launches"], 1)
-                    roof["traffic_source"] = tr[dom].get("source")
-                if dom in tr and "ncu_util" in tr[dom]:  # measured pipe / data-path utilisation (same capture)
-                    roof["ncu_util"] = tr[dom]["ncu_util"]
-            except (OSError, ValueError):
-                pass
+    roof, roof_alu = roofline(prof, wl, cfg, args.steps)
     kernels = {k: {"launches": v["launches"], "ms_per_step": v["ms"] / args.steps,
                    "work_per_step": v["work"] / args.steps} for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
 
     # ---- CPU baseline: the oracle on this host, bounded sample, rank 0 at N=1 only
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        import oracle as O
-        cores = len(os.sched_getaffinity(0))
-        O.set_threads(cores)
-        dt, npairs, ev = oracle_sample(wl, min(args.cpu_pairs, 8) if wl["mode"] == "interp" else args.cpu_pairs)
-        pairs_total = workload_pairs(wl)
-        cpu = {"value": N / (dt / npairs * pairs_total), "unit": "frames/s", "cores": cores, "kind": "oracle",
-               "sample": f"{npairs} of the {pairs_total} NNF pairs (target 0's window, full resolution, same loss, "
-                         f"levels and iterations), {dt:.1f} s, extrapolated by pair count",
-               "evals_per_s": ev / dt}
+        cpu = cpu_sample_record(wl, args.cpu_pairs)
 
     line = {
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": wl["desc"], "N": N, "H": H, "W": W, "M": M, "p": wl["p"], "mode": wl["mode"],
-                   "levels": "auto (5)", "iters_per_level": 5, "alpha": 10.0, "global_batch": N,
-                   "parallelism": f"dp{world} (frame shards + NCCL halo)" if world > 1 else "dp1",
-                   "l2": "inputs 315 MB and per-step state >30 GB exceed the 126 MB L2; no flush needed",
-                   "nnf_pairs_per_step": pairs_step, "evals_per_step": evals_step,
-                   "launches_per_step": launches / args.steps},
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_dict(wl, world),
+        "work": {"nnf_pairs_per_step": int(pairs_step), "evals_per_step": evals_step,
+                 "launches_per_step": launches_all / args.steps},
         "evals_per_s": evals_step / (ms / 1e3),
-        "roofline": roof, "roofline_l1": roof_l1, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-        "clocks": clk,
+        "roofline": roof, "roofline_alu": roof_alu, "kernels": kernels if world == 1 else {"rank0": kernels},
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches_all), "clocks": clk,
     }
+    if world > 1:
+        line["exchange"] = {"backend": backend, "devices": ndev, "oversubscribed": oversub,
+                            "plan": plan}
+        if oversub:
+            line["exchange"]["note"] = (f"{world} ranks on {ndev} GPU(s), gloo with host-staged exchange: a correctness "
+                                        "run of the sharded path, not a scaling measurement")
+        if check is not None:
+            line["sharded_equals_single_call"] = check
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

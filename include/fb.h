@@ -36,11 +36,12 @@ typedef struct fb_ctx_s* fb_ctx;
 
 typedef enum {
     FB_OK = 0,
-    FB_ERR_INVALID_ARG = 1, /* N<1, M<0, p<1, n<0, alpha<0, bad enum, NULL required pointer, bad keys,
+    FB_ERR_INVALID_ARG = 1, /* N<1, M<0, p<1, n<0 or n>1023, rs_steps>4095 (Philox counter fields, D21),
+                             * alpha<0, bad enum, NULL required pointer, bad keys,
                              * BASE/PAIRWISE for a window blend, non-mutual PAIRWISE counterparts */
     FB_ERR_SHAPE = 2,       /* min(H,W) < 2p+1, or explicit levels whose coarsest side < 2p+1 (D32)  */
     FB_ERR_CUDA = 3,        /* a CUDA runtime error (message in fb_last_error)                         */
-    FB_ERR_NCCL = 4,        /* reserved for the multi-GPU entry points                                 */
+    FB_ERR_NCCL = 4,        /* reserved: the multi-GPU exchange runs on torch.distributed (D43) */
     FB_ERR_WORKSPACE = 5,   /* no workspace set, or smaller than fb_workspace_size() requires          */
     FB_ERR_UNSUPPORTED = 6  /* TREE + MEAN_ALIGN (accurate mode is O(N*M) by definition), p > 4 */
 } fb_status;
@@ -104,6 +105,16 @@ size_t fb_workspace_size_range(fb_ctx ctx, int schedule, const fb_match_cfg* cfg
                                int W, int M, int t0, int t1);
 /* Number of kernels this context has launched so far (for launch accounting in bench.py). */
 uint64_t fb_launch_count(fb_ctx ctx);
+
+/* Kernel-schedule options of one context (A/B of equivalent kernel schedules; every setting gives
+ * bit-identical results, which tests/test_gpu_parity.py checks).  Defaults are the measured optima:
+ *   FB_OPT_FUSED_ITER   0  1 = a whole level-0 iteration per launch (k_iter_fast; measured slower)
+ *   FB_OPT_FUSE13       1  0 = level-0 propagation fields 1-3 and the random search as separate launches
+ *   FB_OPT_PHASE0_MID   1  0 = level-0 E init + field 0 with the register-target kernel
+ *   FB_OPT_TGT_REG_ROWS 2  target patch rows held in registers by the fused level-0 kernel (0 = all, 1, 2)
+ * Errors: FB_ERR_INVALID_ARG (unknown option or value). */
+typedef enum { FB_OPT_FUSED_ITER = 0, FB_OPT_FUSE13 = 1, FB_OPT_PHASE0_MID = 2, FB_OPT_TGT_REG_ROWS = 3 } fb_option;
+fb_status fb_set_option(fb_ctx ctx, int option, int value);
 
 /* ---- kernel timing (bench instrumentation) -----------------------------------------------------
  * When enabled, every kernel launch of this context is bracketed by two CUDA events recorded on the

@@ -473,6 +473,22 @@ static void iterate_task(orc_state* st, int t, int k, int it, uint64_t* evals)
     }
 }
 
+/* "Upsample F" (Alg. 1; reading D7): the coarse field Fc [hc, wc, 2] (level k+1) to the fine grid
+ * [h, w, 2] (level k, h = 2hc or 2hc+1):
+ *   F_f(r,c) = clamp(2 F_c(rc,cc) + (r - 2rc, c - 2cc)),  rc = min(r>>1, hc-1),  cc = min(c>>1, wc-1),
+ * clamped to [0,h-1] x [0,w-1] (D10).  The last odd row / column reuses the last coarse cell. */
+void orc_upsample(const int32_t* Fc, int hc, int wc, int32_t* Ff, int h, int w)
+{
+    for (int r = 0; r < h; ++r)
+        for (int c = 0; c < w; ++c) {
+            int rc = (r >> 1) < hc - 1 ? (r >> 1) : hc - 1;
+            int cc = (c >> 1) < wc - 1 ? (c >> 1) : wc - 1;
+            size_t j = (size_t)rc * wc + cc, i = (size_t)r * w + c;
+            Ff[2 * i] = clampi(2 * Fc[2 * j] + (r - 2 * rc), 0, h - 1);
+            Ff[2 * i + 1] = clampi(2 * Fc[2 * j + 1] + (c - 2 * cc), 0, w - 1);
+        }
+}
+
 /* frames: stack [NF, H, W, 3] float (8-bit units).  Outputs per task (nullable):
  * F_out int32 [T,H,W,2], E_out float [T,H,W], X_out float [T,H,W,3] = remap of src style (Alg. 2). */
 int orc_nnf(const orc_cfg* cfg, int T, int H, int W, const float* frames, const orc_task* tasks,
@@ -535,17 +551,9 @@ int orc_nnf(const orc_cfg* cfg, int T, int H, int W, const float* frames, const 
                         F[2 * i + 1] = (int32_t)mulhi32(u[1], (uint32_t)w);
                     }
             } else {
-                /* "Upsample F" (D7): F_f(r,c) = clamp(2 F_c(rc,cc) + (r - 2rc, c - 2cc)) */
                 int hc = st.L[k + 1].h, wc = st.L[k + 1].w;
                 memcpy(tmp, F, sizeof(int32_t) * 2 * (size_t)hc * wc);
-                for (int r = 0; r < h; ++r)
-                    for (int c = 0; c < w; ++c) {
-                        int rc = (r >> 1) < hc - 1 ? (r >> 1) : hc - 1;
-                        int cc = (c >> 1) < wc - 1 ? (c >> 1) : wc - 1;
-                        size_t j = (size_t)rc * wc + cc, i = (size_t)r * w + c;
-                        F[2 * i] = clampi(2 * tmp[2 * j] + (r - 2 * rc), 0, h - 1);
-                        F[2 * i + 1] = clampi(2 * tmp[2 * j + 1] + (c - 2 * cc), 0, w - 1);
-                    }
+                orc_upsample(tmp, hc, wc, F, h, w);
             }
         }
         for (int it = 0; it < cfg->iters_per_level; ++it) {

@@ -11,6 +11,9 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "fb_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+# ORACLE_LIB: load a prebuilt oracle library instead (tools/oracle_mutations.py runs the pins against
+# deliberately broken builds to show that each pin catches its mistake)
+_LIB_OVERRIDE = os.environ.get("ORACLE_LIB")
 
 # -O2, no fast-math, no FP contraction: the only fused ops are the explicit fmaf() calls (D20).
 CFLAGS = ["-O2", "-std=c11", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off", "-fno-fast-math"]
@@ -68,7 +71,7 @@ _lib = None
 def load():
     global _lib
     if _lib is None:
-        _lib = C.CDLL(build())
+        _lib = C.CDLL(_LIB_OVERRIDE or build())
         P = C.POINTER
         _lib.orc_philox4x32_10.argtypes = [P(C.c_uint32), P(C.c_uint32), P(C.c_uint32)]
         _lib.orc_level_count.argtypes = [C.c_int] * 4
@@ -92,6 +95,7 @@ def load():
         _lib.orc_field.argtypes = [P(_Cfg), C.c_int, C.c_int] + [C.c_void_p] * 4 + [C.c_int] * 6 + [C.c_void_p] * 2
         _lib.orc_set_threads.argtypes = [C.c_int]
         _lib.orc_track_field.argtypes = [P(_Cfg), C.c_int, C.c_int] + [C.c_void_p] * 7
+        _lib.orc_upsample.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int]
         _lib.orc_field_step.argtypes = [P(_Cfg), C.c_int, C.c_int] + [C.c_void_p] * 4 + [C.c_int] * 7 + [C.c_void_p] * 2
     return _lib
 
@@ -149,6 +153,15 @@ def remap(S: np.ndarray, F: np.ndarray, p: int) -> np.ndarray:
     out = np.zeros_like(S)
     load().orc_remap(_p(S), h, w, _p(F), p, _p(out))
     return out
+
+
+def upsample(Fc: np.ndarray, h: int, w: int) -> np.ndarray:
+    """Alg. 1 "Upsample F" (D7): coarse NNF int32 [hc,wc,2] -> fine NNF int32 [h,w,2]."""
+    Fc = np.ascontiguousarray(Fc, np.int32)
+    hc, wc, _ = Fc.shape
+    Ff = np.zeros((h, w, 2), np.int32)
+    load().orc_upsample(_p(Fc), hc, wc, _p(Ff), h, w)
+    return Ff
 
 
 def evals_per_task(cfg: Cfg, H: int, W: int) -> int:

@@ -31,12 +31,13 @@ struct fb_ctx_s {
     size_t ws_bytes = 0;
     int64_t max_pairs = 0;
     uint64_t launches = 0;
-    bool fused = false;  // fused iteration kernel on the fast path (FB_FUSED=1; measured slower)
-    bool fuse13 = true;  // fields 1-3 + random search fused on the fast path (FB_FUSE13=0 disables)
-    bool phase0_mid = true;  // E init + field 0 at level 0 through the shared-memory-target kernel (FB_P0MID=0:
-                             // register target; 44 vs 163 registers: field0.L0 95 -> 76 ms at N=48)
-    int tgt_reg_rows = 2;  // fused fields 1-3: target rows in registers, rest in shared memory (FB_HYROWS;
-                           // 0 = all in registers; accurate N=48: field123.L0 413 -> 397 ms)
+    // Kernel-schedule options (fb_set_option; per context, results identical for every setting):
+    bool fused = false;  // FB_OPT_FUSED_ITER: a whole level-0 iteration per launch (measured slower)
+    bool fuse13 = true;  // FB_OPT_FUSE13: fields 1-3 + random search fused on the fast path
+    bool phase0_mid = true;  // FB_OPT_PHASE0_MID: E init + field 0 at level 0 through the shared-memory-target
+                             // kernel (0: register target; 44 vs 163 registers: field0.L0 95 -> 76 ms at N=48)
+    int tgt_reg_rows = 2;  // FB_OPT_TGT_REG_ROWS: fused fields 1-3 target rows in registers, rest in shared
+                           // memory (0 = all in registers; accurate N=48: field123.L0 413 -> 397 ms)
     std::string err;
     // kernel timing (fb_profile_*)
     bool prof = false;
@@ -86,7 +87,7 @@ struct fb_ctx_s {
 namespace {
 
 constexpr size_t kAutoStateBudget = 64ull << 30;  // bytes of per-pair state in one auto-sized batch
-constexpr int kMaxBatchPairs = 65535;              // grid.y limit of the per-task launches
+constexpr int kMaxBatchPairs = 65535;              // pairs per batch (field grids T x tiles stay below 2^31)
 
 struct Fail {
     fb_status st;
@@ -178,12 +179,11 @@ fbk::PLvl padded(int h, int w, int k)
 // Packed source format of level k for a slot whose level-0 format is fmt0 (kernels.h): u8 styles use
 // SF8 at level 0, the exact 10-bit form SF10 at level 1 (n = 4v < 2^10, 8 bytes per texel) and the exact
 // 16-bit integer form SF16 at levels 2..4 (values n / 4^k, n < 2^16).
-static bool sf10_enabled = true;  // A/B knob (FB_SF10=0: level 1 as SF16, identical results)
 int src_fmt(int fmt0, int k)
 {
     if (fmt0 == fbk::SF8F) return k == 0 ? fbk::SF8F : fbk::SF32;  // float styles: u8 guide + f32 style
     if (fmt0 != fbk::SF8) return fbk::SF32;
-    if (k == 1 && sf10_enabled) return fbk::SF10;
+    if (k == 1) return fbk::SF10;
     return k == 0 ? fbk::SF8 : (k <= 4 ? fbk::SF16 : fbk::SF32);
 }
 size_t src_bytes(int fmt)
@@ -247,6 +247,10 @@ void validate_cfg(const fb_match_cfg* cfg)
     if (cfg->patch_radius > 4) throw Fail{FB_ERR_UNSUPPORTED, "patch_radius > 4 is not compiled"};
     if (cfg->iters_per_level < 0 || cfg->levels < 0 || cfg->rs_radius0 < 0 || cfg->rs_steps < 0)
         throw Fail{FB_ERR_INVALID_ARG, "negative iteration / level / random-search parameter"};
+    // the Philox counter word c1 packs purpose << 28 | level << 22 | iter << 12 | step (D21): wider values
+    // would alias draws of different iterations / levels
+    if (cfg->iters_per_level > 1023) throw Fail{FB_ERR_INVALID_ARG, "iters_per_level > 1023 (Philox counter field)"};
+    if (cfg->rs_steps > 4095) throw Fail{FB_ERR_INVALID_ARG, "rs_steps > 4095 (Philox counter field)"};
     if (!(cfg->alpha >= 0.0f)) throw Fail{FB_ERR_INVALID_ARG, "alpha < 0"};
     if (cfg->loss < 0 || cfg->loss > 3) throw Fail{FB_ERR_INVALID_ARG, "unknown loss"};
     if (cfg->init < 0 || cfg->init > 1) throw Fail{FB_ERR_INVALID_ARG, "unknown init"};
@@ -1111,16 +1115,6 @@ fb_status fb_ctx_create(int device, void* cuda_stream, fb_ctx* out)
     *out = nullptr;
     if (cudaSetDevice(device) != cudaSuccess) return FB_ERR_CUDA;
     fb_ctx c = new fb_ctx_s;
-    const char* fused = getenv("FB_FUSED");  // A/B knob: FB_FUSED=1 runs each level-0 iteration as one launch
-    if (fused && fused[0] == '1') c->fused = true;
-    const char* f13 = getenv("FB_FUSE13");
-    if (f13 && f13[0] == '0') c->fuse13 = false;
-    const char* p0 = getenv("FB_P0MID");
-    if (p0) c->phase0_mid = p0[0] == '1';
-    const char* hy = getenv("FB_HYROWS");
-    if (hy) c->tgt_reg_rows = atoi(hy);
-    const char* sf10 = getenv("FB_SF10");
-    sf10_enabled = !(sf10 && sf10[0] == '0');
     c->device = device;
     c->stream = static_cast<cudaStream_t>(cuda_stream);
     *out = c;
@@ -1143,6 +1137,22 @@ fb_status fb_set_max_batch_pairs(fb_ctx ctx, int64_t max_pairs)
 {
     if (!ctx || max_pairs < 0) return FB_ERR_INVALID_ARG;
     ctx->max_pairs = max_pairs;
+    return FB_OK;
+}
+
+fb_status fb_set_option(fb_ctx ctx, int option, int value)
+{
+    if (!ctx) return FB_ERR_INVALID_ARG;
+    switch (option) {
+    case FB_OPT_FUSED_ITER: ctx->fused = value != 0; break;
+    case FB_OPT_FUSE13: ctx->fuse13 = value != 0; break;
+    case FB_OPT_PHASE0_MID: ctx->phase0_mid = value != 0; break;
+    case FB_OPT_TGT_REG_ROWS:
+        if (value < 0 || value > 2) { ctx->err = "tgt_reg_rows must be 0, 1 or 2"; return FB_ERR_INVALID_ARG; }
+        ctx->tgt_reg_rows = value;
+        break;
+    default: ctx->err = "unknown option"; return FB_ERR_INVALID_ARG;
+    }
     return FB_OK;
 }
 
@@ -1396,10 +1406,13 @@ size_t fb_workspace_size(fb_ctx ctx, int op, const fb_match_cfg* cfg, int n, int
     std::string saved = ctx->err;
     fb_status s = FB_OK;
     if (op == FB_OP_NNF) {
+        // worst case: every MEAN_ALIGN pair its own group (one packed T-bar target per group)
         std::vector<fb_pair_key> keys(n, fb_pair_key{0, 0, 6});
         std::vector<int32_t> grp(n, 0);
-        if (cfg->loss == FB_LOSS_PAIRWISE)
-            for (int b = 0; b < n; ++b) grp[b] = (b ^ 1) < n ? (b ^ 1) : b;
+        for (int b = 0; b < n; ++b) {
+            grp[b] = cfg->loss == FB_LOSS_PAIRWISE ? ((b ^ 1) < n ? (b ^ 1) : b) : b;
+            keys[b].tgt_id = b;
+        }
         s = guarded(ctx, nullptr, [&](Exec& ex, fb_stats* st) {
             validate_cfg(cfg);
             const Geo g = make_geo(*cfg, H, W);

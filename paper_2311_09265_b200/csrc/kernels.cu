@@ -13,6 +13,8 @@
 // are bit-identical to the contract regardless of scheduling or thread mapping.
 #include "kernels.h"
 
+#include <algorithm>
+
 namespace fbk {
 
 static constexpr int TILE_X = 32, TILE_Y = 8;  // 256-thread 2D tiles: a warp is one row segment
@@ -1337,43 +1339,66 @@ static inline dim3 grid1d(long long n, int y, int threads = 256)
     return dim3((unsigned)b, (unsigned)y);
 }
 
+// Launches with one grid row per frame / task / output (blockIdx.y) are split into chunks of at most 65535
+// rows (the grid.y limit), each with its base pointers advanced by the chunk's first row.
+constexpr int kMaxGridY = 65535;
+template <class Launch>
+static cudaError_t for_y_chunks(long long n, Launch&& launch)
+{
+    for (long long y0 = 0; y0 < n; y0 += kMaxGridY) {
+        launch(y0, (int)std::min<long long>(kMaxGridY, n - y0));
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t launch_u8_to_pyr0(const uint8_t* frames, float4* pyr, int Bn, int H, int W, long long pyr_stride,
                               cudaStream_t s)
 {
-    k_u8_to_pyr0<<<grid1d((long long)H * W, Bn), 256, 0, s>>>(frames, pyr, H * W, pyr_stride);
-    return cudaGetLastError();
+    return for_y_chunks(Bn, [&](long long y0, int n) {
+        k_u8_to_pyr0<<<grid1d((long long)H * W, n), 256, 0, s>>>(frames + y0 * 3LL * H * W, pyr + y0 * pyr_stride, H * W,
+                                                              pyr_stride);
+    });
 }
 
 cudaError_t launch_box(float4* pyr, int Bn, long long pyr_stride, Lvl prev, Lvl cur, cudaStream_t s)
 {
-    k_box<<<grid1d((long long)cur.h * cur.w, Bn), 256, 0, s>>>(pyr, pyr_stride, prev, cur);
-    return cudaGetLastError();
+    return for_y_chunks(Bn, [&](long long y0, int n) {
+        k_box<<<grid1d((long long)cur.h * cur.w, n), 256, 0, s>>>(pyr + y0 * pyr_stride, pyr_stride, prev, cur);
+    });
 }
 
 cudaError_t launch_pack_src(const PackSrc* jobs, int n, int fmt, PLvl L, cudaStream_t s)
 {
     if (n <= 0) return cudaSuccess;
-    k_pack_src<<<grid1d((long long)L.rows * L.pitch * (fmt == SF8 ? kSF8Copies : 1), n), 256, 0, s>>>(jobs, fmt, L);
-    return cudaGetLastError();
+    const int copies = (fmt == SF8 || fmt == SF10) ? kSF8Copies : 1;
+    return for_y_chunks(n, [&](long long y0, int m) {
+        k_pack_src<<<grid1d((long long)L.rows * L.pitch * copies, m), 256, 0, s>>>(jobs + y0, fmt, L);
+    });
 }
 
 cudaError_t launch_pack_tgt_guide(const DTask* tasks, int T, Lvl L, PLvl P, int tfmt, cudaStream_t s)
 {
-    k_pack_tgt_guide<<<grid1d((long long)P.rows * P.pitch, T), 256, 0, s>>>(tasks, L, P, tfmt);
-    return cudaGetLastError();
+    return for_y_chunks(T, [&](long long y0, int n) {
+        k_pack_tgt_guide<<<grid1d((long long)P.rows * P.pitch, n), 256, 0, s>>>(tasks + y0, L, P, tfmt);
+    });
 }
 
 cudaError_t launch_init(const DTask* tasks, int T, int2* F, long long fstride, Lvl L, int identity, Rng rng,
                         uint32_t level, cudaStream_t s)
 {
-    k_init<<<grid1d((long long)L.h * L.w, T), 256, 0, s>>>(tasks, F, fstride, L, identity, rng, level);
-    return cudaGetLastError();
+    return for_y_chunks(T, [&](long long y0, int n) {
+        k_init<<<grid1d((long long)L.h * L.w, n), 256, 0, s>>>(tasks + y0, F + y0 * fstride, fstride, L, identity, rng,
+                                                            level);
+    });
 }
 
 cudaError_t launch_upsample(const int2* Fc, int2* Ff, int T, long long fstride, Lvl Lc, Lvl Lf, cudaStream_t s)
 {
-    k_upsample<<<grid1d((long long)Lf.h * Lf.w, T), 256, 0, s>>>(Fc, Ff, fstride, Lc, Lf);
-    return cudaGetLastError();
+    return for_y_chunks(T, [&](long long y0, int n) {
+        k_upsample<<<grid1d((long long)Lf.h * Lf.w, n), 256, 0, s>>>(Fc + y0 * fstride, Ff + y0 * fstride, fstride, Lc, Lf);
+    });
 }
 
 #define FB_DISPATCH_P(p, CALL) \
@@ -1386,49 +1411,62 @@ cudaError_t launch_upsample(const int2* Fc, int2* Ff, int T, long long fstride, 
     }
 
 template <int P>
-static void launch_aux_remap_t(const DTask* tasks, int T, const int2* F, long long fstride, Lvl L, PLvl PL, int tfmt,
-                               int sfmt, long long src_off, cudaStream_t s)
+static cudaError_t launch_aux_remap_t(const DTask* tasks, int T, const int2* F, long long fstride, Lvl L, PLvl PL,
+                                      int tfmt, int sfmt, long long src_off, cudaStream_t s)
 {
-    const dim3 g = grid1d((long long)PL.rows * PL.pitch, T);
-    if (sfmt == SF8) k_aux_remap<P, SF8><<<g, 256, 0, s>>>(tasks, F, fstride, L, PL, tfmt, src_off);
-    else if (sfmt == SF10) k_aux_remap<P, SF10><<<g, 256, 0, s>>>(tasks, F, fstride, L, PL, tfmt, src_off);
-    else if (sfmt == SF16) k_aux_remap<P, SF16><<<g, 256, 0, s>>>(tasks, F, fstride, L, PL, tfmt, src_off);
-    else k_aux_remap<P, -1><<<g, 256, 0, s>>>(tasks, F, fstride, L, PL, tfmt, src_off);
+    return for_y_chunks(T, [&](long long y0, int n) {
+        const dim3 g = grid1d((long long)PL.rows * PL.pitch, n);
+        const DTask* tk = tasks + y0;
+        const int2* Fy = F + y0 * fstride;
+        if (sfmt == SF8) k_aux_remap<P, SF8><<<g, 256, 0, s>>>(tk, Fy, fstride, L, PL, tfmt, src_off);
+        else if (sfmt == SF10) k_aux_remap<P, SF10><<<g, 256, 0, s>>>(tk, Fy, fstride, L, PL, tfmt, src_off);
+        else if (sfmt == SF16) k_aux_remap<P, SF16><<<g, 256, 0, s>>>(tk, Fy, fstride, L, PL, tfmt, src_off);
+        else k_aux_remap<P, -1><<<g, 256, 0, s>>>(tk, Fy, fstride, L, PL, tfmt, src_off);
+    });
 }
 
 cudaError_t launch_aux_remap(const DTask* tasks, int T, const int2* F, long long fstride, Lvl L, PLvl PL, int p,
                              int tfmt, int sfmt, long long src_off, cudaStream_t s)
 {
-    FB_DISPATCH_P(p, (launch_aux_remap_t<PP>(tasks, T, F, fstride, L, PL, tfmt, sfmt, src_off, s)));
-    return cudaGetLastError();
+    cudaError_t e = cudaSuccess;
+    FB_DISPATCH_P(p, (e = launch_aux_remap_t<PP>(tasks, T, F, fstride, L, PL, tfmt, sfmt, src_off, s)));
+    return e;
 }
 
 template <int P>
-static void launch_combine_t(const DOut* outs, int n_outs, const DMember* mem, const int2* F, long long fstride,
-                             int h, int w, int fmt, PLvl PL, cudaStream_t s)
+static cudaError_t launch_combine_t(const DOut* outs, int n_outs, const DMember* mem, const int2* F, long long fstride,
+                                    int h, int w, int fmt, PLvl PL, cudaStream_t s)
 {
-    const dim3 g = grid1d(fmt >= 2 ? (long long)PL.rows * PL.pitch : (long long)h * w, n_outs);
-    switch (fmt) {
-    case 0: k_combine<P, 0><<<g, 256, 0, s>>>(outs, mem, F, fstride, h, w, PL); break;
-    case 1: k_combine<P, 1><<<g, 256, 0, s>>>(outs, mem, F, fstride, h, w, PL); break;
-    case 2: k_combine<P, 2><<<g, 256, 0, s>>>(outs, mem, F, fstride, h, w, PL); break;
-    default: k_combine<P, 3><<<g, 256, 0, s>>>(outs, mem, F, fstride, h, w, PL); break;
-    }
+    return for_y_chunks(n_outs, [&](long long y0, int n) {  // member task indices stay absolute (F is not offset)
+        const dim3 g = grid1d(fmt >= 2 ? (long long)PL.rows * PL.pitch : (long long)h * w, n);
+        const DOut* o = outs + y0;
+        switch (fmt) {
+        case 0: k_combine<P, 0><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); break;
+        case 1: k_combine<P, 1><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); break;
+        case 2: k_combine<P, 2><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); break;
+        default: k_combine<P, 3><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); break;
+        }
+    });
 }
 
 cudaError_t launch_combine(const DOut* outs, int n_outs, const DMember* mem, const int2* F, long long fstride,
                            int h, int w, int p, int fmt, PLvl PL, cudaStream_t s)
 {
     if (n_outs <= 0) return cudaSuccess;
-    FB_DISPATCH_P(p, (launch_combine_t<PP>(outs, n_outs, mem, F, fstride, h, w, fmt, PL, s)));
-    return cudaGetLastError();
+    cudaError_t e = cudaSuccess;
+    FB_DISPATCH_P(p, (e = launch_combine_t<PP>(outs, n_outs, mem, F, fstride, h, w, fmt, PL, s)));
+    return e;
 }
 
 cudaError_t launch_remap_f3(const float* src, const int2* F, float* out, int Bn, int H, int W, int p,
                             cudaStream_t s)
 {
-    FB_DISPATCH_P(p, (k_remap_f3<PP><<<grid1d((long long)H * W, Bn), 256, 0, s>>>(src, F, out, H, W)));
-    return cudaGetLastError();
+    const long long n = (long long)H * W;
+    cudaError_t e = cudaSuccess;
+    FB_DISPATCH_P(p, (e = for_y_chunks(Bn, [&](long long y0, int m) {
+        k_remap_f3<PP><<<grid1d(n, m), 256, 0, s>>>(src + 3 * y0 * n, F + y0 * n, out + 3 * y0 * n, H, W);
+    })));
+    return e;
 }
 
 template <int P, bool TWO, int SFMT, bool PW = false>

@@ -7,6 +7,7 @@ fb_blend_window, fb_interpolate_keyframes).
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 from dataclasses import dataclass
@@ -19,13 +20,14 @@ BASE, GUIDE_STYLE, MEAN_ALIGN, PAIRWISE = 0, 1, 2, 3
 DIRECT, TREE = 0, 1
 INIT_RANDOM, INIT_IDENTITY = 0, 1
 OP_NNF, OP_BLEND_DIRECT, OP_BLEND_TREE, OP_INTERPOLATE = 0, 1, 2, 3
+OPT_FUSED_ITER, OPT_FUSE13, OPT_PHASE0_MID, OPT_TGT_REG_ROWS = 0, 1, 2, 3
 TAG_DIRECT, TAG_TREE_BUILD_F, TAG_TREE_QUERY_F, TAG_TREE_BUILD_R, TAG_TREE_QUERY_R, TAG_INTERP, TAG_API = range(7)
 
 STATUS = {0: "FB_OK", 1: "FB_ERR_INVALID_ARG", 2: "FB_ERR_SHAPE", 3: "FB_ERR_CUDA", 4: "FB_ERR_NCCL",
           5: "FB_ERR_WORKSPACE", 6: "FB_ERR_UNSUPPORTED"}
 
 SYMBOLS = ["fb_ctx_create", "fb_ctx_destroy", "fb_last_error", "fb_set_workspace", "fb_set_max_batch_pairs",
-           "fb_workspace_size", "fb_workspace_size_range", "fb_launch_count", "fb_pyramid_elems", "fb_build_pyramid", "fb_nnf_estimate",
+           "fb_workspace_size", "fb_workspace_size_range", "fb_launch_count", "fb_set_option", "fb_pyramid_elems", "fb_build_pyramid", "fb_nnf_estimate",
            "fb_remap", "fb_blend_window", "fb_blend_window_range", "fb_interpolate_keyframes", "fb_profile_enable",
            "fb_profile_read", "fb_profile_reset", "fb_tree_cell_texels", "fb_tree_build_cells", "fb_tree_query",
            "fb_interpolate_keyframes_range"]
@@ -107,6 +109,7 @@ def load_library(build_if_missing: bool = True):
     lib.fb_workspace_size.restype = C.c_size_t
     lib.fb_workspace_size_range.argtypes = [V, C.c_int, P(_Cfg)] + [C.c_int] * 8
     lib.fb_workspace_size_range.restype = C.c_size_t
+    lib.fb_set_option.argtypes = [V, C.c_int, C.c_int]
     lib.fb_launch_count.argtypes = [V]
     lib.fb_launch_count.restype = C.c_uint64
     lib.fb_pyramid_elems.argtypes = [C.c_int] * 4
@@ -130,7 +133,7 @@ def load_library(build_if_missing: bool = True):
     lib.fb_profile_read.restype = C.c_int
     lib.fb_profile_reset.argtypes = [V]
     lib.fb_profile_reset.restype = None
-    for fn in ("fb_profile_enable", "fb_ctx_create", "fb_set_workspace", "fb_set_max_batch_pairs", "fb_build_pyramid", "fb_nnf_estimate",
+    for fn in ("fb_set_option", "fb_profile_enable", "fb_ctx_create", "fb_set_workspace", "fb_set_max_batch_pairs", "fb_build_pyramid", "fb_nnf_estimate",
                "fb_remap", "fb_blend_window", "fb_blend_window_range", "fb_interpolate_keyframes"):
         getattr(lib, fn).restype = C.c_int
     _lib = lib
@@ -167,6 +170,26 @@ class Context:
         if max_batch_pairs:
             self.set_max_batch_pairs(max_batch_pairs)
 
+    @contextlib.contextmanager
+    def _ordered(self):
+        """Orders the context stream after the caller's current stream (inputs copied, outputs and workspace
+        allocated there) and the current stream after the context stream (outputs ready, buffers safe to free
+        or reuse there).  A no-op when the context enqueues on the current stream."""
+        cur = torch.cuda.current_stream(self.device)
+        if cur == self.stream:
+            yield
+            return
+        self.stream.wait_stream(cur)
+        try:
+            yield
+        finally:
+            cur.wait_stream(self.stream)
+
+    def _run(self, status_fn, *args):
+        with self._ordered():
+            status = status_fn(self.h, *args)
+        self._check(status)
+
     def _check(self, status: int, h=None):
         if status != 0:
             msg = self.lib.fb_last_error(h if h is not None else self.h)
@@ -185,6 +208,10 @@ class Context:
 
     def set_max_batch_pairs(self, n: int):
         self._check(self.lib.fb_set_max_batch_pairs(self.h, int(n)))
+
+    def set_option(self, option: int, value: int):
+        """fb_set_option: an equivalent kernel schedule (OPT_*; results are bit-identical for every value)."""
+        self._check(self.lib.fb_set_option(self.h, int(option), int(value)))
 
     def launch_count(self) -> int:
         return int(self.lib.fb_launch_count(self.h))
@@ -211,8 +238,10 @@ class Context:
         if nbytes <= 0:  # invalid arguments: the entry point itself reports the precise status
             return
         if self.ws is None or self.ws.numel() < nbytes:
-            self.ws = None
+            self.ws = None  # freed on its allocation stream, which waited for this context's last call (_ordered)
             self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            if self.stream != torch.cuda.current_stream(self.device):
+                self.ws.record_stream(self.stream)
             self._check(self.lib.fb_set_workspace(self.h, C.c_void_p(self.ws.data_ptr()), self.ws.numel()))
 
     # ------------------------------------------------------------------------------ entry points
@@ -221,7 +250,7 @@ class Context:
         B, H, W, _ = frames.shape
         n = int(self.lib.fb_pyramid_elems(B, H, W, levels))
         out = torch.empty(n, dtype=torch.float32, device=self.device)
-        self._check(self.lib.fb_build_pyramid(self.h, _ptr(frames), B, H, W, levels, _ptr(out)))
+        self._run(self.lib.fb_build_pyramid, _ptr(frames), B, H, W, levels, _ptr(out))
         return out.view(B, -1, 4)
 
     def fb_nnf_estimate(self, cfg: MatchCfg, src_guide, tgt_guide, src_style=None, tgt_style=None, group=None,
@@ -242,8 +271,8 @@ class Context:
         rem = torch.empty((B, H, W, 3), dtype=torch.float32, device=self.device) if want_remap and ss is not None else None
         st = _Stats()
         c = cfg.c()
-        self._check(self.lib.fb_nnf_estimate(self.h, C.byref(c), B, H, W, _ptr(sg), _ptr(tg), _ptr(ss), _ptr(ts),
-                                             grp, keys, _ptr(nnf), _ptr(err), _ptr(rem), C.byref(st)))
+        self._run(self.lib.fb_nnf_estimate, C.byref(c), B, H, W, _ptr(sg), _ptr(tg), _ptr(ss), _ptr(ts),
+                                             grp, keys, _ptr(nnf), _ptr(err), _ptr(rem), C.byref(st))
         return nnf, err, rem, st.as_dict()
 
     def fb_remap(self, src: torch.Tensor, nnf: torch.Tensor, p: int) -> torch.Tensor:
@@ -251,7 +280,7 @@ class Context:
         nnf = _dev(nnf, self.device, torch.int32)
         B, H, W, _ = src.shape
         out = torch.empty_like(src)
-        self._check(self.lib.fb_remap(self.h, B, H, W, p, _ptr(src), _ptr(nnf), _ptr(out)))
+        self._run(self.lib.fb_remap, B, H, W, p, _ptr(src), _ptr(nnf), _ptr(out))
         return out
 
     def fb_blend_window(self, cfg: MatchCfg, schedule: int, guide, style, M: int, out: torch.Tensor | None = None):
@@ -265,8 +294,8 @@ class Context:
             out = torch.empty((N, H, W, 3), dtype=torch.float32, device=self.device)
         st = _Stats()
         c = cfg.c()
-        self._check(self.lib.fb_blend_window(self.h, C.byref(c), schedule, N, H, W, M, _ptr(g), _ptr(s), _ptr(out),
-                                             C.byref(st)))
+        self._run(self.lib.fb_blend_window, C.byref(c), schedule, N, H, W, M, _ptr(g), _ptr(s), _ptr(out),
+                                             C.byref(st))
         return out, st.as_dict()
 
     # ---- sharded tree schedule with cell exchange (include/fb.h) -------------------------
@@ -290,13 +319,13 @@ class Context:
         arr, n = self._cells(cells)
         c = cfg.c()
         need = C.c_size_t(0)
-        self._check(self.lib.fb_tree_build_cells(self.h, C.byref(c), N_total, f0, N, H, W, _ptr(g), _ptr(s), n, arr,
-                                                  None, None, C.byref(need)))
+        self._run(self.lib.fb_tree_build_cells, C.byref(c), N_total, f0, N, H, W, _ptr(g), _ptr(s), n, arr,
+                                                  None, None, C.byref(need))
         self.ensure_workspace(int(need.value))
         out = torch.empty((n, self.tree_cell_texels(cfg, H, W), 4), dtype=torch.float32, device=self.device)
         st = _Stats()
-        self._check(self.lib.fb_tree_build_cells(self.h, C.byref(c), N_total, f0, N, H, W, _ptr(g), _ptr(s), n, arr,
-                                                  _ptr(out), C.byref(st), None))
+        self._run(self.lib.fb_tree_build_cells, C.byref(c), N_total, f0, N, H, W, _ptr(g), _ptr(s), n, arr,
+                                                  _ptr(out), C.byref(st), None)
         return out, st.as_dict()
 
     def fb_tree_query(self, cfg: MatchCfg, N_total: int, f0: int, guide, style, M: int, t0: int, t1: int, cells,
@@ -314,14 +343,14 @@ class Context:
         ptrs = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in tens])
         c = cfg.c()
         need = C.c_size_t(0)
-        self._check(self.lib.fb_tree_query(self.h, C.byref(c), N_total, f0, N, H, W, M, _ptr(g), _ptr(s), t0, t1, n,
-                                            arr, ptrs, None, None, C.byref(need)))
+        self._run(self.lib.fb_tree_query, C.byref(c), N_total, f0, N, H, W, M, _ptr(g), _ptr(s), t0, t1, n,
+                                            arr, ptrs, None, None, C.byref(need))
         self.ensure_workspace(int(need.value))
         if out is None:
             out = torch.empty((t1 - t0, H, W, 3), dtype=torch.float32, device=self.device)
         st = _Stats()
-        self._check(self.lib.fb_tree_query(self.h, C.byref(c), N_total, f0, N, H, W, M, _ptr(g), _ptr(s), t0, t1, n,
-                                            arr, ptrs, _ptr(out), C.byref(st), None))
+        self._run(self.lib.fb_tree_query, C.byref(c), N_total, f0, N, H, W, M, _ptr(g), _ptr(s), t0, t1, n,
+                                            arr, ptrs, _ptr(out), C.byref(st), None)
         return out, st.as_dict()
 
     def fb_blend_window_range(self, cfg: MatchCfg, schedule: int, N_total: int, f0: int, guide, style, M: int,
@@ -337,8 +366,8 @@ class Context:
             out = torch.empty((t1 - t0, H, W, 3), dtype=torch.float32, device=self.device)
         st = _Stats()
         c = cfg.c()
-        self._check(self.lib.fb_blend_window_range(self.h, C.byref(c), schedule, N_total, f0, N, H, W, M, _ptr(g),
-                                                    _ptr(s), t0, t1, _ptr(out), C.byref(st)))
+        self._run(self.lib.fb_blend_window_range, C.byref(c), schedule, N_total, f0, N, H, W, M, _ptr(g),
+                                                    _ptr(s), t0, t1, _ptr(out), C.byref(st))
         return out, st.as_dict()
 
     def fb_interpolate_keyframes(self, cfg: MatchCfg, guide, key_index, key_style, out: torch.Tensor | None = None):
@@ -353,8 +382,8 @@ class Context:
         ki = (C.c_int32 * max(K, 1))(*keys)
         st = _Stats()
         c = cfg.c()
-        self._check(self.lib.fb_interpolate_keyframes(self.h, C.byref(c), N, H, W, _ptr(g), K, ki, _ptr(ks), _ptr(out),
-                                                      C.byref(st)))
+        self._run(self.lib.fb_interpolate_keyframes, C.byref(c), N, H, W, _ptr(g), K, ki, _ptr(ks), _ptr(out),
+                                                      C.byref(st))
         return out, st.as_dict()
 
 
@@ -370,14 +399,14 @@ class Context:
         ki = (C.c_int32 * max(K, 1))(*keys)
         c = cfg.c()
         need = C.c_size_t(0)
-        self._check(self.lib.fb_interpolate_keyframes_range(self.h, C.byref(c), N, H, W, t0, t1, _ptr(g), K, ki, _ptr(kg),
-                                                            _ptr(ks), None, None, C.byref(need)))
+        self._run(self.lib.fb_interpolate_keyframes_range, C.byref(c), N, H, W, t0, t1, _ptr(g), K, ki, _ptr(kg),
+                                                            _ptr(ks), None, None, C.byref(need))
         self.ensure_workspace(int(need.value))
         if out is None:
             out = torch.empty((t1 - t0, H, W, 3), dtype=torch.float32, device=self.device)
         st = _Stats()
-        self._check(self.lib.fb_interpolate_keyframes_range(self.h, C.byref(c), N, H, W, t0, t1, _ptr(g), K, ki, _ptr(kg),
-                                                            _ptr(ks), _ptr(out), C.byref(st), None))
+        self._run(self.lib.fb_interpolate_keyframes_range, C.byref(c), N, H, W, t0, t1, _ptr(g), K, ki, _ptr(kg),
+                                                            _ptr(ks), _ptr(out), C.byref(st), None)
         return out, st.as_dict()
 
 

@@ -3,7 +3,9 @@
 One process per GPU.  Output targets are split into contiguous ranges balanced by NNF pair count (not
 frame count); rank g owns targets [t0, t1) and needs input frames [t0 - M, t1 + M) clipped to the video.
 Each rank holds only its own frames; the halo frames are the one real exchange step of the path and
-move with torch.distributed point-to-point ops (NCCL over NVLink on the GPU box, gloo in CPU tests).
+move with torch.distributed point-to-point ops (NCCL over NVLink on the GPU box; gloo -- host-staged for
+device tensors -- in the CPU tests and the world-2-on-one-GPU correctness runs).  Reading D43:
+the exchange transport is torch.distributed, not an fb_group inside the C ABI.
 After the exchange the shards are independent: each calls fb_blend_window_range on its local frames.
 Pair-keyed RNG (D21) makes the result identical for every world size.
 """
@@ -91,6 +93,39 @@ def owner_of(plan: list[tuple[int, int]], f: int) -> int:
     raise ValueError(f"frame {f} not owned")
 
 
+def _host_staged(group=None) -> bool:
+    """gloo moves CPU tensors only: device tensors are staged through host memory (the world-2-on-one-GPU
+    correctness runs; on the 8-GPU box the backend is NCCL and tensors move device to device)."""
+    return dist.get_backend(group) == "gloo"
+
+
+def _p2p(ops: list, group=None):
+    """batch_isend_irecv of (op, tensor, peer) triples; with host staging, device tensors are copied to pinned
+    host buffers for the transfer and received ones copied back."""
+    if not ops:
+        return
+    staged = _host_staged(group)
+    real, back = [], []
+    for op, t, peer in ops:
+        if staged and t.is_cuda:
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            if op is dist.isend:
+                h.copy_(t)
+            else:
+                back.append((t, h))
+            t = h
+        real.append(dist.P2POp(op, t, _global(peer, group), group))
+    for r in dist.batch_isend_irecv(real):
+        r.wait()
+    for t, h in back:
+        t.copy_(h, non_blocking=True)
+
+
+def _global(g: int, group=None) -> int:
+    """Plan index (rank within `group`) -> global rank, as torch.distributed's P2P and broadcast expect."""
+    return g if group is None else dist.get_global_rank(group, g)
+
+
 def halo_exchange(owned: list[torch.Tensor], plan: list[tuple[int, int]], N: int, M: int, rank: int,
                   group=None) -> tuple[list[torch.Tensor], int]:
     """owned: tensors [t1-t0, ...] of this rank's frames (same plan for every tensor, e.g. guide and
@@ -113,7 +148,7 @@ def halo_exchange(owned: list[torch.Tensor], plan: list[tuple[int, int]], N: int
         lo, hi = max(a, f0), min(b, f1)
         if lo < hi:
             for loc in locals_:
-                ops.append(dist.P2POp(dist.irecv, loc[lo - f0:hi - f0], g, group))
+                ops.append((dist.irecv, loc[lo - f0:hi - f0], g))
     # sends: for every peer, the intersection of its halo with my owned range
     for g in range(world):
         if g == rank:
@@ -123,12 +158,22 @@ def halo_exchange(owned: list[torch.Tensor], plan: list[tuple[int, int]], N: int
         lo, hi = max(t0, pf0), min(t1, pf1)
         if lo < hi:
             for x in owned:
-                ops.append(dist.P2POp(dist.isend, x[lo - t0:hi - t0].contiguous(), g, group))
-    if ops:
-        with _nvtx("halo exchange"):
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
+                ops.append((dist.isend, x[lo - t0:hi - t0].contiguous(), g))
+    with _nvtx("halo exchange"):
+        _p2p(ops, group)
     return locals_, f0
+
+
+def blend_direct_sharded(ctx, cfg, plan: list[tuple[int, int]], N: int, M: int, rank: int, guide_own, style_own,
+                         out=None, group=None):
+    """Direct schedule (balanced / accurate) of this rank's targets: halo exchange, then fb_blend_window_range
+    on the local frames.  A rank with an empty range takes part in the exchange and returns (None, {})."""
+    t0, t1 = plan[rank]
+    (g_loc, s_loc), f0 = halo_exchange([guide_own, style_own], plan, N, M, rank, group)
+    if t1 <= t0:
+        return None, {}
+    from .fb import DIRECT
+    return ctx.fb_blend_window_range(cfg, DIRECT, N, f0, g_loc, s_loc, M, t0, t1, out=out)
 
 
 # ---------------------------------------------------------------------------------------------- tree
@@ -184,16 +229,14 @@ def exchange_cells(plan: list[tuple[int, int]], N: int, M: int, rank: int, built
         a, b = plan[g]
         theirs = [c for c in tree_cells_needed(N, M, a, b) if owner_of(plan, cell_frame(N, c)) == rank] if b > a else []
         if theirs:
-            ops.append(dist.P2POp(dist.isend, torch.stack([built[c] for c in theirs]).contiguous(), g, group))
+            ops.append((dist.isend, torch.stack([built[c] for c in theirs]).contiguous(), g))
         from_g = [c for c in mine if owner[c] == g]
         if from_g:
             buf = torch.empty((len(from_g), texels, 4), dtype=torch.float32, device=device)
-            ops.append(dist.P2POp(dist.irecv, buf, g, group))
+            ops.append((dist.irecv, buf, g))
             recv[g] = (from_g, buf)
-    if ops:
-        with _nvtx("tree cell exchange"):
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
+    with _nvtx("tree cell exchange"):
+        _p2p(ops, group)
     cells = {c: built[c] for c in mine if owner[c] == rank}
     for from_g, buf in recv.values():
         for k, c in enumerate(from_g):
@@ -222,6 +265,8 @@ def blend_tree_exchange(ctx, cfg, plan: list[tuple[int, int]], N: int, M: int, r
         T, st_b = ctx.fb_tree_build_cells(cfg, N, f0, guide_loc, style_loc, build)
         built = {c: T[k] for k, c in enumerate(build)}
     cells = exchange_cells(plan, N, M, rank, built, texels, guide_loc.device, group)
+    if t1 <= t0:  # an empty range builds and sends nothing, and has no queries
+        return None, st_b
     order = sorted(cells)
     out, st_q = ctx.fb_tree_query(cfg, N, f0, guide_loc, style_loc, M, t0, t1, order, [cells[c] for c in order],
                                   out=out)
@@ -261,11 +306,21 @@ def _broadcast_keyframes(plan, keys, rank, guide_own, key_style, group):
         src = owner_of(plan, f)
         if src == rank:
             kg[k].copy_(guide_own[f - t0])
-        dist.broadcast(kg[k], src, group)
+        _broadcast(kg[k], src, group)
     ks = key_style.contiguous() if rank == 0 else torch.empty((K,) + shape, dtype=guide_own.dtype,
                                                               device=guide_own.device)
-    dist.broadcast(ks, 0, group)
+    _broadcast(ks, 0, group)
     return kg, ks
+
+
+def _broadcast(t: torch.Tensor, src: int, group=None):
+    """dist.broadcast from plan index `src` (host-staged under gloo, like _p2p)."""
+    if _host_staged(group) and t.is_cuda:
+        h = t.cpu()
+        dist.broadcast(h, _global(src, group), group)
+        t.copy_(h)
+    else:
+        dist.broadcast(t, _global(src, group), group)
 
 
 def interpolate_sharded(ctx, cfg, plan: list[tuple[int, int]], N: int, keys: list[int], rank: int,

@@ -71,8 +71,12 @@ def _quant(x: np.ndarray) -> np.ndarray:
     return np.clip(np.rint(x), 0, 255).astype(np.uint8)  # np.rint = round-half-even
 
 
-def moving_texture(N: int, H: int, W: int, seed: int = SEED_VIDEO, n_sprites: int = 4):
-    """(guide, style) uint8 [N, H, W, 3] — the synthetic workload of DESIGN.md §5."""
+def moving_texture(N: int, H: int, W: int, seed: int = SEED_VIDEO, n_sprites: int = 4, t0: int = 0,
+                   t1: int | None = None):
+    """(guide, style) uint8 [N, H, W, 3] — the synthetic workload of DESIGN.md §5.  With t0/t1 only frames
+    [t0, t1) of the N-frame video are generated (identical to the same rows of the full call: a frame depends
+    only on its index and the video-wide draws), so a shard can build just its own frames."""
+    t1 = N if t1 is None else t1
     rng = np.random.default_rng(seed)
     v = rng.uniform(-1.5, 1.5, size=2)
     span = np.abs(v) * max(N - 1, 0)
@@ -95,9 +99,9 @@ def moving_texture(N: int, H: int, W: int, seed: int = SEED_VIDEO, n_sprites: in
     gamma = rng.uniform(0.6, 1.6, size=3)
     contrast = rng.uniform(0.8, 1.3, size=3)
     rot = int(rng.integers(1, 3))
-    guide = np.empty((N, H, W, 3), np.uint8)
-    style = np.empty((N, H, W, 3), np.uint8)
-    for t in range(N):
+    guide = np.empty((t1 - t0, H, W, 3), np.uint8)
+    style = np.empty((t1 - t0, H, W, 3), np.uint8)
+    for t in range(t0, t1):
         o_r = pad_r + int(np.rint(v[0] * t))
         o_c = pad_c + int(np.rint(v[1] * t))
         frame = canvas[o_r:o_r + H, o_c:o_c + W].copy()
@@ -113,14 +117,14 @@ def moving_texture(N: int, H: int, W: int, seed: int = SEED_VIDEO, n_sprites: in
             frame[y0:y1, x0:x1][sub_m] = sub_t[sub_m]
         frame = frame * (1.0 + 0.02 * np.sin(2 * np.pi * t / 50.0))
         g = _quant(frame)
-        guide[t] = g
+        guide[t - t0] = g
         x = g.astype(np.float64) / 255.0
         s = 255.0 * np.clip((x ** gamma - 0.5) * contrast + 0.5, 0, 1)
         s = np.roll(s, rot, axis=2)
         frng = np.random.default_rng([seed, t])
         field = _bilinear(frng.uniform(-25, 25, size=(8 + 1, 8 + 1, 3)), H, W, H / 8.0)
         s = s + field + frng.uniform(-4, 4, size=s.shape)
-        style[t] = _quant(s)
+        style[t - t0] = _quant(s)
     return guide, style
 
 

@@ -199,19 +199,26 @@ def test_constant_and_static_videos(fb, ctx):
 
 @pytest.mark.parametrize("mode", ["balanced", "accurate", "fast"])
 def test_batching_and_sharding_invariance(fb, mode):
+    """Streaming (f4: batches of <= max_batch_pairs pairs, each with only its frames resident) and the
+    shard entry point, every form against the oracle (not only against the single-batch GPU run)."""
     g, s = moving_texture(10, 40, 40, seed=31)
     loss = fb.MEAN_ALIGN if mode == "accurate" else fb.GUIDE_STYLE
     sched = fb.TREE if mode == "fast" else fb.DIRECT
     cfg = fb.MatchCfg(iters_per_level=1, loss=loss)
     M = 3
-    full, _ = fb.Context(0).fb_blend_window(cfg, sched, dev(g), dev(s), M)
-    small, _ = fb.Context(0, max_batch_pairs=5).fb_blend_window(cfg, sched, dev(g), dev(s), M)
-    assert torch.equal(full, small)
-    ctx = fb.Context(0)
+    ref, pairs, evals = (O.blend_tree if mode == "fast" else O.blend_direct)(ocfg(cfg), g, s, M)
+    full, st = fb.Context(0).fb_blend_window(cfg, sched, dev(g), dev(s), M)
+    assert st["nnf_pairs"] == pairs and st["candidate_evals"] == evals
+    assert_frames(full, ref)
+    for cap in (1, 5):
+        small, st = fb.Context(0, max_batch_pairs=cap).fb_blend_window(cfg, sched, dev(g), dev(s), M)
+        assert st["nnf_pairs"] == pairs
+        assert_frames(small, ref)
+    ctx = fb.Context(0, max_batch_pairs=4)
     for t0, t1 in ((0, 4), (4, 7), (7, 10)):
         f0, f1 = max(0, t0 - M), min(10, t1 + M)
         part, _ = ctx.fb_blend_window_range(cfg, sched, 10, f0, dev(g[f0:f1]), dev(s[f0:f1]), M, t0, t1)
-        assert torch.equal(part, full[t0:t1])
+        assert_frames(part, ref[t0:t1])
 
 
 # ------------------------------------------------------------------------------ a11 interpolation
@@ -329,7 +336,7 @@ def test_tracking_interpolation_parity(fb, ctx, keys, align):
 
 # ------------------------------------------------------------------------------ schedule invariance / races
 @pytest.mark.parametrize("mode", ["accurate", "fast"])
-def test_fused_fields_equal_per_field_launches(fb, mode, monkeypatch):
+def test_fused_fields_equal_per_field_launches(fb, mode):
     """k_iter13_fast (fields 1-3 + random search in one launch, halo lanes) must equal the per-field launches
     (P:76 Jacobi fields) bit for bit, on every repetition: its halo lanes read the field-0 E of pixels owned
     by other tiles, so it must never write E in place (a timing-dependent race that this test repeats)."""
@@ -337,9 +344,9 @@ def test_fused_fields_equal_per_field_launches(fb, mode, monkeypatch):
     loss = fb.MEAN_ALIGN if mode == "accurate" else fb.GUIDE_STYLE
     sched = fb.TREE if mode == "fast" else fb.DIRECT
     cfg = fb.MatchCfg(iters_per_level=3, loss=loss)
-    monkeypatch.setenv("FB_FUSE13", "0")
-    ref, _ = fb.Context(0).fb_blend_window(cfg, sched, dev(g), dev(s), 3)
-    monkeypatch.setenv("FB_FUSE13", "1")
+    c0 = fb.Context(0)
+    c0.set_option(fb.fb.OPT_FUSE13, 0)
+    ref, _ = c0.fb_blend_window(cfg, sched, dev(g), dev(s), 3)
     c = fb.Context(0)
     for _ in range(4):
         out, _ = c.fb_blend_window(cfg, sched, dev(g), dev(s), 3)
@@ -371,6 +378,8 @@ def test_tree_cell_exchange_matches_full_blend(fb, N, M, world):
         need = shard.tree_cells_needed(N, M, t0, t1)
         out, _ = ctx.fb_tree_query(cfg, N, f0, dev(g[f0:f1]), dev(s[f0:f1]), M, t0, t1, need, [pool[c] for c in need])
         assert torch.equal(out, full[t0:t1])
+        ref, _, _ = O.blend_tree(ocfg(cfg), g, s, M, targets=list(range(t0, t1)))
+        assert_frames(out, ref)
         if need:  # a query whose cells are incomplete is rejected, not silently wrong
             with pytest.raises(fb.FBError):
                 ctx.fb_tree_query(cfg, N, f0, dev(g[f0:f1]), dev(s[f0:f1]), M, t0, t1, need[1:],
@@ -388,9 +397,12 @@ def test_interpolation_range_equals_full_call(fb, loss):
     cfg = fb.MatchCfg(iters_per_level=2, loss=getattr(fb, loss))
     ctx = fb.Context(0)
     full, _ = ctx.fb_interpolate_keyframes(cfg, dev(g), keys, dev(ks))
+    ref, _, _ = O.interpolate(ocfg(cfg), g, keys, ks)
+    assert_frames(full, ref)
     for t0, t1 in shard.plan_interp_shards(N, keys, 3) + [(2, 3), (5, 6)]:
         part, _ = ctx.fb_interpolate_keyframes_range(cfg, N, t0, t1, dev(g[t0:t1]), keys, dev(g[keys]), dev(ks))
         assert torch.equal(part, full[t0:t1])
+        assert_frames(part, ref[t0:t1])
     cfg_t = fb.MatchCfg(iters_per_level=2, loss=fb.GUIDE_STYLE, tracking=1)
     with pytest.raises(fb.FBError):
         ctx.fb_interpolate_keyframes_range(cfg_t, N, 0, 4, dev(g[0:4]), keys, dev(g[keys]), dev(ks))
@@ -407,3 +419,43 @@ def test_context_on_a_side_stream(fb):
         out, _ = c.fb_blend_window(cfg, fb.DIRECT, dev(g), dev(s), 2)
     side.synchronize()
     assert torch.equal(out, ref)
+
+
+def test_context_stream_differs_from_current_stream(fb):
+    """a context bound to a side stream, called while another stream is current: inputs copied and
+    outputs allocated on the current stream must be ordered with the context's kernels (fb.py _ordered)."""
+    g, s = moving_texture(6, 64, 48, seed=9)
+    cfg = fb.MatchCfg(iters_per_level=2, loss=fb.MEAN_ALIGN)
+    ref, _ = fb.Context(0).fb_blend_window(cfg, fb.DIRECT, dev(g), dev(s), 2)
+    side = torch.cuda.Stream()
+    c = fb.Context(0, stream=side)
+    for _ in range(3):  # host tensors: the H2D copies run on the current stream, the kernels on `side`
+        out, _ = c.fb_blend_window(cfg, fb.DIRECT, torch.from_numpy(g), torch.from_numpy(s), 2)
+        assert torch.equal(out, ref)  # compared on the current stream without an explicit side.synchronize()
+
+
+def test_mean_align_multi_group_fresh_context_workspace(fb):
+    """fb_workspace_size(FB_OP_NNF) must cover one packed T-bar target per MEAN_ALIGN group."""
+    g, s = moving_texture(5, 48, 40, seed=12)
+    sg, tg = np.stack([g[0], g[2], g[1], g[3]]), np.stack([g[1], g[1], g[4], g[4]])
+    ss, ts = np.stack([s[0], s[2], s[1], s[3]]), np.stack([s[1], s[1], s[4], s[4]])
+    cfg = fb.MatchCfg(iters_per_level=2, loss=fb.MEAN_ALIGN)
+    keys = [(0, 1, 0), (2, 1, 0), (1, 4, 0), (3, 4, 0)]
+    F, E, X, st = fb.Context(0).fb_nnf_estimate(cfg, dev(sg), dev(tg), dev(ss), dev(ts), group=[0, 0, 1, 1],
+                                                pair_keys=keys)
+    frames = np.concatenate([g, s]).astype(np.float32)
+    tasks = [dict(src_guide=a, tgt_guide=b, src_style=5 + a, tgt_style=5 + b, group=b, src_id=a, tgt_id=b, tag=0)
+             for a, b, _ in keys]
+    Fr, Er, Xr, ev = O.nnf(ocfg(cfg), frames, tasks)
+    assert st["candidate_evals"] == ev
+    assert_nnf(F, E, Fr, Er)
+    assert_frames(X, Xr)
+
+
+def test_invalid_iteration_and_step_counts_rejected(fb, ctx):
+    """iters_per_level and rs_steps beyond the Philox counter fields (D21) are rejected."""
+    g, s = moving_texture(3, 32, 32)
+    for cfg in (fb.MatchCfg(iters_per_level=1024), fb.MatchCfg(rs_steps=4096)):
+        with pytest.raises(fb.FBError) as e:
+            ctx.fb_blend_window(cfg, fb.DIRECT, dev(g), dev(s), 1)
+        assert e.value.status == 1

@@ -347,6 +347,111 @@ def test_random_init_identical_frames_converges_to_identity():
     assert np.all(E[0] == 0)
 
 
+# ------------------------------------------------------------------ D7 upsample / coarse-to-fine hand-off
+# Alg. 1 "Upsample F".  Pinned by what the mathematics fixes: a field that is the identity at the
+# coarse level is the identity at the fine level (every fine pixel (r, c) lies in the coarse cell (r>>1,
+# c>>1), whose identity match scaled by 2 plus the sub-cell offset is (r, c) itself -- also for the last
+# odd row / column, which reuses the last coarse cell); a constant shift (a, b) becomes the shift (2a, 2b).
+@pytest.mark.parametrize("hc,wc,odd_r,odd_c", [(48, 40, 0, 0), (67, 33, 1, 1), (33, 16, 1, 0), (5, 7, 0, 1)])
+def test_upsample_identity_is_identity(hc, wc, odd_r, odd_c):
+    h, w = 2 * hc + odd_r, 2 * wc + odd_c
+    rr, cc = np.mgrid[0:hc, 0:wc]
+    Ff = O.upsample(np.stack([rr, cc], -1), h, w)
+    fr, fc = np.mgrid[0:h, 0:w]
+    np.testing.assert_array_equal(Ff[..., 0], fr)
+    np.testing.assert_array_equal(Ff[..., 1], fc)
+
+
+@pytest.mark.parametrize("a,b", [(3, -5), (-2, 4), (0, 7)])
+@pytest.mark.parametrize("hc,wc,odd", [(40, 48, 0), (33, 27, 1)])
+def test_upsample_constant_shift_doubles(a, b, hc, wc, odd):
+    """Coarse F(r,c) = (r+a, c+b) (clamped into the coarse grid) upsamples to (r+2a, c+2b) wherever the coarse
+    cell's match was not clamped and the fine match stays inside the image; elsewhere it is clamped into it."""
+    h, w = 2 * hc + odd, 2 * wc + odd
+    rr, cc = np.mgrid[0:hc, 0:wc]
+    Fc = np.stack([np.clip(rr + a, 0, hc - 1), np.clip(cc + b, 0, wc - 1)], -1)
+    Ff = O.upsample(Fc, h, w)
+    fr, fc = np.mgrid[0:h, 0:w]
+    rc, ccc = np.minimum(fr >> 1, hc - 1), np.minimum(fc >> 1, wc - 1)
+    free_r = (rc + a >= 0) & (rc + a <= hc - 1) & (fr + 2 * a >= 0) & (fr + 2 * a <= h - 1)
+    free_c = (ccc + b >= 0) & (ccc + b <= wc - 1) & (fc + 2 * b >= 0) & (fc + 2 * b <= w - 1)
+    assert free_r.mean() > 0.8 and free_c.mean() > 0.7
+    np.testing.assert_array_equal(Ff[..., 0][free_r], (fr + 2 * a)[free_r])
+    np.testing.assert_array_equal(Ff[..., 1][free_c], (fc + 2 * b)[free_c])
+    assert Ff[..., 0].min() >= 0 and Ff[..., 0].max() <= h - 1 and Ff[..., 1].min() >= 0 and Ff[..., 1].max() <= w - 1
+
+
+@pytest.mark.parametrize("hc,wc", [(9, 7), (16, 13)])
+def test_upsample_keeps_matched_patches_coherent(hc, wc):
+    """Linear fields cannot tell which coarse cell a fine pixel inherits from, so a random coarse field
+    pins the structure instead: the 2x2 fine pixels of a coarse cell match a 2x2 block of source pixels
+    anchored at an even position (the x2 of a coarse match), and the last odd row / column continues the
+    block above / to the left by one more pixel (it reuses the last coarse cell, D7) -- properties of the
+    nearest-parent rule, not a re-statement of it.  Values are kept away from the borders: no clamping."""
+    rng = np.random.default_rng(hc * 100 + wc)
+    h, w = 2 * hc + 1, 2 * wc + 1
+    Fc = np.stack([rng.integers(1, hc - 1, (hc, wc)), rng.integers(1, wc - 1, (hc, wc))], -1).astype(np.int32)
+    Ff = O.upsample(Fc, h, w).astype(np.int64)
+    even = Ff[0:2 * hc:2, 0:2 * wc:2]
+    assert np.all(even % 2 == 0)                                   # anchored at 2 x (a coarse match)
+    assert sorted(map(tuple, (even // 2).reshape(-1, 2))) == sorted(map(tuple, Fc.reshape(-1, 2)))
+    for dr in (0, 1):
+        for dc in (0, 1):
+            np.testing.assert_array_equal(Ff[dr:2 * hc:2, dc:2 * wc:2] - even, np.broadcast_to([dr, dc], even.shape))
+    np.testing.assert_array_equal(Ff[2 * hc, :2 * wc] - Ff[2 * hc - 1, :2 * wc], np.broadcast_to([1, 0], (2 * wc, 2)))
+    np.testing.assert_array_equal(Ff[:2 * hc, 2 * wc] - Ff[:2 * hc, 2 * wc - 1], np.broadcast_to([0, 1], (2 * hc, 2)))
+    assert tuple(Ff[2 * hc, 2 * wc] - Ff[2 * hc - 1, 2 * wc - 1]) == (1, 1)
+
+
+@pytest.mark.parametrize("H,W,levels", [(96, 80, 2), (96, 80, 4), (135, 67, 3), (135, 67, 4), (61, 90, 3)])
+def test_identity_init_survives_level_handoffs(H, W, levels):
+    """iters_per_level = 0: Alg. 1 reduces to init at the coarsest level and the upsamples; identity init must
+    come out as the identity at level 0 for even and odd sizes (1080p-like odd chains 135 -> 67 -> 33)."""
+    g = iid_frames(2, H, W, seed=3).astype(np.float32)
+    cfg = O.Cfg(patch_radius=2, levels=levels, iters_per_level=0, loss=O.BASE, init=O.INIT_IDENTITY)
+    F, _, _, ev = O.nnf(cfg, g, [dict(src_guide=0, tgt_guide=1, src_id=0, tgt_id=1)], want_x=False)
+    assert ev == 0
+    rr, cc = np.mgrid[0:H, 0:W]
+    np.testing.assert_array_equal(F[0][..., 0], rr)
+    np.testing.assert_array_equal(F[0][..., 1], cc)
+
+
+@pytest.mark.parametrize("H,W,levels", [(64, 48, 3), (75, 101, 3)])
+def test_random_init_handoff_equals_composed_upsamples(H, W, levels):
+    """iters_per_level = 0 with random init: the level-0 field is the coarsest level's Philox draw (D21 counter:
+    pixel, level << 22, src_id, tag << 28 | tgt_id; drawn here from the KAT-pinned generator) passed through
+    one upsample per level change, in coarse-to-fine order with each level's own dimensions."""
+    g = iid_frames(2, H, W, seed=4).astype(np.float32)
+    seed, src_id, tgt_id, tag = 0x1234567890AB, 3, 9, O.TAG_DIRECT
+    cfg = O.Cfg(patch_radius=2, levels=levels, iters_per_level=0, loss=O.BASE, seed=seed)
+    F, _, _, _ = O.nnf(cfg, g, [dict(src_guide=0, tgt_guide=1, src_id=src_id, tgt_id=tgt_id, tag=tag)], want_x=False)
+    k = levels - 1
+    hk, wk = H >> k, W >> k
+    Fc = np.zeros((hk, wk, 2), np.int32)
+    key = (seed & 0xFFFFFFFF, seed >> 32)
+    for i in range(hk * wk):
+        u = O.philox4x32_10((i, k << 22, src_id, (tag << 28) | tgt_id), key)
+        Fc[i // wk, i % wk] = ((u[0] * hk) >> 32, (u[1] * wk) >> 32)
+    for kk in range(k - 1, -1, -1):
+        Fc = O.upsample(Fc, H >> kk, W >> kk)
+    np.testing.assert_array_equal(F[0], Fc)
+
+
+@pytest.mark.parametrize("H,W,levels", [(48, 40, 3), (135, 67, 3), (96, 80, 4)])
+def test_identical_frames_identity_init_multilevel(H, W, levels):
+    """Identical frames + identity init through several levels with iterations: identity has E = 0 at every
+    level, nothing beats it under the strict select (D16), so F stays the identity and E = 0 at level 0."""
+    t = textured_frame(H, W, seed=8)[None]
+    frames = np.concatenate([t, t, t]).astype(np.float32)
+    cfg = O.Cfg(patch_radius=2, levels=levels, iters_per_level=2, loss=O.GUIDE_STYLE, init=O.INIT_IDENTITY)
+    F, E, X, _ = O.nnf(cfg, frames, [dict(src_guide=0, tgt_guide=1, src_style=2, src_id=0, tgt_id=1)])
+    rr, cc = np.mgrid[0:H, 0:W]
+    np.testing.assert_array_equal(F[0][..., 0], rr)
+    np.testing.assert_array_equal(F[0][..., 1], cc)
+    assert np.all(E[0] == 0)
+    np.testing.assert_array_equal(X[0], frames[2])
+
+
 # ------------------------------------------------------------------ P7 constant video
 def test_constant_video_every_schedule_exact():
     g, s = constant_video(6, 32, 40)
