@@ -38,6 +38,10 @@ struct fb_ctx_s {
                              // kernel (0: register target; 44 vs 163 registers: field0.L0 95 -> 76 ms at N=48)
     int tgt_reg_rows = 2;  // FB_OPT_TGT_REG_ROWS: fused fields 1-3 target rows in registers, rest in shared
                            // memory (0 = all in registers; accurate N=48: field123.L0 413 -> 397 ms)
+    bool l1_fast = false;  // FB_OPT_L1_FAST: level 1 of u8 sources (SF10) through the level-0 kernel structure
+                           // (16-byte TF10 targets, fused fields 1-3 + random search); bit-identical but slower
+                           // (N=48 accurate 683 -> 724 ms: field123.L1 158 ms vs 113 for fields 1-3 of the
+                           // general kernel), so off by default
     std::string err;
     // kernel timing (fb_profile_*)
     bool prof = false;
@@ -362,6 +366,8 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
     // level 0 uses packed u8 operands (TF16 targets) with SF8 / SF8F sources: in registers (fast kernels,
     // p <= 2) or as a shared-memory tile (mid kernel, p = 3, 4)
     const bool fast0 = slots.fmt0 == fbk::SF8 || slots.fmt0 == fbk::SF8F;
+    const bool l1_fast_ok = ex.ctx->l1_fast && slots.fmt0 == fbk::SF8 && g.p == 2 && g.Lv > 1 &&
+                            (cfg.loss == FB_LOSS_GUIDE_STYLE || cfg.loss == FB_LOSS_MEAN_ALIGN);
     BatchOut out;
     out.fstride = n0;
     int2* F[2] = {ex.ar.take<int2>((size_t)T * n0), ex.ar.take<int2>((size_t)T * n0)};
@@ -373,7 +379,8 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
     bool e_final_used = false;
     size_t tbytes = 0;  // one packed target operand, largest level
     for (int k = 0; k < g.Lv; ++k)
-        tbytes = std::max(tbytes, (size_t)g.PL[k].rows * g.PL[k].pitch * ((k == 0 && fast0) ? 16 : 32));
+        tbytes = std::max(tbytes, (size_t)g.PL[k].rows * g.PL[k].pitch *
+                                      (((k == 0 && fast0) || (k == 1 && l1_fast_ok)) ? 16 : 32));
     tbytes = (tbytes + 255) & ~size_t(255);
     const bool per_group = cfg.loss == FB_LOSS_MEAN_ALIGN;
     const bool pairwise = cfg.loss == FB_LOSS_PAIRWISE;
@@ -444,8 +451,10 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
         const fbk::PLvl PL = g.PL[k];
         const bool tf16 = k == 0 && fast0;
         const bool fast = tf16 && g.p <= 2;                 // kernel kind 1
-        const int kind = fast ? 1 : (tf16 ? 2 : 0);        // 2: mid kernel (p = 3, 4)
-        const int tfmt = tf16 ? fbk::TF16 : fbk::TF32;
+        // level 1 of u8 sources: SF10 source + TF10 target through the mid / fused kernels (p = 2)
+        const bool l1 = l1_fast_ok && k == 1;
+        const int kind = fast ? 1 : ((tf16 || l1) ? 2 : 0);  // 2: mid kernel (p = 3, 4 at level 0; level 1)
+        const int tfmt = tf16 ? fbk::TF16 : (l1 ? fbk::TF10 : fbk::TF32);
         if (k == g.Lv - 1) {
             ex.launch("init", [&] { return fbk::launch_init(d_tasks, T, F[cur], n0, L, cfg.init == FB_INIT_IDENTITY,
                                                             rng, (uint32_t)k, s); });
@@ -467,7 +476,7 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
                 if (st) st->remap_pixels += (uint64_t)T * L.h * L.w;
             } else if (per_group) {  // T-bar refresh (Eq. 7, D27)
                 ex.launch(k == 0 ? "tbar.L0" : "tbar.L1+", [&] { return fbk::launch_combine(d_outs[k], (int)groups.size(), d_mem[k], F[cur], n0,
-                                                                   L.h, L.w, g.p, tf16 ? 2 : 3, PL, s); },
+                                                                   L.h, L.w, g.p, tf16 ? 2 : (l1 ? 4 : 3), PL, s); },
                           (uint64_t)T * L.h * L.w);
                 if (st) st->remap_pixels += (uint64_t)T * L.h * L.w;
             }
@@ -494,10 +503,10 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
             for (int j = J - 1; j >= 0; --j) {
                 a.step = 1 << j;
                 const bool last = j == 0;
-                if (last && fast && ex.ctx->fuse13) {  // field 0, then fields 1-3 + random search in one launch
+                if (last && (fast || l1) && ex.ctx->fuse13) {  // field 0, then fields 1-3 + random search in one launch
                     a.Fin = F[cur]; a.Fout = F[cur ^ 1];
-                    const int kind0 = (ex.ctx->phase0_mid && !pairwise && g.p == 2 &&
-                                       (a.src_fmt == fbk::SF8 || a.src_fmt == fbk::SF8F)) ? 2 : kind;
+                    const int kind0 = (l1 || (ex.ctx->phase0_mid && !pairwise && g.p == 2 &&
+                                              (a.src_fmt == fbk::SF8 || a.src_fmt == fbk::SF8F))) ? 2 : kind;
                     ex.launch(names[0], [&] { return fbk::launch_field(a, T, g.p, cfg.loss, 0, kind0, s); },
                               (1ull + (uint64_t)a.einit) * T * L.h * L.w);
                     cur ^= 1;
@@ -1147,6 +1156,7 @@ fb_status fb_set_option(fb_ctx ctx, int option, int value)
     case FB_OPT_FUSED_ITER: ctx->fused = value != 0; break;
     case FB_OPT_FUSE13: ctx->fuse13 = value != 0; break;
     case FB_OPT_PHASE0_MID: ctx->phase0_mid = value != 0; break;
+    case FB_OPT_L1_FAST: ctx->l1_fast = value != 0; break;
     case FB_OPT_TGT_REG_ROWS:
         if (value < 0 || value > 2) { ctx->err = "tgt_reg_rows must be 0, 1 or 2"; return FB_ERR_INVALID_ARG; }
         ctx->tgt_reg_rows = value;

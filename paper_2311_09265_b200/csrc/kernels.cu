@@ -72,6 +72,16 @@ __device__ __forceinline__ uint32_t pack_rgb(float r, float g, float b)  // exac
 {
     return (uint32_t)r | ((uint32_t)g << 8) | ((uint32_t)b << 16);
 }
+__device__ __forceinline__ uint32_t pack10(float r, float g, float b)  // SF10 / TF10 fields n = 4v (level 1, exact)
+{
+    return (uint32_t)(r * 4.0f) | ((uint32_t)(g * 4.0f) << 10) | ((uint32_t)(b * 4.0f) << 20);
+}
+// SF10 / TF10 channel as the exact value v = n / 4 biased by 2^21 (channels 0 and 2) or 2^11 (channel 1): the
+// field is placed in the mantissa of the bias (one LOP3 / funnel shift, no add).  Two biased values of one
+// channel differ by exactly t - s (same binade: Sterbenz), so the guide delta of D20 costs one FSUB.
+__device__ __forceinline__ float b10_0(uint32_t w) { return __uint_as_float((w & 0x3FFu) | 0x4A000000u); }
+__device__ __forceinline__ float b10_1(uint32_t w) { return __uint_as_float((w & 0xFFC00u) | 0x45000000u); }
+__device__ __forceinline__ float b10_2(uint32_t w) { return __uint_as_float(__funnelshift_r(w, 0x4A000u, 20)); }
 
 // ------------------------------------------------------------------------------------ pyramid (D6)
 __global__ void k_u8_to_pyr0(const uint8_t* __restrict__ frames, float4* __restrict__ pyr, int npx,
@@ -173,9 +183,10 @@ __global__ void k_pack_src(const PackSrc* __restrict__ jobs, int fmt, PLvl L)
 
 __device__ __forceinline__ void store_tgt(char* out, int tfmt, int i, bool in, float4 g, float ar, float ag, float ab)
 {
-    if (tfmt == TF16) {
+    if (tfmt == TF16 || tfmt == TF10) {
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (in) v = make_uint4(pack_rgb(g.x, g.y, g.z), __float_as_uint(ar), __float_as_uint(ag), __float_as_uint(ab));
+        if (in) v = make_uint4(tfmt == TF16 ? pack_rgb(g.x, g.y, g.z) : pack10(g.x, g.y, g.z), __float_as_uint(ar),
+                               __float_as_uint(ag), __float_as_uint(ab));
         reinterpret_cast<uint4*>(out)[i] = v;
     } else {
         float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
@@ -412,7 +423,7 @@ __global__ void __launch_bounds__(256, P <= 2 ? COMBINE_MINB : 1) k_combine(cons
             d[0] = ax; d[1] = ay; d[2] = az;
         } else {
             const float4 g = in ? __ldg(&o.guide[r * w + c]) : make_float4(0.f, 0.f, 0.f, 0.f);
-            store_tgt(static_cast<char*>(o.out), FMT == 2 ? TF16 : TF32, i, in, g, ax, ay, az);
+            store_tgt(static_cast<char*>(o.out), FMT == 2 ? TF16 : (FMT == 4 ? TF10 : TF32), i, in, g, ax, ay, az);
         }
     }
 }
@@ -831,7 +842,7 @@ static constexpr int I13_TY = 4;
 // NR < D (hybrid target): only the first NR rows of each lane's target patch live in registers -- row 0 is
 // read by every candidate, rows >= 1 only by candidates that survive row 0 -- and the rest is read from a
 // shared-memory copy of the CTA's target tile.  Registers drop from 168 to <= 128: 4 CTAs/SM instead of 3.
-template <int P, bool TWO, bool PW = false, int SFL = 0, int NR = 2 * P + 1>
+template <int P, bool TWO, bool PW = false, int SFL = 0, int NR = 2 * P + 1, int SF = 0>
 #ifndef I13_HY_MINB
 #define I13_HY_MINB 5  // 96 registers, no spills: 5 CTAs/SM (N=48: 388 -> 357 ms; 6 and 7 spill and lose)
 #endif
@@ -892,9 +903,40 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (SFL ? I13_SFL_M
         }
     };
     // One patch row of the loss (D20): exact integer guide SSD, FP32 style chain, row partial added.
-    auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
+    // SF = 1 (level 1, SF10 source + TF10 target): both terms are the literal FP32 chains of D20, with the
+    // guide deltas of the exact biased values (b10_*) and the style converted exactly (f10_*); the guide rows
+    // are added in FP32 (dgf), as the level-1 sum can exceed 2^24 sixteenths.
+    auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& dgf, float& ds) {
         const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
         FB_ASSERT((unsigned)sr < (unsigned)h && (unsigned)sc < (unsigned)w && FB_ROW_OK(idx, a.L, D));
+        if constexpr (SF == 1) {
+            const uint4* cp = reinterpret_cast<const uint4*>(S + (size_t)(idx & 1) * (a.L.rows * pitch) + (idx & ~1));
+            uint32_t wd[4 * NCH];
+#pragma unroll
+            for (int k = 0; k < NCH; ++k) {
+                const uint4 v = __ldg(cp + k);
+                wd[4 * k] = v.x; wd[4 * k + 1] = v.y; wd[4 * k + 2] = v.z; wd[4 * k + 3] = v.w;
+            }
+            float rg = 0.0f, rs = 0.0f;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const uint32_t gw = wd[2 * j], sw = wd[2 * j + 1];
+                uint32_t tg; float ta[3];
+                tgt(dr, j, tg, ta[0], ta[1], ta[2]);
+                float dl;
+                dl = __fsub_rn(b10_0(tg), b10_0(gw)); rg = __fmaf_rn(dl, dl, rg);
+                dl = __fsub_rn(b10_1(tg), b10_1(gw)); rg = __fmaf_rn(dl, dl, rg);
+                dl = __fsub_rn(b10_2(tg), b10_2(gw)); rg = __fmaf_rn(dl, dl, rg);
+                if (TWO) {
+                    dl = __fsub_rn(ta[0], f10_0(sw)); rs = __fmaf_rn(dl, dl, rs);
+                    dl = __fsub_rn(ta[1], f10_1(sw)); rs = __fmaf_rn(dl, dl, rs);
+                    dl = __fsub_rn(ta[2], f10_2(sw)); rs = __fmaf_rn(dl, dl, rs);
+                }
+            }
+            dgf = __fadd_rn(dgf, rg);
+            if (TWO) ds = __fadd_rn(ds, rs);
+            return;
+        }
         if (SFL == 1) {  // SF8F float style (blending-table cells): one 16-byte texel per tap
             const uint4* tp = reinterpret_cast<const uint4*>(S) + idx;
             float rs = 0.0f;
@@ -948,19 +990,20 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (SFL ? I13_SFL_M
     // are unchanged: selected candidates are always evaluated in full, in the D20 order.
     auto loss = [&](int sr, int sc, float bound) -> float {
         uint32_t dg = 0u;
-        float ds = 0.0f;
+        float dgf = 0.0f, ds = 0.0f;
+        auto gsum = [&]() { return SF == 1 ? dgf : __uint2float_rn(dg); };
         constexpr int S1 = PDE_FAST_S1(P), S2 = PDE_I13_S2(P);
 #pragma unroll
-        for (int dr = 0; dr < S1; ++dr) row(sr, sc, dr, dg, ds);
-        if (partial_loss(a.alpha, __uint2float_rn(dg), ds, TWO) >= bound) return __int_as_float(0x7f800000);
+        for (int dr = 0; dr < S1; ++dr) row(sr, sc, dr, dg, dgf, ds);
+        if (partial_loss(a.alpha, gsum(), ds, TWO) >= bound) return __int_as_float(0x7f800000);
         if (S2 < D) {
 #pragma unroll
-            for (int dr = S1; dr < S2; ++dr) row(sr, sc, dr, dg, ds);
-            if (partial_loss(a.alpha, __uint2float_rn(dg), ds, TWO) >= bound) return __int_as_float(0x7f800000);
+            for (int dr = S1; dr < S2; ++dr) row(sr, sc, dr, dg, dgf, ds);
+            if (partial_loss(a.alpha, gsum(), ds, TWO) >= bound) return __int_as_float(0x7f800000);
         }
 #pragma unroll
-        for (int dr = (S2 < D ? S2 : S1); dr < D; ++dr) row(sr, sc, dr, dg, ds);
-        const float fg = __uint2float_rn(dg);
+        for (int dr = (S2 < D ? S2 : S1); dr < D; ++dr) row(sr, sc, dr, dg, dgf, ds);
+        const float fg = gsum();
         return TWO ? __fmaf_rn(a.alpha, fg, ds) : fg;
     };
     // A candidate equal to the incumbent has exactly the incumbent's loss (same aux within the
@@ -1021,14 +1064,17 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (SFL ? I13_SFL_M
 // ---- level-0 variant for p = 3, 4: SF8 source, TF16 target tile in shared memory -----------------
 // The target patch of p >= 3 does not fit in registers, so it is staged per tile; the source rows and the
 // exact integer guide term (every partial < 2^24 for p <= 4 at level 0) are those of k_field_fast.
-template <int P, bool TWO, int PHASE, int SFL = 0>
+template <int P, bool TWO, int PHASE, int SFL = 0, int SF = 0>
 #ifndef MID_MINB
 #define MID_MINB 8  // p = 2 (phase 0): 8 CTAs/SM at 32 registers beats 5 at 44 (balanced N=48: 68 -> 62 ms)
 #endif
 #ifndef MID3_MINB
 #define MID3_MINB 4  // p = 3: 64 registers, 4 CTAs/SM (config-5 shard 27.3 -> 30.6 G evals/s)
 #endif
-__global__ void __launch_bounds__(TILE_X* TILE_Y, P == 2 ? MID_MINB : (P == 3 ? MID3_MINB : 1)) k_field_mid(FieldArgs a)
+#ifndef MID10_MINB
+#define MID10_MINB 4  // level-1 SF10 variant (more ALU per tap than the u8 one)
+#endif
+__global__ void __launch_bounds__(TILE_X* TILE_Y, P == 2 ? (SF ? MID10_MINB : MID_MINB) : (P == 3 ? MID3_MINB : 1)) k_field_mid(FieldArgs a)
 {
     constexpr int D = 2 * P + 1, SX = TILE_X + 2 * P, SY = TILE_Y + 2 * P;
     constexpr int NCH = (D + 2) / 2;  // 16-byte chunks covering D texels from an even start
@@ -1052,9 +1098,37 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y, P == 2 ? MID_MINB : (P == 3 ? 
     if (r >= h || c >= w) return;
     const uint2* S = reinterpret_cast<const uint2*>(T.src + a.src_off);
     const int plane = a.L.rows * pitch;
-    auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& ds) {
+    // SF = 1: level-1 SF10 source and TF10 target tile, the literal FP32 chains of D20 (see k_iter13_fast)
+    auto row = [&](int sr, int sc, int dr, uint32_t& dg, float& dgf, float& ds) {
         const int idx = (sr + dr - P + B) * pitch + (sc - P + B);
         FB_ASSERT((unsigned)sr < (unsigned)h && (unsigned)sc < (unsigned)w && FB_ROW_OK(idx, a.L, D));
+        if constexpr (SF == 1) {
+            const uint4* cp = reinterpret_cast<const uint4*>(S + (size_t)(idx & 1) * plane + (idx & ~1));
+            uint32_t wd[4 * NCH];
+#pragma unroll
+            for (int k = 0; k < NCH; ++k) {
+                const uint4 v = __ldg(cp + k);
+                wd[4 * k] = v.x; wd[4 * k + 1] = v.y; wd[4 * k + 2] = v.z; wd[4 * k + 3] = v.w;
+            }
+            float rg = 0.0f, rs = 0.0f;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const uint4 tv = tT[ly + dr][lx + j];
+                const uint32_t gw = wd[2 * j], sw = wd[2 * j + 1];
+                float dl;
+                dl = __fsub_rn(b10_0(tv.x), b10_0(gw)); rg = __fmaf_rn(dl, dl, rg);
+                dl = __fsub_rn(b10_1(tv.x), b10_1(gw)); rg = __fmaf_rn(dl, dl, rg);
+                dl = __fsub_rn(b10_2(tv.x), b10_2(gw)); rg = __fmaf_rn(dl, dl, rg);
+                if (TWO) {
+                    dl = __fsub_rn(__uint_as_float(tv.y), f10_0(sw)); rs = __fmaf_rn(dl, dl, rs);
+                    dl = __fsub_rn(__uint_as_float(tv.z), f10_1(sw)); rs = __fmaf_rn(dl, dl, rs);
+                    dl = __fsub_rn(__uint_as_float(tv.w), f10_2(sw)); rs = __fmaf_rn(dl, dl, rs);
+                }
+            }
+            dgf = __fadd_rn(dgf, rg);
+            if (TWO) ds = __fadd_rn(ds, rs);
+            return;
+        }
         if (SFL == 1) {  // SF8F float style (blending-table cells): one 16-byte texel per tap
             const uint4* tp = reinterpret_cast<const uint4*>(T.src + a.src_off) + idx;
             float rs = 0.0f;
@@ -1100,19 +1174,20 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y, P == 2 ? MID_MINB : (P == 3 ? 
     };
     auto loss = [&](int sr, int sc, float bound) -> float {
         uint32_t dg = 0u;
-        float ds = 0.0f;
+        float dgf = 0.0f, ds = 0.0f;
+        auto gsum = [&]() { return SF == 1 ? dgf : __uint2float_rn(dg); };
         constexpr int S1 = PDE_GEN_S1(P), S2 = PDE_GEN_S2(P);
 #pragma unroll
-        for (int dr = 0; dr < S1; ++dr) row(sr, sc, dr, dg, ds);
-        if (partial_loss(a.alpha, __uint2float_rn(dg), ds, TWO) >= bound) return __int_as_float(0x7f800000);
+        for (int dr = 0; dr < S1; ++dr) row(sr, sc, dr, dg, dgf, ds);
+        if (partial_loss(a.alpha, gsum(), ds, TWO) >= bound) return __int_as_float(0x7f800000);
         if (S2 < D) {
 #pragma unroll
-            for (int dr = S1; dr < S2; ++dr) row(sr, sc, dr, dg, ds);
-            if (partial_loss(a.alpha, __uint2float_rn(dg), ds, TWO) >= bound) return __int_as_float(0x7f800000);
+            for (int dr = S1; dr < S2; ++dr) row(sr, sc, dr, dg, dgf, ds);
+            if (partial_loss(a.alpha, gsum(), ds, TWO) >= bound) return __int_as_float(0x7f800000);
         }
 #pragma unroll
-        for (int dr = (S2 < D ? S2 : S1); dr < D; ++dr) row(sr, sc, dr, dg, ds);
-        const float fg = __uint2float_rn(dg);
+        for (int dr = (S2 < D ? S2 : S1); dr < D; ++dr) row(sr, sc, dr, dg, dgf, ds);
+        const float fg = gsum();
         return TWO ? __fmaf_rn(a.alpha, fg, ds) : fg;
     };
     auto select = [&](int2& f, float& e, int sr, int sc) {
@@ -1444,6 +1519,7 @@ static cudaError_t launch_combine_t(const DOut* outs, int n_outs, const DMember*
         case 0: k_combine<P, 0><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); break;
         case 1: k_combine<P, 1><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); break;
         case 2: k_combine<P, 2><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); break;
+        case 4: k_combine<P, 4><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); break;
         default: k_combine<P, 3><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); break;
         }
     });
@@ -1512,6 +1588,12 @@ cudaError_t launch_iter13_fast(const FieldArgs& a0, int T, int p, int loss, cuda
     a.tiles_per_task = a.tiles_x * ((a.L.h + I13_TY - 1) / I13_TY);
     const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(32 * I13_TY);
     const int hy = a.tgt_reg_rows;  // hybrid target (rows in registers; 0 = all)
+    if (a.src_fmt == SF10) {  // level 1: SF10 source + TF10 target (GUIDE_STYLE / MEAN_ALIGN, p = 2)
+        if (p != 2 || (loss != 1 && loss != 2)) return cudaErrorInvalidValue;
+        if (hy == 1) k_iter13_fast<2, true, false, 0, 1, 1><<<grid, block, 0, s>>>(a);
+        else k_iter13_fast<2, true, false, 0, 2, 1><<<grid, block, 0, s>>>(a);
+        return cudaGetLastError();
+    }
     if (a.src_fmt == SF8F) {
         if (loss != 1 && loss != 2) return cudaErrorInvalidValue;
         if (p == 1) k_iter13_fast<1, true, false, 1><<<grid, block, 0, s>>>(a);
@@ -1542,15 +1624,15 @@ cudaError_t launch_iter13_fast(const FieldArgs& a0, int T, int p, int loss, cuda
     return cudaGetLastError();
 }
 
-template <int P, bool TWO, int SFL = 0>
+template <int P, bool TWO, int SFL = 0, int SF = 0>
 static void launch_field_mid(const FieldArgs& a, int T, int phase, cudaStream_t s)
 {
     const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(TILE_X * TILE_Y);
     switch (phase) {
-    case 0: k_field_mid<P, TWO, 0, SFL><<<grid, block, 0, s>>>(a); break;
-    case 1: k_field_mid<P, TWO, 1, SFL><<<grid, block, 0, s>>>(a); break;
-    case 2: k_field_mid<P, TWO, 2, SFL><<<grid, block, 0, s>>>(a); break;
-    default: k_field_mid<P, TWO, 3, SFL><<<grid, block, 0, s>>>(a); break;
+    case 0: k_field_mid<P, TWO, 0, SFL, SF><<<grid, block, 0, s>>>(a); break;
+    case 1: k_field_mid<P, TWO, 1, SFL, SF><<<grid, block, 0, s>>>(a); break;
+    case 2: k_field_mid<P, TWO, 2, SFL, SF><<<grid, block, 0, s>>>(a); break;
+    default: k_field_mid<P, TWO, 3, SFL, SF><<<grid, block, 0, s>>>(a); break;
     }
 }
 
@@ -1561,8 +1643,13 @@ cudaError_t launch_field(const FieldArgs& a0, int T, int p, int loss, int phase,
     a.tiles_x = (a.L.w + TILE_X - 1) / TILE_X;
     a.tiles_per_task = a.tiles_x * ((a.L.h + (fast ? FAST_TY : TILE_Y) - 1) / (fast ? FAST_TY : TILE_Y));
     const bool pw = loss == 3;
-    if (kind == 2) {  // level 0: SF8 (or, p = 2, SF8F) source, TF16 target tile (not PAIRWISE)
+    if (kind == 2) {  // level 0: SF8 (or, p = 2, SF8F) source, TF16 target tile; level 1: SF10 + TF10 (p = 2)
         if (pw) return cudaErrorInvalidValue;
+        if (a.src_fmt == SF10) {
+            if (p != 2 || !loss) return cudaErrorInvalidValue;
+            launch_field_mid<2, true, 0, 1>(a, T, phase, s);
+            return cudaGetLastError();
+        }
         if (a.src_fmt == SF8F) {
             if (p != 2 || !loss) return cudaErrorInvalidValue;
             launch_field_mid<2, true, 1>(a, T, phase, s);

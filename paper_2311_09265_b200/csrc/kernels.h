@@ -17,6 +17,7 @@
 //                   as f32}; the guide is still u8-exact at level 0                              16 B
 //              SF32 (otherwise):           float4 {G.r,G.g,G.b,S.r}, float4 {S.g,S.b,0,0}     32 B
 //      target  TF16 (with SF8):            uint4  {G rgb u8, aux.r, aux.g, aux.b (f32 bits)}  16 B
+//              TF10 (with SF10, level 1):  uint4  {G as SF10 10-bit fields, aux.r, aux.g, aux.b}  16 B
 //              TF32 (with SF32):           float4 {G.r,G.g,G.b,aux.r}, float4 {aux.g,aux.b,0,0} 32 B
 #pragma once
 #include <cuda_runtime.h>
@@ -31,7 +32,7 @@ constexpr int kBorder = 4;  // >= the largest compiled patch radius
 constexpr int kSF8Copies = FB_SF8_COPIES;
 
 enum SrcFmt { SF8 = 0, SF32 = 1, SF16 = 2, SF8F = 3, SF10 = 4 };
-enum TgtFmt { TF16 = 0, TF32 = 1 };
+enum TgtFmt { TF16 = 0, TF32 = 1, TF10 = 2 };
 
 // One NNF task (pair).
 struct DTask {
@@ -126,14 +127,15 @@ cudaError_t launch_combine(const DOut* outs, int n_outs, const DMember* mem, con
                            int h, int w, int p, int fmt, PLvl P, cudaStream_t s);
 // phase 0: E init + propagation (-1,0); 1: (+1,0); 2: (0,-1); 3: (0,+1) + all random-search steps.
 // kind: 0 general (SF16/SF32 source, TF32 target tile in smem), 1 fast (SF8/SF8F, TF16 target patch in
-// registers, p <= 2), 2 mid (level 0, p = 3..4: SF8 source, TF16 target tile in smem).
+// registers, p <= 2), 2 mid (16-byte target tile in smem: level 0 SF8/SF8F + TF16, or level 1 SF10 + TF10
+// at p = 2).
 // loss: fb_loss (0 BASE, 1 GUIDE_STYLE, 2 MEAN_ALIGN, 3 PAIRWISE).
 cudaError_t launch_field(const FieldArgs& a, int T, int p, int loss, int phase, int kind, cudaStream_t s);
 // The whole updating sequence of one iteration (E init, four propagation fields, random search) in one
 // launch, fast operands only (SF8/TF16, p <= 2).  Fin -> Fout, E written.
 cudaError_t launch_iter_fast(const FieldArgs& a, int T, int p, int loss, cudaStream_t s);
-// Fields 1-3 and the random search of one iteration in one launch (fast operands); Fin holds the
-// field-0 result and E its errors.  Fin -> Fout, E updated.
+// Fields 1-3 and the random search of one iteration in one launch (fast operands: SF8/SF8F + TF16 at
+// level 0, SF10 + TF10 at level 1 for p = 2); Fin holds the field-0 result and E its errors.  Fin -> Fout.
 cudaError_t launch_iter13_fast(const FieldArgs& a, int T, int p, int loss, cudaStream_t s);
 cudaError_t launch_remap_f3(const float* src, const int2* F, float* out, int B, int H, int W, int p,
                             cudaStream_t s);

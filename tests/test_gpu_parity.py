@@ -459,3 +459,39 @@ def test_invalid_iteration_and_step_counts_rejected(fb, ctx):
         with pytest.raises(fb.FBError) as e:
             ctx.fb_blend_window(cfg, fb.DIRECT, dev(g), dev(s), 1)
         assert e.value.status == 1
+
+
+@pytest.mark.parametrize("mode,H,W", [("accurate", 96, 80), ("balanced", 128, 112), ("accurate", 135, 67)])
+def test_level1_fast_path_matches_oracle(fb, mode, H, W):
+    """Level 1 of u8 sources runs through the 16-byte TF10 target and the fused kernels (FB_OPT_L1_FAST): the
+    FP32 chains on exact biased operands must equal the oracle bit for bit, and equal the general kernel."""
+    g, s = moving_texture(5, H, W, seed=41)
+    loss = fb.MEAN_ALIGN if mode == "accurate" else fb.GUIDE_STYLE
+    cfg = fb.MatchCfg(iters_per_level=2, loss=loss, levels=3 if H == 135 else 0)
+    ctx = fb.Context(0)
+    ctx.set_option(fb.fb.OPT_L1_FAST, 1)
+    out, st = ctx.fb_blend_window(cfg, fb.DIRECT, dev(g), dev(s), 2)
+    ref, pairs, evals = O.blend_direct(ocfg(cfg), g, s, 2)
+    assert st["candidate_evals"] == evals
+    assert_frames(out, ref)
+    c2 = fb.Context(0)
+    c2.set_option(fb.fb.OPT_L1_FAST, 0)
+    out2, _ = c2.fb_blend_window(cfg, fb.DIRECT, dev(g), dev(s), 2)
+    assert torch.equal(out, out2)
+
+
+@pytest.mark.parametrize("l1_fast", [0, 1])
+def test_level1_fast_path_nnf_and_error(fb, l1_fast):
+    """NNF and E after a 3-level estimation (levels 2 -> 1 -> 0) through fb_nnf_estimate, against the oracle."""
+    ctx = fb.Context(0)
+    ctx.set_option(fb.fb.OPT_L1_FAST, l1_fast)
+    g, s = moving_texture(3, 72, 88, seed=43)
+    cfg = fb.MatchCfg(iters_per_level=2, loss=fb.GUIDE_STYLE, levels=3)
+    F, E, X, st = ctx.fb_nnf_estimate(cfg, dev(g[[0, 2]]), dev(g[[1, 1]]), dev(s[[0, 2]]), pair_keys=[(0, 1, 0), (2, 1, 0)])
+    frames = np.concatenate([g, s]).astype(np.float32)
+    tasks = [dict(src_guide=0, tgt_guide=1, src_style=3, src_id=0, tgt_id=1, tag=0),
+             dict(src_guide=2, tgt_guide=1, src_style=5, src_id=2, tgt_id=1, tag=0)]
+    Fr, Er, Xr, ev = O.nnf(ocfg(cfg), frames, tasks)
+    assert st["candidate_evals"] == ev
+    assert_nnf(F, E, Fr, Er)
+    assert_frames(X, Xr)
