@@ -36,8 +36,12 @@ struct fb_ctx_s {
     bool fuse13 = true;  // FB_OPT_FUSE13: fields 1-3 + random search fused on the fast path
     bool phase0_mid = true;  // FB_OPT_PHASE0_MID: E init + field 0 at level 0 through the shared-memory-target
                              // kernel (0: register target; 44 vs 163 registers: field0.L0 95 -> 76 ms at N=48)
-    int tgt_reg_rows = 2;  // FB_OPT_TGT_REG_ROWS: fused fields 1-3 target rows in registers, rest in shared
-                           // memory (0 = all in registers; accurate N=48: field123.L0 413 -> 397 ms)
+    int tgt_reg_rows = 1;  // FB_OPT_TGT_REG_ROWS: fused fields 1-3 target rows in registers, rest in shared
+                           // memory (0 = all in registers).  With the patch-sum bound most random-search
+                           // candidates never read a target row: one register row at 6 CTAs/SM beats two at 5
+                           // (accurate N=48: field123.L0 353 -> 333 ms)
+    bool sum_bound = true;  // FB_OPT_SUM_BOUND: random-search candidates rejected by the patch-sum bound (level 0,
+                            // and level 1 with FB_OPT_L1_FAST) before any patch row is gathered
     bool l1_fast = false;  // FB_OPT_L1_FAST: level 1 of u8 sources (SF10) through the level-0 kernel structure
                            // (16-byte TF10 targets, fused fields 1-3 + random search); bit-identical but slower
                            // (N=48 accurate 683 -> 724 ms: field123.L1 158 ms vs 113 for fields 1-3 of the
@@ -300,7 +304,9 @@ struct Slots {
     char* base = nullptr;
     size_t stride = 0;  // bytes per slot
     size_t off[24] = {};
+    long long sum_off[24];  // patch-sum plane of level k inside a slot (kernels.h SumJob), or -1
     int fmt0 = fbk::SF8;
+    Slots() { std::fill(sum_off, sum_off + 24, -1LL); }
     const char* slot(long long i) const { return base + (size_t)i * stride; }
 };
 
@@ -310,11 +316,20 @@ Slots pack_sources(Exec& ex, const Geo& g, int fmt0, const std::vector<SlotSpec>
     if (g.p > 2 && fmt0 == fbk::SF8F) fmt0 = fbk::SF32;  // float styles at p > 2: general kernel
     S.fmt0 = fmt0;
     size_t off = 0;
+    const int D = 2 * g.p + 1;
     for (int k = 0; k < g.Lv; ++k) {
         S.off[k] = off;
         const int f = src_fmt(fmt0, k);
         const size_t copies = (f == fbk::SF8 || f == fbk::SF10) ? fbk::kSF8Copies : 1;
         off = (off + copies * g.PL[k].rows * g.PL[k].pitch * src_bytes(f) + 255) & ~size_t(255);
+        // patch sums for the random-search bound where a kernel reads them: level 0 (SF8) through the fused
+        // fields-1-3 kernel (p <= 2), levels >= 1 of exact packed sources (SF10, SF16); every sum must fit its
+        // 21-bit field (and the fused kernel's 16-bit target sums)
+        const bool sums = ex.ctx->sum_bound && (long long)D * D * 255 * (1LL << (2 * k)) < (1LL << 21) &&
+                          ((f == fbk::SF8 && k == 0 && g.p <= 2) || f == fbk::SF10 || f == fbk::SF16) &&
+                          (f != fbk::SF10 || !ex.ctx->l1_fast || D * D * 1020 < 65536);
+        S.sum_off[k] = sums ? (long long)off : -1;
+        if (sums) off = (off + (size_t)g.PL[k].h * g.PL[k].w * sizeof(uint4) + 255) & ~size_t(255);
     }
     S.stride = off;
     const int n = (int)specs.size();
@@ -331,6 +346,15 @@ Slots pack_sources(Exec& ex, const Geo& g, int fmt0, const std::vector<SlotSpec>
         const int fmt = src_fmt(fmt0, k);
         ex.launch("pack_src", [&] { return fbk::launch_pack_src(dj, n, fmt, g.PL[k], ex.ctx->stream); },
                   (uint64_t)n * g.PL[k].rows * g.PL[k].pitch);
+        if (S.sum_off[k] >= 0) {
+            std::vector<fbk::SumJob> sj(n);
+            for (int i = 0; i < n; ++i)
+                sj[i] = fbk::SumJob{S.base + (size_t)i * S.stride + S.off[k],
+                                    reinterpret_cast<uint4*>(S.base + (size_t)i * S.stride + S.sum_off[k])};
+            const fbk::SumJob* dsj = ex.upload(sj);
+            ex.launch("patch_sums", [&] { return fbk::launch_patch_sums(dsj, n, fmt, g.PL[k], g.p, ex.ctx->stream); },
+                      (uint64_t)n * g.PL[k].h * g.PL[k].w);
+        }
     }
     return S;
 }
@@ -485,6 +509,7 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
             a.alpha = cfg.alpha; a.rng = rng; a.level = (uint32_t)k; a.iter = (uint32_t)it; a.rs_r0 = r0; a.rs_k = rk;
             a.src_fmt = src_fmt(slots.fmt0, k);
             a.tgt_reg_rows = ex.ctx->tgt_reg_rows;
+            a.sum_off = slots.sum_off[k];
             char names[4][32];
             for (int ph = 0; ph < 4; ++ph) snprintf(names[ph], sizeof names[ph], "field%d.L%d", ph, k);
             const int J = std::max(1, cfg.prop_scales);  // jump-flood scales (D41)
@@ -1157,6 +1182,7 @@ fb_status fb_set_option(fb_ctx ctx, int option, int value)
     case FB_OPT_FUSE13: ctx->fuse13 = value != 0; break;
     case FB_OPT_PHASE0_MID: ctx->phase0_mid = value != 0; break;
     case FB_OPT_L1_FAST: ctx->l1_fast = value != 0; break;
+    case FB_OPT_SUM_BOUND: ctx->sum_bound = value != 0; break;
     case FB_OPT_TGT_REG_ROWS:
         if (value < 0 || value > 2) { ctx->err = "tgt_reg_rows must be 0, 1 or 2"; return FB_ERR_INVALID_ARG; }
         ctx->tgt_reg_rows = value;

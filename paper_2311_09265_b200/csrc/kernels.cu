@@ -181,6 +181,94 @@ __global__ void k_pack_src(const PackSrc* __restrict__ jobs, int fmt, PLvl L)
     }
 }
 
+// Patch sums (SumJob, kernels.h) of SF8 (u8 fields), SF10 (10-bit fields n = 4v) or SF16 (16-bit n = v 4^k)
+// source blocks: integer sums over the (2p+1)^2 patch (zero border = zero padding, D9), exact; the caller checks
+// that every sum fits its 21-bit field.  The patch rows are re-read per output texel (L1 hits).
+template <int P>
+__global__ void k_patch_sums(const SumJob* __restrict__ jobs, int fmt, PLvl L)
+{
+    constexpr int D = 2 * P + 1;
+    const SumJob J = jobs[blockIdx.y];
+    const int n = L.h * L.w;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int r = i / L.w, c = i - r * L.w;
+        uint32_t g0 = 0, g1 = 0, g2 = 0, s0 = 0, s1 = 0, s2 = 0;
+        for (int dr = 0; dr < D; ++dr) {
+            const size_t row0 = (size_t)(r + dr - P + B) * L.pitch + (c - P + B);
+#pragma unroll
+            for (int dc = 0; dc < D; ++dc) {
+                if (fmt == SF16) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4*>(J.blk) + row0 + dc);
+                    g0 += v.x & 0xFFFFu; g1 += v.x >> 16; g2 += v.y & 0xFFFFu;
+                    s0 += v.z & 0xFFFFu; s1 += v.z >> 16; s2 += v.w & 0xFFFFu;
+                } else {
+                    const uint2 v = __ldg(reinterpret_cast<const uint2*>(J.blk) + row0 + dc);
+                    if (fmt == SF8) {
+                        g0 += v.x & 0xFFu; g1 += (v.x >> 8) & 0xFFu; g2 += (v.x >> 16) & 0xFFu;
+                        s0 += v.y & 0xFFu; s1 += (v.y >> 8) & 0xFFu; s2 += (v.y >> 16) & 0xFFu;
+                    } else {
+                        g0 += v.x & 0x3FFu; g1 += (v.x >> 10) & 0x3FFu; g2 += v.x >> 20;
+                        s0 += v.y & 0x3FFu; s1 += (v.y >> 10) & 0x3FFu; s2 += v.y >> 20;
+                    }
+                }
+            }
+        }
+        const unsigned long long lo = g0 | ((unsigned long long)g1 << 21) | ((unsigned long long)g2 << 42);
+        const unsigned long long hi = s0 | ((unsigned long long)s1 << 21) | ((unsigned long long)s2 << 42);
+        J.sums[i] = make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32));
+    }
+}
+
+// ---- patch-sum bound ("exact work elimination") ------------------------------------------
+// Per channel, Cauchy-Schwarz gives sum_taps (t - s)^2 >= (sum t - sum s)^2 / D^2, so
+//   LB = alpha * sum_c (dG_c)^2 / D^2 + sum_c (dS_c)^2 / D^2  <=  L*,
+// the exact loss of the candidate over the stored operand values.  The FP32 loss the kernels compute
+// (non-negative terms, every chain <= 23 roundings) is >= L* (1 - 23 u), u = 2^-24.  Guide sums are exact (integer
+// multiples of 4^-k below 2^21 units); the target aux sums carry an absolute error <= 8 u sum|t| (two-pass sums),
+// removed, with the rounding of the delta, from |dS_c| before squaring (margin m = 2 D^2 u sum|t|, an upper
+// bound); LB is evaluated with round-down operations.  So rd(LB (1 - 2^-16)) >= E implies the candidate's
+// FP32 loss is >= E: it cannot win the strict select (D16) and rejecting it changes nothing.
+struct TSums {
+    float g0, g1, g2;  // target guide patch sums (exact, level units)
+    float a0, a1, a2;  // target aux patch sums (FP32)
+    float m;           // absolute margin of the aux sums
+};
+// q: the candidate's source patch sums (k_patch_sums, 21-bit fields in units of `scale` = 4^-k)
+template <int D, bool TWO>
+__device__ __forceinline__ bool csb_reject(uint4 q, const TSums& t, float scale, float alpha, float e)
+{
+    constexpr unsigned long long M21 = (1ull << 21) - 1;
+    const unsigned long long lo = ((unsigned long long)q.y << 32) | q.x;
+    const float d0 = __fsub_rn(t.g0, (float)(uint32_t)(lo & M21) * scale);  // exact: multiples of scale < 2^22
+    const float d1 = __fsub_rn(t.g1, (float)(uint32_t)((lo >> 21) & M21) * scale);
+    const float d2 = __fsub_rn(t.g2, (float)(uint32_t)(lo >> 42) * scale);
+    const float inv = __frcp_rd((float)(D * D));
+    float lb = __fmul_rd(__fmaf_rd(d2, d2, __fmaf_rd(d1, d1, __fmul_rd(d0, d0))), inv);
+    if (TWO) {
+        const unsigned long long hi = ((unsigned long long)q.w << 32) | q.z;
+        constexpr float kS = 1.0f - 0x1p-22f;
+        const float l0 = fmaxf(__fsub_rd(__fmul_rd(fabsf(__fsub_rn(t.a0, (float)(uint32_t)(hi & M21) * scale)), kS), t.m), 0.0f);
+        const float l1 = fmaxf(__fsub_rd(__fmul_rd(fabsf(__fsub_rn(t.a1, (float)(uint32_t)((hi >> 21) & M21) * scale)), kS), t.m), 0.0f);
+        const float l2 = fmaxf(__fsub_rd(__fmul_rd(fabsf(__fsub_rn(t.a2, (float)(uint32_t)(hi >> 42) * scale)), kS), t.m), 0.0f);
+        lb = __fmaf_rd(alpha, lb, __fmul_rd(__fmaf_rd(l2, l2, __fmaf_rd(l1, l1, __fmul_rd(l0, l0))), inv));
+    }
+    return __fmul_rd(lb, 1.0f - 0x1p-16f) >= e;
+}
+// margin of a two-pass FP32 sum of D^2 aux values whose absolute values sum to <= absum
+// Random-search offset of step s (D13, D21): uniform in [-R, R]^2, R = max(r0 >> s, 1).
+__device__ __forceinline__ int2 rs_offset(const FieldArgs& a, const DTask& T, int i, int s)
+{
+    const int R = max(a.rs_r0 >> s, 1);
+    const uint4 u = philox4x32_10(
+        make_uint4((uint32_t)i, (1u << 28) | (a.level << 22) | (a.iter << 12) | (uint32_t)s, T.c2, T.c3), a.rng.k0,
+        a.rng.k1);
+    const uint32_t span = 2u * (uint32_t)R + 1u;
+    return make_int2((int)__umulhi(u.x, span) - R, (int)__umulhi(u.y, span) - R);
+}
+
+template <int D>
+__device__ __forceinline__ float csb_margin(float absum) { return __fmul_ru(absum, (float)(2 * D * D) * 0x1p-24f); }
+
 __device__ __forceinline__ void store_tgt(char* out, int tfmt, int i, bool in, float4 g, float ar, float ag, float ab)
 {
     if (tfmt == TF16 || tfmt == TF10) {
@@ -849,7 +937,10 @@ template <int P, bool TWO, bool PW = false, int SFL = 0, int NR = 2 * P + 1, int
 #ifndef I13_SFL_MINB
 #define I13_SFL_MINB 4  // SF8F (16-byte texel) queries spill at 5 CTAs/SM: fast N=48 field123.L0 126 -> 124 ms
 #endif
-__global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (SFL ? I13_SFL_MINB : I13_HY_MINB) : 3) k_iter13_fast(FieldArgs a)
+#ifndef I13_HY1_MINB
+#define I13_HY1_MINB 6  // one target row in registers
+#endif
+__global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (SFL ? I13_SFL_MINB : (NR == 1 ? I13_HY1_MINB : I13_HY_MINB)) : 3) k_iter13_fast(FieldArgs a)
 {
     constexpr int D = 2 * P + 1;
     constexpr bool HY = NR < D;
@@ -879,6 +970,8 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (SFL ? I13_SFL_M
         }
         __syncthreads();
     }
+    constexpr bool CSB = SFL == 0 && !PW && HY;  // patch-sum bound of the random search (csb_reject)
+    const bool use_csb = CSB && a.sum_off >= 0;
     if (valid) {
 #pragma unroll
         for (int dr = 0; dr < NRR; ++dr)
@@ -1035,9 +1128,49 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (SFL ? I13_SFL_M
         }
     }
     // field 3: d = (0,+1), neighbour (r, c+1) of the field-2 result (lane + 1), then random search
+    const int2 fr = make_int2(__shfl_down_sync(0xffffffffu, f.x, 1), __shfl_down_sync(0xffffffffu, f.y, 1));
+    // Target patch sums of the bound, while all 32 lanes are converged: column sums over the D patch rows of
+    // the shared tile (tile columns 32.. by lanes 0..2P-1), then the D columns of each lane's patch by shuffles.
+    TSums ts{};
+    if (use_csb) {
+        uint32_t cg[2][2] = {{0u, 0u}, {0u, 0u}};  // [main, extra] {g0 | g1 << 16, g2}
+        float ca[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};  // {a0, a1, a2, max_c sum|a_c|}
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+            if (x == 1 && lane >= 2 * P) break;
+            float b0 = 0.f, b1 = 0.f, b2 = 0.f;
+#pragma unroll
+            for (int dr = 0; dr < D; ++dr) {
+                const uint4 v = tT[CSB ? wy + dr : 0][CSB ? lane + 32 * x : 0];
+                if (SF == 1) { cg[x][0] += (v.x & 0x3FFu) | (((v.x >> 10) & 0x3FFu) << 16); cg[x][1] += v.x >> 20; }
+                else { cg[x][0] += (v.x & 0xFFu) | (((v.x >> 8) & 0xFFu) << 16); cg[x][1] += (v.x >> 16) & 0xFFu; }
+                const float t0 = __uint_as_float(v.y), t1 = __uint_as_float(v.z), t2 = __uint_as_float(v.w);
+                ca[x][0] = __fadd_rn(ca[x][0], t0); ca[x][1] = __fadd_rn(ca[x][1], t1); ca[x][2] = __fadd_rn(ca[x][2], t2);
+                b0 = __fadd_ru(b0, fabsf(t0)); b1 = __fadd_ru(b1, fabsf(t1)); b2 = __fadd_ru(b2, fabsf(t2));
+            }
+            ca[x][3] = fmaxf(b0, fmaxf(b1, b2));
+        }
+        uint32_t g01 = cg[0][0], g2 = cg[0][1];  // 16-bit lanes: every sum <= D^2 * 1020 < 2^16
+        float a0 = ca[0][0], a1 = ca[0][1], a2 = ca[0][2], m = ca[0][3];
+#pragma unroll
+        for (int j = 1; j < D; ++j) {
+            const bool own = lane + j < 32;
+            const int src = (lane + j) & 31;
+            const uint32_t x0 = __shfl_down_sync(0xffffffffu, cg[0][0], j), y0 = __shfl_sync(0xffffffffu, cg[1][0], src);
+            const uint32_t x1 = __shfl_down_sync(0xffffffffu, cg[0][1], j), y1 = __shfl_sync(0xffffffffu, cg[1][1], src);
+            const float p0 = __shfl_down_sync(0xffffffffu, ca[0][0], j), q0 = __shfl_sync(0xffffffffu, ca[1][0], src);
+            const float p1 = __shfl_down_sync(0xffffffffu, ca[0][1], j), q1 = __shfl_sync(0xffffffffu, ca[1][1], src);
+            const float p2 = __shfl_down_sync(0xffffffffu, ca[0][2], j), q2 = __shfl_sync(0xffffffffu, ca[1][2], src);
+            const float p3 = __shfl_down_sync(0xffffffffu, ca[0][3], j), q3 = __shfl_sync(0xffffffffu, ca[1][3], src);
+            g01 += own ? x0 : y0; g2 += own ? x1 : y1;
+            a0 = __fadd_rn(a0, own ? p0 : q0); a1 = __fadd_rn(a1, own ? p1 : q1); a2 = __fadd_rn(a2, own ? p2 : q2);
+            m = __fadd_ru(m, own ? p3 : q3);
+        }
+        constexpr float gsc = SF == 1 ? 0.25f : 1.0f;
+        ts = TSums{(float)(g01 & 0xFFFFu) * gsc, (float)(g01 >> 16) * gsc, (float)g2 * gsc, a0, a1, a2, csb_margin<D>(m)};
+    }
+    if (!valid || lane == 0 || lane == 31) return;
     {
-        const int2 fr = make_int2(__shfl_down_sync(0xffffffffu, f.x, 1), __shfl_down_sync(0xffffffffu, f.y, 1));
-        if (!valid || lane == 0 || lane == 31) return;
         const int2 fn = c + 1 < w ? fr : f;
         select(f, e, fn.x, max(fn.y - 1, 0));
     }
@@ -1047,14 +1180,15 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (SFL ? I13_SFL_M
             const int2 g = __ldg(&T.trk[z][i]);
             select(f, e, g.x, g.y);
         }
+    const uint4* SUMS = use_csb ? reinterpret_cast<const uint4*>(T.src + a.sum_off) : nullptr;
+    constexpr float ssc = SF == 1 ? 0.25f : 1.0f;  // source sums: n = v (SF8) or n = 4 v (SF10)
     for (int s = 0; s < a.rs_k; ++s) {
-        const int R = max(a.rs_r0 >> s, 1);
-        const uint4 u = philox4x32_10(
-            make_uint4((uint32_t)i, (1u << 28) | (a.level << 22) | (a.iter << 12) | (uint32_t)s, T.c2, T.c3),
-            a.rng.k0, a.rng.k1);
-        const uint32_t span = 2u * (uint32_t)R + 1u;
-        const int ox = (int)__umulhi(u.x, span) - R, oy = (int)__umulhi(u.y, span) - R;
-        select(f, e, clampi(f.x + ox, 0, h - 1), clampi(f.y + oy, 0, w - 1));
+        const int2 o = rs_offset(a, T, i, s);
+        const int sr = clampi(f.x + o.x, 0, h - 1), sc = clampi(f.y + o.y, 0, w - 1);
+        if (CSB && use_csb && (sr != f.x || sc != f.y) &&
+            csb_reject<D, TWO>(__ldg(SUMS + sr * w + sc), ts, ssc, a.alpha, e))
+            continue;
+        select(f, e, sr, sc);
     }
     FB_ASSERT((unsigned)f.x < (unsigned)h && (unsigned)f.y < (unsigned)w);
     a.Fout[t * a.fstride + i] = f;
@@ -1257,6 +1391,47 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
     }
     __syncthreads();
     const int lx = threadIdx.x & (TILE_X - 1), ly = threadIdx.x / TILE_X;
+    // Patch-sum bound of the random search (csb_reject, levels with exact packed sources): the target patch sums,
+    // computed while the warp is converged -- column sums over the D rows of the tile (tile columns 32.. by lanes
+    // 0..2P-1), then the D columns of each lane's patch by shuffles.  Guide sums are exact (multiples of 4^-k
+    // below 2^21 units).
+    constexpr bool CSB = PHASE == 3 && !PW && (SFMT == SF10 || SFMT == SF16);
+    const bool use_csb = CSB && a.do_rs && a.sum_off >= 0;
+    TSums ts{};
+    if (use_csb) {
+        float cs[2][7];  // [main, extra] {g0, g1, g2, a0, a1, a2, max_c sum|a_c|}
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+#pragma unroll
+            for (int q = 0; q < 7; ++q) cs[x][q] = 0.0f;
+            if (x == 1 && lx >= 2 * P) break;
+            float b0 = 0.f, b1 = 0.f, b2 = 0.f;
+#pragma unroll
+            for (int dr = 0; dr < D; ++dr) {
+                const float4 q0 = t0[ly + dr][lx + 32 * x];
+                const float2 q1 = t1[ly + dr][lx + 32 * x];
+                cs[x][0] = __fadd_rn(cs[x][0], q0.x); cs[x][1] = __fadd_rn(cs[x][1], q0.y);
+                cs[x][2] = __fadd_rn(cs[x][2], q0.z); cs[x][3] = __fadd_rn(cs[x][3], q0.w);
+                cs[x][4] = __fadd_rn(cs[x][4], q1.x); cs[x][5] = __fadd_rn(cs[x][5], q1.y);
+                b0 = __fadd_ru(b0, fabsf(q0.w)); b1 = __fadd_ru(b1, fabsf(q1.x)); b2 = __fadd_ru(b2, fabsf(q1.y));
+            }
+            cs[x][6] = fmaxf(b0, fmaxf(b1, b2));
+        }
+        float acc[7];
+#pragma unroll
+        for (int q = 0; q < 7; ++q) acc[q] = cs[0][q];
+#pragma unroll
+        for (int j = 1; j < D; ++j) {
+            const bool own = lx + j < 32;
+            const int src = (lx + j) & 31;
+#pragma unroll
+            for (int q = 0; q < 7; ++q) {
+                const float pv = __shfl_down_sync(0xffffffffu, cs[0][q], j), qv = __shfl_sync(0xffffffffu, cs[1][q], src);
+                acc[q] = q == 6 ? __fadd_ru(acc[q], own ? pv : qv) : __fadd_rn(acc[q], own ? pv : qv);
+            }
+        }
+        ts = TSums{acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], csb_margin<D>(acc[6])};
+    }
     const int c = tx * TILE_X + lx, r = ty * TILE_Y + ly;
     if (r >= h || c >= w) return;
     const float4* S = reinterpret_cast<const float4*>(T.src + a.src_off);
@@ -1386,15 +1561,13 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
                     if (e2 < e) { f = g; e = e2; }
                 }
             }
+        const uint4* SUMS = use_csb ? reinterpret_cast<const uint4*>(T.src + a.sum_off) : nullptr;
+        const float scale = __uint_as_float((uint32_t)(127 - 2 * a.L.k) << 23);  // 4^-k: unit of the source sums
         for (int s = 0; s < a.rs_k; ++s) {
-            const int R = max(a.rs_r0 >> s, 1);
-            const uint4 u = philox4x32_10(
-                make_uint4((uint32_t)i, (1u << 28) | (a.level << 22) | (a.iter << 12) | (uint32_t)s, T.c2, T.c3),
-                a.rng.k0, a.rng.k1);
-            const uint32_t span = 2u * (uint32_t)R + 1u;
-            const int ox = (int)__umulhi(u.x, span) - R, oy = (int)__umulhi(u.y, span) - R;
-            const int sr = clampi(f.x + ox, 0, h - 1), sc = clampi(f.y + oy, 0, w - 1);
+            const int2 o = rs_offset(a, T, i, s);
+            const int sr = clampi(f.x + o.x, 0, h - 1), sc = clampi(f.y + o.y, 0, w - 1);
             if (sr != f.x || sc != f.y) {
+                if (CSB && use_csb && csb_reject<D, TWO>(__ldg(SUMS + sr * w + sc), ts, scale, a.alpha, e)) continue;
                 const float e2 = loss(sr, sc, e);
                 if (e2 < e) { f = make_int2(sr, sc); e = e2; }
             }
@@ -1484,6 +1657,17 @@ cudaError_t launch_upsample(const int2* Fc, int2* Ff, int T, long long fstride, 
     case 4: { constexpr int PP = 4; CALL; } break; \
     default: return cudaErrorInvalidValue;          \
     }
+
+cudaError_t launch_patch_sums(const SumJob* jobs, int n, int fmt, PLvl L, int p, cudaStream_t s)
+{
+    if (n <= 0) return cudaSuccess;
+    if (fmt != SF8 && fmt != SF10 && fmt != SF16) return cudaErrorInvalidValue;
+    cudaError_t e = cudaSuccess;
+    FB_DISPATCH_P(p, (e = for_y_chunks(n, [&](long long y0, int m) {
+        k_patch_sums<PP><<<grid1d((long long)L.h * L.w, m), 256, 0, s>>>(jobs + y0, fmt, L);
+    })));
+    return e;
+}
 
 template <int P>
 static cudaError_t launch_aux_remap_t(const DTask* tasks, int T, const int2* F, long long fstride, Lvl L, PLvl PL,

@@ -99,6 +99,17 @@ struct FieldArgs {
     int do_rs;             // phase 3 runs the random search (last field of the iteration)
     float* Eout;           // fused fields 1-3: final E (nullable); E itself is read-only there
     int tgt_reg_rows;      // fused fields 1-3 (p = 2): target patch rows held in registers (0 = all)
+    long long sum_off;     // byte offset of this level's patch-sum plane inside each source slot, or -1 (none):
+                           // the random search then rejects candidates by the patch-sum bound
+};
+
+// Patch sums of a packed source level block (SF8 at level 0, SF10 at level 1): for every texel (r, c) of the
+// level, the sums over its (2p+1)^2 patch (zero padding, D9) of the integer fields n of each guide and style
+// channel, as uint4 {sG.r | sG.g << 16, sG.b | sS.r << 16, sS.g | sS.b << 16, 0} at [r * w + c]; every sum
+// is below 2^16 (checked by the caller: (2p+1)^2 * max n < 2^16).
+struct SumJob {
+    const char* blk;  // packed level block (copy 0)
+    uint4* sums;      // [h * w]
 };
 
 // Packing jobs: one per (slot, level) for sources, one per task/group for BASE targets.
@@ -115,6 +126,7 @@ cudaError_t launch_u8_to_pyr0(const uint8_t* frames, float4* pyr, int B, int H, 
                               cudaStream_t s);
 cudaError_t launch_box(float4* pyr, int B, long long pyr_stride, Lvl prev, Lvl cur, cudaStream_t s);
 cudaError_t launch_pack_src(const PackSrc* jobs, int n, int fmt, PLvl L, cudaStream_t s);
+cudaError_t launch_patch_sums(const SumJob* jobs, int n, int fmt, PLvl L, int p, cudaStream_t s);
 cudaError_t launch_pack_tgt_guide(const DTask* tasks, int T, Lvl L, PLvl P, int tfmt, cudaStream_t s);
 cudaError_t launch_init(const DTask* tasks, int T, int2* F, long long fstride, Lvl L, int identity, Rng rng,
                         uint32_t level, cudaStream_t s);

@@ -495,3 +495,26 @@ def test_level1_fast_path_nnf_and_error(fb, l1_fast):
     assert st["candidate_evals"] == ev
     assert_nnf(F, E, Fr, Er)
     assert_frames(X, Xr)
+
+
+@pytest.mark.parametrize("loss,H,W,sb,l1,rows", [(1, 96, 112, 1, 0, 1), (2, 96, 112, 1, 0, 1), (0, 64, 80, 1, 0, 1),
+                                                 (1, 96, 112, 0, 0, 1), (2, 135, 67, 1, 1, 1), (1, 128, 112, 1, 1, 1),
+                                                 (2, 96, 112, 1, 0, 0), (2, 96, 112, 1, 0, 2), (1, 67, 135, 1, 0, 2)])
+def test_patch_sum_bound_matches_oracle(fb, loss, H, W, sb, l1, rows):
+    """The random search's patch-sum bound (FB_OPT_SUM_BOUND) only skips candidates that provably
+    lose the strict select: NNF and E equal the oracle bit for bit with the bound on and off, at level 0 and, with
+    FB_OPT_L1_FAST, at level 1, for every count of target rows held in registers; odd sizes put candidates on the
+    zero-padded border."""
+    c = fb.Context(0)
+    c.set_option(fb.fb.OPT_SUM_BOUND, sb)
+    c.set_option(fb.fb.OPT_L1_FAST, l1)
+    c.set_option(fb.fb.OPT_TGT_REG_ROWS, rows)
+    cfg, (sg, tg, ss, ts, keys), frames, tasks = _nnf_case(fb, loss, H, W, seed=47, n=3, levels=3)
+    group = [0] * len(keys) if loss == fb.MEAN_ALIGN else None
+    F, E, X, st = c.fb_nnf_estimate(cfg, dev(sg), dev(tg), None if loss == 0 else dev(ss),
+                                    dev(ts) if loss == 2 else None, group=group, pair_keys=keys)
+    Fr, Er, Xr, ev = O.nnf(ocfg(cfg), frames, tasks, want_x=loss != 0)
+    assert st["candidate_evals"] == ev
+    assert_nnf(F, E, Fr, Er)
+    if loss != 0:
+        assert_frames(X, Xr)

@@ -1,0 +1,76 @@
+"""Development aid (not the product, not a test): how many random-search candidates a cheap lower bound of
+the patch loss would reject before any patch row is gathered, against the first-row partial-distance test.
+
+Runs the oracle on one accurate-mode-shaped pair to get a converged (F, E, X), then draws random-search
+candidates around F at every radius of the schedule and, per candidate, compares
+  full   = the Eq. 3 loss (float64),
+  row0   = its first patch row (the current elimination test after one row),
+  mean   = Cauchy-Schwarz on patch sums: sum_c (sum_i a_ic - sum_i b_ic)^2 / n  <=  sum_ic (a_ic - b_ic)^2,
+  rows   = the same per patch row (5 row sums per channel).
+usage: python tools/bound_sim.py [H] [pair_distance]"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle as O  # noqa: E402
+from synth import moving_texture  # noqa: E402
+
+H = int(sys.argv[1]) if len(sys.argv) > 1 else 192
+dj = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+p, alpha = 2, 10.0
+g, s = moving_texture(dj + 1, H, H)
+frames = np.concatenate([g[[dj, 0]], s[[dj]]]).astype(np.float32)
+tasks = [dict(src_guide=0, tgt_guide=1, src_style=2, src_id=dj, tgt_id=0, tag=0)]
+cfg = O.Cfg(iters_per_level=5, loss=O.GUIDE_STYLE)
+F, E, X, _ = O.nnf(cfg, frames, tasks)
+F, E, X = F[0], E[0].astype(np.float64), X[0].astype(np.float64)
+G_s, S_s, G_t = (frames[i].astype(np.float64) for i in (0, 2, 1))
+T_aux = X  # the style target of the last refresh (S-hat)
+D = 2 * p + 1
+n = D * D
+
+
+def pad(a):
+    return np.pad(a, ((p, p), (p, p), (0, 0)))
+
+
+Gs, Ss, Gt, Tt = pad(G_s), pad(S_s), pad(G_t), pad(T_aux)
+
+
+def patches(A, r, c):  # [..., D, D, 3] patches centred at (r, c) of an unpadded-coordinate grid
+    rr = r[..., None, None] + np.arange(D)[:, None]
+    cc = c[..., None, None] + np.arange(D)[None, :]
+    return A[rr, cc]
+
+
+rows, cols = np.meshgrid(np.arange(H), np.arange(H), indexing="ij")
+tg, ta = patches(Gt, rows, cols), patches(Tt, rows, cols)
+rng = np.random.default_rng(0)
+R = H
+tot = dict(cands=0, lose=0, row0=0, mean=0, rows=0, mean_or_row0=0)
+print(f"H={H}, pair distance {dj}: median E {np.median(E):.0f}")
+while R >= 1:
+    off = rng.integers(-R, R + 1, size=(H, H, 2))
+    cr = np.clip(F[..., 0] + off[..., 0], 0, H - 1)
+    cc = np.clip(F[..., 1] + off[..., 1], 0, H - 1)
+    sg, ss = patches(Gs, cr, cc), patches(Ss, cr, cc)
+    dg, ds = (sg - tg) ** 2, (ss - ta) ** 2
+    full = alpha * dg.sum((-3, -2, -1)) + ds.sum((-3, -2, -1))
+    row0 = alpha * dg[..., 0, :, :].sum((-2, -1)) + ds[..., 0, :, :].sum((-2, -1))
+    mean = (alpha * ((sg.sum((-3, -2)) - tg.sum((-3, -2))) ** 2).sum(-1)
+            + ((ss.sum((-3, -2)) - ta.sum((-3, -2))) ** 2).sum(-1)) / n
+    rws = (alpha * ((sg.sum(-2) - tg.sum(-2)) ** 2).sum((-2, -1))
+           + ((ss.sum(-2) - ta.sum(-2)) ** 2).sum((-2, -1))) / D
+    lose = full >= E
+    st = dict(cands=lose.size, lose=lose.sum(), row0=(row0 >= E).sum(), mean=(mean >= E).sum(),
+              rows=(rws >= E).sum(), mean_or_row0=((mean >= E) | (row0 >= E)).sum())
+    for k in tot:
+        tot[k] += st[k]
+    print(f"R={R:4d}: lose {st['lose']/st['cands']:.3f}  rejected by row0 {st['row0']/st['cands']:.3f}  "
+          f"mean {st['mean']/st['cands']:.3f}  row sums {st['rows']/st['cands']:.3f}  "
+          f"mean|row0 {st['mean_or_row0']/st['cands']:.3f}")
+    R >>= 1
+c = tot["cands"]
+print("all radii: " + "  ".join(f"{k} {v/c:.3f}" for k, v in tot.items() if k != "cands"))

@@ -12,6 +12,8 @@ cap() {  # name regex skip   (ONLY = space-separated names to capture; empty = a
     ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:$2" -s "$3" -c 1 -f \
         -o gpurun_out/${1}_$TAG python tools/prof_case.py 24 > gpurun_out/ncu_${1}_$TAG.log 2>&1
     ncu -i gpurun_out/${1}_$TAG.ncu-rep --page raw --csv > gpurun_out/${1}_${TAG}_raw.csv 2>/dev/null
+    # per-source-line stall samples (needs -lineinfo): KEEP_SRC=1
+    [ -z "$KEEP_SRC" ] || ncu -i gpurun_out/${1}_$TAG.ncu-rep --page source --csv > gpurun_out/${1}_${TAG}_src.csv 2>/dev/null
     [ -n "$KEEP_REP" ] || rm -f gpurun_out/${1}_$TAG.ncu-rep  # gpurun copies back <= 64 MiB
 }
 # demangled names read e.g. "void fbk::k_field_gen<(int)2, (bool)1, (int)0, (int)4, (bool)0>(fbk::FieldArgs)"
