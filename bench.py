@@ -301,8 +301,9 @@ def roofline(prof, wl, cfg, steps):
             "frac": achieved / peak, "frac_of_nominal": achieved / nominal, "traffic": None, "peak_basis": peak_src,
             "bytes_per_eval": bpe, "evals_per_launch": d["work"] / max(d["launches"], 1),
             "avg_launch_ms": d["ms"] / max(d["launches"], 1), "share_of_kernel_time": d["ms"] / total_ms,
-            "note": "algorithmic bytes: partial-distance elimination and the 8-byte exact texels load fewer; the "
-                    "hardware L1 utilisation of the same kernel is ncu_util.l1tex_lsu_wavefronts_pct"}
+            "note": "algorithmic bytes (SURVEY 8(d): every evaluation gathers its whole FP32 patch); the exact "
+                    "eliminations (patch-sum bound, partial distances) and the 8-byte exact texels load far fewer, "
+                    "so frac can exceed 1; `hardware` is the same kernel's measured L1 data-pipe traffic"}
     traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(traffic_file):
         try:
@@ -312,6 +313,13 @@ def roofline(prof, wl, cfg, steps):
                 roof["traffic_source"] = tr[dom].get("source")
             if dom in tr and "ncu_util" in tr[dom]:
                 roof["ncu_util"] = tr[dom]["ncu_util"]
+            if dom in tr and "l1_wavefronts_per_work" in tr[dom]:
+                # hardware view of the same launches: L1 data-pipe wavefronts (128 B each) per evaluation from
+                # the committed ncu capture, times this run's evaluations, over this run's CUDA-event time
+                hw = tr[dom]["l1_wavefronts_per_work"] * 128.0 * d["work"] / sec / 1e9
+                roof["hardware"] = {"achieved": hw, "peak": peak, "unit": "GB/s", "frac": hw / peak,
+                                    "l1_wavefronts_per_eval": tr[dom]["l1_wavefronts_per_work"],
+                                    "source": tr[dom].get("source")}
         except (OSError, ValueError):
             pass
     fp32_peak = SMS * FP32_LANES_PER_SM * 2 * SM_MAX_MHZ * 1e6 / 1e12

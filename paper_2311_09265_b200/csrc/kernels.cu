@@ -29,6 +29,14 @@ static constexpr int B = kBorder;
 #else
 #define FB_ASSERT(cond) do { } while (0)
 #endif
+// Event counters of the fused level-0 kernel (development build with -DFB_COUNTERS: tools/build_variant.sh and
+// fb_debug_counters); no-ops in the product build.
+#ifdef FB_COUNTERS
+__device__ unsigned long long g_fb_cnt[32];
+#define FB_CNT(k) atomicAdd(&g_fb_cnt[(k)], 1ull)
+#else
+#define FB_CNT(k) do { } while (0)
+#endif
 // a patch row of D texels starting at padded texel idx (rounded down to even, NCH texel pairs) lies in
 // the level block and in the row band the zero border provides
 #define FB_ROW_OK(idx, L, D) ((idx) >= 0 && ((idx) & ~1) + 2 * (((D) + 2) / 2) <= (L).rows * (L).pitch && \
@@ -233,6 +241,20 @@ struct TSums {
     float a0, a1, a2;  // target aux patch sums (FP32)
     float m;           // absolute margin of the aux sums
 };
+// Random-search offset of step s (D13, D21): uniform in [-R, R]^2, R = max(r0 >> s, 1).
+__device__ __forceinline__ int2 rs_offset(const FieldArgs& a, const DTask& T, int i, int s)
+{
+    const int R = max(a.rs_r0 >> s, 1);
+    const uint4 u = philox4x32_10(
+        make_uint4((uint32_t)i, (1u << 28) | (a.level << 22) | (a.iter << 12) | (uint32_t)s, T.c2, T.c3), a.rng.k0,
+        a.rng.k1);
+    const uint32_t span = 2u * (uint32_t)R + 1u;
+    return make_int2((int)__umulhi(u.x, span) - R, (int)__umulhi(u.y, span) - R);
+}
+
+// margin of a two-pass FP32 sum of D^2 aux values whose absolute values sum to <= absum
+template <int D>
+__device__ __forceinline__ float csb_margin(float absum) { return __fmul_ru(absum, (float)(2 * D * D) * 0x1p-24f); }
 // q: the candidate's source patch sums (k_patch_sums, 21-bit fields in units of `scale` = 4^-k)
 template <int D, bool TWO>
 __device__ __forceinline__ bool csb_reject(uint4 q, const TSums& t, float scale, float alpha, float e)
@@ -254,20 +276,47 @@ __device__ __forceinline__ bool csb_reject(uint4 q, const TSums& t, float scale,
     }
     return __fmul_rd(lb, 1.0f - 0x1p-16f) >= e;
 }
-// margin of a two-pass FP32 sum of D^2 aux values whose absolute values sum to <= absum
-// Random-search offset of step s (D13, D21): uniform in [-R, R]^2, R = max(r0 >> s, 1).
-__device__ __forceinline__ int2 rs_offset(const FieldArgs& a, const DTask& T, int i, int s)
+// Target patch sums of the bound for lane (lx, ly) of a warp-per-tile-row layout (tile column lx + j, row ly + dr):
+// column sums over the D rows (tile columns 32.. by lanes 0..2P-1), then the D columns by shuffles.  All 32 lanes
+// must call it converged.  fetch(yy, xx, v) returns the tile texel's guide (v[0..2], level units) and aux
+// (v[3..5]); guide sums are exact (multiples of 4^-k below 2^21 units), aux sums carry the margin of csb_margin.
+template <int P, class Fetch>
+__device__ __forceinline__ TSums tile_patch_sums(int lx, int ly, Fetch&& fetch)
 {
-    const int R = max(a.rs_r0 >> s, 1);
-    const uint4 u = philox4x32_10(
-        make_uint4((uint32_t)i, (1u << 28) | (a.level << 22) | (a.iter << 12) | (uint32_t)s, T.c2, T.c3), a.rng.k0,
-        a.rng.k1);
-    const uint32_t span = 2u * (uint32_t)R + 1u;
-    return make_int2((int)__umulhi(u.x, span) - R, (int)__umulhi(u.y, span) - R);
+    constexpr int D = 2 * P + 1;
+    float cs[2][7];  // [main, extra] {g0, g1, g2, a0, a1, a2, max_c sum|a_c|}
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+#pragma unroll
+        for (int q = 0; q < 7; ++q) cs[x][q] = 0.0f;
+        if (x == 1 && lx >= 2 * P) break;
+        float b0 = 0.f, b1 = 0.f, b2 = 0.f;
+#pragma unroll
+        for (int dr = 0; dr < D; ++dr) {
+            float v[6];
+            fetch(ly + dr, lx + 32 * x, v);
+#pragma unroll
+            for (int q = 0; q < 6; ++q) cs[x][q] = __fadd_rn(cs[x][q], v[q]);
+            b0 = __fadd_ru(b0, fabsf(v[3])); b1 = __fadd_ru(b1, fabsf(v[4])); b2 = __fadd_ru(b2, fabsf(v[5]));
+        }
+        cs[x][6] = fmaxf(b0, fmaxf(b1, b2));
+    }
+    float acc[7];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) acc[q] = cs[0][q];
+#pragma unroll
+    for (int j = 1; j < D; ++j) {
+        const bool own = lx + j < 32;
+        const int src = (lx + j) & 31;
+#pragma unroll
+        for (int q = 0; q < 7; ++q) {
+            const float pv = __shfl_down_sync(0xffffffffu, cs[0][q], j), qv = __shfl_sync(0xffffffffu, cs[1][q], src);
+            acc[q] = q == 6 ? __fadd_ru(acc[q], own ? pv : qv) : __fadd_rn(acc[q], own ? pv : qv);
+        }
+    }
+    return TSums{acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], csb_margin<D>(acc[6])};
 }
 
-template <int D>
-__device__ __forceinline__ float csb_margin(float absum) { return __fmul_ru(absum, (float)(2 * D * D) * 0x1p-24f); }
 
 __device__ __forceinline__ void store_tgt(char* out, int tfmt, int i, bool in, float4 g, float ar, float ag, float ab)
 {
@@ -1081,31 +1130,34 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (SFL ? I13_SFL_M
     // monotone, so once the partial loss after the first P rows is >= `bound` the full loss is too and
     // the candidate cannot win the strict select (D16); its remaining rows are never loaded.  Results
     // are unchanged: selected candidates are always evaluated in full, in the D20 order.
+    int cbase = 0;  // FB_COUNTERS: 0 propagation, 8 random search
     auto loss = [&](int sr, int sc, float bound) -> float {
         uint32_t dg = 0u;
         float dgf = 0.0f, ds = 0.0f;
         auto gsum = [&]() { return SF == 1 ? dgf : __uint2float_rn(dg); };
         constexpr int S1 = PDE_FAST_S1(P), S2 = PDE_I13_S2(P);
+        FB_CNT(cbase + 0);
 #pragma unroll
         for (int dr = 0; dr < S1; ++dr) row(sr, sc, dr, dg, dgf, ds);
-        if (partial_loss(a.alpha, gsum(), ds, TWO) >= bound) return __int_as_float(0x7f800000);
+        if (partial_loss(a.alpha, gsum(), ds, TWO) >= bound) { FB_CNT(cbase + 1); return __int_as_float(0x7f800000); }
         if (S2 < D) {
 #pragma unroll
             for (int dr = S1; dr < S2; ++dr) row(sr, sc, dr, dg, dgf, ds);
-            if (partial_loss(a.alpha, gsum(), ds, TWO) >= bound) return __int_as_float(0x7f800000);
+            if (partial_loss(a.alpha, gsum(), ds, TWO) >= bound) { FB_CNT(cbase + 2); return __int_as_float(0x7f800000); }
         }
 #pragma unroll
         for (int dr = (S2 < D ? S2 : S1); dr < D; ++dr) row(sr, sc, dr, dg, dgf, ds);
+        FB_CNT(cbase + 3);
         const float fg = gsum();
         return TWO ? __fmaf_rn(a.alpha, fg, ds) : fg;
     };
     // A candidate equal to the incumbent has exactly the incumbent's loss (same aux within the
     // iteration), so it cannot win the strict select (D16): skipping it changes nothing.
     auto select = [&](int2& f, float& e, int sr, int sc) {
-        if (sr == f.x && sc == f.y) return;
+        if (sr == f.x && sc == f.y) { FB_CNT(cbase + 5); return; }
         if (sr != f.x || sc != f.y) {  // an incumbent-equal candidate cannot win (see select)
             const float e2 = loss(sr, sc, e);
-            if (e2 < e) { f = make_int2(sr, sc); e = e2; }
+            if (e2 < e) { f = make_int2(sr, sc); e = e2; FB_CNT(cbase + 4); }
         }
     };
     const int2* Fi = a.Fin + t * a.fstride;
@@ -1182,12 +1234,15 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (SFL ? I13_SFL_M
         }
     const uint4* SUMS = use_csb ? reinterpret_cast<const uint4*>(T.src + a.sum_off) : nullptr;
     constexpr float ssc = SF == 1 ? 0.25f : 1.0f;  // source sums: n = v (SF8) or n = 4 v (SF10)
+    cbase = 8;
     for (int s = 0; s < a.rs_k; ++s) {
         const int2 o = rs_offset(a, T, i, s);
         const int sr = clampi(f.x + o.x, 0, h - 1), sc = clampi(f.y + o.y, 0, w - 1);
         if (CSB && use_csb && (sr != f.x || sc != f.y) &&
-            csb_reject<D, TWO>(__ldg(SUMS + sr * w + sc), ts, ssc, a.alpha, e))
+            csb_reject<D, TWO>(__ldg(SUMS + sr * w + sc), ts, ssc, a.alpha, e)) {
+            FB_CNT(14);
             continue;
+        }
         select(f, e, sr, sc);
     }
     FB_ASSERT((unsigned)f.x < (unsigned)h && (unsigned)f.y < (unsigned)w);
@@ -1229,6 +1284,17 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y, P == 2 ? (SF ? MID10_MINB : MI
     __syncthreads();
     const int lx = threadIdx.x & (TILE_X - 1), ly = threadIdx.x / TILE_X;
     const int c = tx * TILE_X + lx, r = ty * TILE_Y + ly;
+    // patch-sum bound of the random search (csb_reject): target sums while the warp is converged
+    constexpr bool CSB = PHASE == 3 && SFL == 0;
+    const bool use_csb = CSB && a.do_rs && a.sum_off >= 0;
+    TSums ts{};
+    if (use_csb)
+        ts = tile_patch_sums<P>(lx, ly, [&](int yy, int xx, float (&v)[6]) {
+            const uint4 q = tT[yy][xx];
+            if (SF == 1) { v[0] = f10_0(q.x); v[1] = f10_1(q.x); v[2] = f10_2(q.x); }
+            else { v[0] = (float)(q.x & 0xFFu); v[1] = (float)((q.x >> 8) & 0xFFu); v[2] = (float)((q.x >> 16) & 0xFFu); }
+            v[3] = __uint_as_float(q.y); v[4] = __uint_as_float(q.z); v[5] = __uint_as_float(q.w);
+        });
     if (r >= h || c >= w) return;
     const uint2* S = reinterpret_cast<const uint2*>(T.src + a.src_off);
     const int plane = a.L.rows * pitch;
@@ -1347,14 +1413,15 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y, P == 2 ? (SF ? MID10_MINB : MI
                 const int2 g = __ldg(&T.trk[z][i]);
                 select(f, e, g.x, g.y);
             }
+        const uint4* SUMS = use_csb ? reinterpret_cast<const uint4*>(T.src + a.sum_off) : nullptr;
+        constexpr float ssc = SF == 1 ? 0.25f : 1.0f;  // source sums: n = v (SF8) or n = 4 v (SF10)
         for (int s = 0; s < a.rs_k; ++s) {
-            const int R = max(a.rs_r0 >> s, 1);
-            const uint4 u = philox4x32_10(
-                make_uint4((uint32_t)i, (1u << 28) | (a.level << 22) | (a.iter << 12) | (uint32_t)s, T.c2, T.c3),
-                a.rng.k0, a.rng.k1);
-            const uint32_t span = 2u * (uint32_t)R + 1u;
-            const int ox = (int)__umulhi(u.x, span) - R, oy = (int)__umulhi(u.y, span) - R;
-            select(f, e, clampi(f.x + ox, 0, h - 1), clampi(f.y + oy, 0, w - 1));
+            const int2 o = rs_offset(a, T, i, s);
+            const int sr = clampi(f.x + o.x, 0, h - 1), sc = clampi(f.y + o.y, 0, w - 1);
+            if (CSB && use_csb && (sr != f.x || sc != f.y) &&
+                csb_reject<D, TWO>(__ldg(SUMS + sr * w + sc), ts, ssc, a.alpha, e))
+                continue;
+            select(f, e, sr, sc);
         }
     }
     FB_ASSERT((unsigned)f.x < (unsigned)h && (unsigned)f.y < (unsigned)w);
@@ -1398,40 +1465,12 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
     constexpr bool CSB = PHASE == 3 && !PW && (SFMT == SF10 || SFMT == SF16);
     const bool use_csb = CSB && a.do_rs && a.sum_off >= 0;
     TSums ts{};
-    if (use_csb) {
-        float cs[2][7];  // [main, extra] {g0, g1, g2, a0, a1, a2, max_c sum|a_c|}
-#pragma unroll
-        for (int x = 0; x < 2; ++x) {
-#pragma unroll
-            for (int q = 0; q < 7; ++q) cs[x][q] = 0.0f;
-            if (x == 1 && lx >= 2 * P) break;
-            float b0 = 0.f, b1 = 0.f, b2 = 0.f;
-#pragma unroll
-            for (int dr = 0; dr < D; ++dr) {
-                const float4 q0 = t0[ly + dr][lx + 32 * x];
-                const float2 q1 = t1[ly + dr][lx + 32 * x];
-                cs[x][0] = __fadd_rn(cs[x][0], q0.x); cs[x][1] = __fadd_rn(cs[x][1], q0.y);
-                cs[x][2] = __fadd_rn(cs[x][2], q0.z); cs[x][3] = __fadd_rn(cs[x][3], q0.w);
-                cs[x][4] = __fadd_rn(cs[x][4], q1.x); cs[x][5] = __fadd_rn(cs[x][5], q1.y);
-                b0 = __fadd_ru(b0, fabsf(q0.w)); b1 = __fadd_ru(b1, fabsf(q1.x)); b2 = __fadd_ru(b2, fabsf(q1.y));
-            }
-            cs[x][6] = fmaxf(b0, fmaxf(b1, b2));
-        }
-        float acc[7];
-#pragma unroll
-        for (int q = 0; q < 7; ++q) acc[q] = cs[0][q];
-#pragma unroll
-        for (int j = 1; j < D; ++j) {
-            const bool own = lx + j < 32;
-            const int src = (lx + j) & 31;
-#pragma unroll
-            for (int q = 0; q < 7; ++q) {
-                const float pv = __shfl_down_sync(0xffffffffu, cs[0][q], j), qv = __shfl_sync(0xffffffffu, cs[1][q], src);
-                acc[q] = q == 6 ? __fadd_ru(acc[q], own ? pv : qv) : __fadd_rn(acc[q], own ? pv : qv);
-            }
-        }
-        ts = TSums{acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], csb_margin<D>(acc[6])};
-    }
+    if (use_csb)
+        ts = tile_patch_sums<P>(lx, ly, [&](int yy, int xx, float (&v)[6]) {
+            const float4 q0 = t0[yy][xx];
+            const float2 q1 = t1[yy][xx];
+            v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w; v[4] = q1.x; v[5] = q1.y;
+        });
     const int c = tx * TILE_X + lx, r = ty * TILE_Y + ly;
     if (r >= h || c >= w) return;
     const float4* S = reinterpret_cast<const float4*>(T.src + a.src_off);
@@ -1894,3 +1933,16 @@ cudaError_t launch_field(const FieldArgs& a0, int T, int p, int loss, int phase,
 }
 
 }  // namespace fbk
+
+#ifdef FB_COUNTERS
+extern "C" int fb_debug_counters(unsigned long long* out, int reset)
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, fbk::g_fb_cnt, sizeof(unsigned long long) * 32);
+    if (reset) {
+        unsigned long long z[32] = {};
+        cudaMemcpyToSymbol(fbk::g_fb_cnt, z, sizeof z);
+    }
+    return 0;
+}
+#endif
