@@ -325,10 +325,10 @@ Slots pack_sources(Exec& ex, const Geo& g, int fmt0, const std::vector<SlotSpec>
         // patch sums for the random-search bound (exact packed sources: SF8 at level 0, SF10, SF16); every sum
         // must fit its 21-bit field (and, through the fused kernel at level 1, its 16-bit target sums)
         const bool sums = ex.ctx->sum_bound && (long long)D * D * 255 * (1LL << (2 * k)) < (1LL << 21) &&
-                          (f == fbk::SF8 || f == fbk::SF10 || f == fbk::SF16) &&
+                          (f == fbk::SF8 || f == fbk::SF10 || f == fbk::SF16 || (f == fbk::SF8F && g.p <= 2)) &&
                           (f != fbk::SF10 || !ex.ctx->l1_fast || D * D * 1020 < 65536);
         S.sum_off[k] = sums ? (long long)off : -1;
-        if (sums) off = (off + (size_t)g.PL[k].h * g.PL[k].w * sizeof(uint4) + 255) & ~size_t(255);
+        if (sums) off = (off + (size_t)g.PL[k].h * g.PL[k].w * sizeof(uint4) * (f == fbk::SF8F ? 2 : 1) + 255) & ~size_t(255);
     }
     S.stride = off;
     const int n = (int)specs.size();

@@ -200,6 +200,25 @@ __global__ void k_patch_sums(const SumJob* __restrict__ jobs, int fmt, PLvl L)
     const int n = L.h * L.w;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int r = i / L.w, c = i - r * L.w;
+        if (fmt == SF8F) {  // u8 guide (exact integer sums) + f32 style (FP32 sums with an absolute margin)
+            uint32_t g0 = 0, g1 = 0, g2 = 0;
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, b0 = 0.f, b1 = 0.f, b2 = 0.f;
+            for (int dr = 0; dr < D; ++dr) {
+                const size_t row0 = (size_t)(r + dr - P + B) * L.pitch + (c - P + B);
+#pragma unroll
+                for (int dc = 0; dc < D; ++dc) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4*>(J.blk) + row0 + dc);
+                    g0 += v.x & 0xFFu; g1 += (v.x >> 8) & 0xFFu; g2 += (v.x >> 16) & 0xFFu;
+                    const float t0 = __uint_as_float(v.y), t1 = __uint_as_float(v.z), t2 = __uint_as_float(v.w);
+                    s0 = __fadd_rn(s0, t0); s1 = __fadd_rn(s1, t1); s2 = __fadd_rn(s2, t2);
+                    b0 = __fadd_ru(b0, fabsf(t0)); b1 = __fadd_ru(b1, fabsf(t1)); b2 = __fadd_ru(b2, fabsf(t2));
+                }
+            }
+            const float m = __fmul_ru(fmaxf(b0, fmaxf(b1, b2)), (float)(2 * D * D) * 0x1p-24f);
+            J.sums[2 * i] = make_uint4(g0, g1, g2, __float_as_uint(s0));
+            J.sums[2 * i + 1] = make_uint4(__float_as_uint(s1), __float_as_uint(s2), __float_as_uint(m), 0u);
+            continue;
+        }
         uint32_t g0 = 0, g1 = 0, g2 = 0, s0 = 0, s1 = 0, s2 = 0;
         for (int dr = 0; dr < D; ++dr) {
             const size_t row0 = (size_t)(r + dr - P + B) * L.pitch + (c - P + B);
@@ -272,6 +291,24 @@ __device__ __forceinline__ bool csb_reject(uint4 q, const TSums& t, float scale,
         const float l0 = fmaxf(__fsub_rd(__fmul_rd(fabsf(__fsub_rn(t.a0, (float)(uint32_t)(hi & M21) * scale)), kS), t.m), 0.0f);
         const float l1 = fmaxf(__fsub_rd(__fmul_rd(fabsf(__fsub_rn(t.a1, (float)(uint32_t)((hi >> 21) & M21) * scale)), kS), t.m), 0.0f);
         const float l2 = fmaxf(__fsub_rd(__fmul_rd(fabsf(__fsub_rn(t.a2, (float)(uint32_t)(hi >> 42) * scale)), kS), t.m), 0.0f);
+        lb = __fmaf_rd(alpha, lb, __fmul_rd(__fmaf_rd(l2, l2, __fmaf_rd(l1, l1, __fmul_rd(l0, l0))), inv));
+    }
+    return __fmul_rd(lb, 1.0f - 0x1p-16f) >= e;
+}
+// The same bound for SF8F sources (float styles, e.g. blending-table cells): two 16-byte texels {G sums (exact),
+// S.r sum} {S.g, S.b sums, their absolute margin ms}; the style delta loses both sums' margins.
+template <int D, bool TWO>
+__device__ __forceinline__ bool csb_reject_f(uint4 qa, uint4 qb, const TSums& t, float alpha, float e)
+{
+    const float d0 = __fsub_rn(t.g0, (float)qa.x), d1 = __fsub_rn(t.g1, (float)qa.y), d2 = __fsub_rn(t.g2, (float)qa.z);
+    const float inv = __frcp_rd((float)(D * D));
+    float lb = __fmul_rd(__fmaf_rd(d2, d2, __fmaf_rd(d1, d1, __fmul_rd(d0, d0))), inv);
+    if (TWO) {
+        constexpr float kS = 1.0f - 0x1p-22f;
+        const float m = __fadd_ru(t.m, __uint_as_float(qb.z));
+        const float l0 = fmaxf(__fsub_rd(__fmul_rd(fabsf(__fsub_rn(t.a0, __uint_as_float(qa.w))), kS), m), 0.0f);
+        const float l1 = fmaxf(__fsub_rd(__fmul_rd(fabsf(__fsub_rn(t.a1, __uint_as_float(qb.x))), kS), m), 0.0f);
+        const float l2 = fmaxf(__fsub_rd(__fmul_rd(fabsf(__fsub_rn(t.a2, __uint_as_float(qb.y))), kS), m), 0.0f);
         lb = __fmaf_rd(alpha, lb, __fmul_rd(__fmaf_rd(l2, l2, __fmaf_rd(l1, l1, __fmul_rd(l0, l0))), inv));
     }
     return __fmul_rd(lb, 1.0f - 0x1p-16f) >= e;
@@ -1019,7 +1056,7 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (SFL ? I13_SFL_M
         }
         __syncthreads();
     }
-    constexpr bool CSB = SFL == 0 && !PW && HY;  // patch-sum bound of the random search (csb_reject)
+    constexpr bool CSB = (SFL == 0 || SFL == 1) && !PW && HY;  // patch-sum bound of the random search (csb_reject)
     const bool use_csb = CSB && a.sum_off >= 0;
     if (valid) {
 #pragma unroll
@@ -1239,7 +1276,9 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (SFL ? I13_SFL_M
         const int2 o = rs_offset(a, T, i, s);
         const int sr = clampi(f.x + o.x, 0, h - 1), sc = clampi(f.y + o.y, 0, w - 1);
         if (CSB && use_csb && (sr != f.x || sc != f.y) &&
-            csb_reject<D, TWO>(__ldg(SUMS + sr * w + sc), ts, ssc, a.alpha, e)) {
+            (SFL == 1 ? csb_reject_f<D, TWO>(__ldg(SUMS + 2 * (sr * w + sc)), __ldg(SUMS + 2 * (sr * w + sc) + 1), ts,
+                                             a.alpha, e)
+                      : csb_reject<D, TWO>(__ldg(SUMS + sr * w + sc), ts, ssc, a.alpha, e))) {
             FB_CNT(14);
             continue;
         }
@@ -1700,7 +1739,7 @@ cudaError_t launch_upsample(const int2* Fc, int2* Ff, int T, long long fstride, 
 cudaError_t launch_patch_sums(const SumJob* jobs, int n, int fmt, PLvl L, int p, cudaStream_t s)
 {
     if (n <= 0) return cudaSuccess;
-    if (fmt != SF8 && fmt != SF10 && fmt != SF16) return cudaErrorInvalidValue;
+    if (fmt != SF8 && fmt != SF10 && fmt != SF16 && fmt != SF8F) return cudaErrorInvalidValue;
     cudaError_t e = cudaSuccess;
     FB_DISPATCH_P(p, (e = for_y_chunks(n, [&](long long y0, int m) {
         k_patch_sums<PP><<<grid1d((long long)L.h * L.w, m), 256, 0, s>>>(jobs + y0, fmt, L);

@@ -518,3 +518,17 @@ def test_patch_sum_bound_matches_oracle(fb, loss, H, W, sb, l1, rows):
     assert_nnf(F, E, Fr, Er)
     if loss != 0:
         assert_frames(X, Xr)
+
+
+@pytest.mark.parametrize("sb", [0, 1])
+def test_patch_sum_bound_tree_blend(fb, sb):
+    """Fast mode: the tree queries' float-style sources (SF8F blending-table cells) carry FP32 patch sums with an
+    absolute margin; the blend equals the oracle bit for bit with the bound on and off."""
+    c = fb.Context(0)
+    c.set_option(fb.fb.OPT_SUM_BOUND, sb)
+    g, s = moving_texture(9, 72, 96, seed=53)
+    cfg = fb.MatchCfg(iters_per_level=3, loss=fb.GUIDE_STYLE, levels=2)
+    out, st = c.fb_blend_window(cfg, fb.TREE, dev(g), dev(s), 4)
+    ref, pairs, evals = O.blend_tree(ocfg(cfg), g, s, 4)
+    assert st["candidate_evals"] == evals
+    assert_frames(out, ref)
