@@ -111,7 +111,8 @@ uint64_t fb_launch_count(fb_ctx ctx);
  *   FB_OPT_FUSED_ITER   0  1 = a whole level-0 iteration per launch (k_iter_fast; measured slower)
  *   FB_OPT_FUSE13       1  0 = level-0 propagation fields 1-3 and the random search as separate launches
  *   FB_OPT_PHASE0_MID   1  0 = level-0 E init + field 0 with the register-target kernel
- *   FB_OPT_TGT_REG_ROWS 1  target patch rows held in registers by the fused level-0 kernel (0 = all, 1, 2)
+ *   FB_OPT_TGT_REG_ROWS 3  target patch rows held in registers by the fused level-0 kernel (0 = all, 1, 2,
+ *                          3 = none: every row from the shared tile)
  *   FB_OPT_L1_FAST      0  1 = level 1 (u8 sources, p = 2) through 16-byte TF10 targets and the fused
  *                          fields-1-3 kernel instead of the general kernel (bit-identical, measured slower)
  *   FB_OPT_SUM_BOUND    1  0 = no patch-sum lower bound in the random search (every candidate gathers its

@@ -36,10 +36,11 @@ struct fb_ctx_s {
     bool fuse13 = true;  // FB_OPT_FUSE13: fields 1-3 + random search fused on the fast path
     bool phase0_mid = true;  // FB_OPT_PHASE0_MID: E init + field 0 at level 0 through the shared-memory-target
                              // kernel (0: register target; 44 vs 163 registers: field0.L0 95 -> 76 ms at N=48)
-    int tgt_reg_rows = 1;  // FB_OPT_TGT_REG_ROWS: fused fields 1-3 target rows in registers, rest in shared
-                           // memory (0 = all in registers).  With the patch-sum bound most random-search
-                           // candidates never read a target row: one register row at 6 CTAs/SM beats two at 5
-                           // (accurate N=48: field123.L0 353 -> 333 ms)
+    int tgt_reg_rows = 3;  // FB_OPT_TGT_REG_ROWS: fused fields 1-3 target rows in registers, rest in shared
+                           // memory (0 = all in registers, 3 = none).  With the patch-sum bound most random-
+                           // search candidates never read a target row, and occupancy wins: N=48 field123.L0
+                           // two rows at 5 CTAs/SM 353 ms, one row at 6: 333, none at 8: 324 (accurate);
+                           // 285 -> 268 balanced, 112 -> 102 fast
     bool sum_bound = true;  // FB_OPT_SUM_BOUND: random-search candidates rejected by the patch-sum bound (level 0,
                             // and level 1 with FB_OPT_L1_FAST) before any patch row is gathered
     bool l1_fast = false;  // FB_OPT_L1_FAST: level 1 of u8 sources (SF10) through the level-0 kernel structure
@@ -1183,7 +1184,7 @@ fb_status fb_set_option(fb_ctx ctx, int option, int value)
     case FB_OPT_L1_FAST: ctx->l1_fast = value != 0; break;
     case FB_OPT_SUM_BOUND: ctx->sum_bound = value != 0; break;
     case FB_OPT_TGT_REG_ROWS:
-        if (value < 0 || value > 2) { ctx->err = "tgt_reg_rows must be 0, 1 or 2"; return FB_ERR_INVALID_ARG; }
+        if (value < 0 || value > 3) { ctx->err = "tgt_reg_rows must be 0 (all), 1, 2 or 3 (none)"; return FB_ERR_INVALID_ARG; }
         ctx->tgt_reg_rows = value;
         break;
     default: ctx->err = "unknown option"; return FB_ERR_INVALID_ARG;

@@ -1026,7 +1026,10 @@ template <int P, bool TWO, bool PW = false, int SFL = 0, int NR = 2 * P + 1, int
 #ifndef I13_HY1_MINB
 #define I13_HY1_MINB 6  // one target row in registers
 #endif
-__global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (SFL ? I13_SFL_MINB : (NR == 1 ? I13_HY1_MINB : I13_HY_MINB)) : 3) k_iter13_fast(FieldArgs a)
+#ifndef I13_HY0_MINB
+#define I13_HY0_MINB 8  // no target row in registers (every row from the shared tile)
+#endif
+__global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? I13_HY0_MINB : (SFL ? I13_SFL_MINB : (NR == 1 ? I13_HY1_MINB : I13_HY_MINB))) : 3) k_iter13_fast(FieldArgs a)
 {
     constexpr int D = 2 * P + 1;
     constexpr bool HY = NR < D;
@@ -1043,8 +1046,8 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (SFL ? I13_SFL_M
     const uint2* S = reinterpret_cast<const uint2*>(T.src + a.src_off);
     const uint4* Tt = reinterpret_cast<const uint4*>(T.tgt);
     constexpr int NRR = HY ? NR : D;
-    uint32_t tgG[NRR][D];
-    float tgA[NRR][D][3];
+    uint32_t tgG[NRR > 0 ? NRR : 1][D];
+    float tgA[NRR > 0 ? NRR : 1][D][3];
     constexpr int TTY = HY ? I13_TY + 2 * P : 1, TTX = HY ? 32 + 2 * P : 1;
     __shared__ uint4 tT[TTY][TTX];
     if (HY) {  // the CTA's target tile (rows r0-P.., cols c0-P..), zero outside the padded plane
@@ -1849,7 +1852,7 @@ cudaError_t launch_iter13_fast(const FieldArgs& a0, int T, int p, int loss, cuda
     a.tiles_x = (a.L.w + IT_TX - 1) / IT_TX;
     a.tiles_per_task = a.tiles_x * ((a.L.h + I13_TY - 1) / I13_TY);
     const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(32 * I13_TY);
-    const int hy = a.tgt_reg_rows;  // hybrid target (rows in registers; 0 = all)
+    const int hy = a.tgt_reg_rows;  // hybrid target (rows in registers: 1, 2; 3 = none; 0 = all)
     if (a.src_fmt == SF10) {  // level 1: SF10 source + TF10 target (GUIDE_STYLE / MEAN_ALIGN, p = 2)
         if (p != 2 || (loss != 1 && loss != 2)) return cudaErrorInvalidValue;
         if (hy == 1) k_iter13_fast<2, true, false, 0, 1, 1><<<grid, block, 0, s>>>(a);
@@ -1859,14 +1862,16 @@ cudaError_t launch_iter13_fast(const FieldArgs& a0, int T, int p, int loss, cuda
     if (a.src_fmt == SF8F) {
         if (loss != 1 && loss != 2) return cudaErrorInvalidValue;
         if (p == 1) k_iter13_fast<1, true, false, 1><<<grid, block, 0, s>>>(a);
+        else if (p == 2 && hy == 3) k_iter13_fast<2, true, false, 1, 0><<<grid, block, 0, s>>>(a);
         else if (p == 2 && hy == 1) k_iter13_fast<2, true, false, 1, 1><<<grid, block, 0, s>>>(a);
         else if (p == 2 && hy == 2) k_iter13_fast<2, true, false, 1, 2><<<grid, block, 0, s>>>(a);
         else if (p == 2) k_iter13_fast<2, true, false, 1><<<grid, block, 0, s>>>(a);
         else return cudaErrorInvalidValue;
         return cudaGetLastError();
     }
-    if (p == 2 && loss != 3 && (hy == 1 || hy == 2)) {
-        if (loss && hy == 1) k_iter13_fast<2, true, false, 0, 1><<<grid, block, 0, s>>>(a);
+    if (p == 2 && loss != 3 && hy >= 1) {
+        if (loss && hy == 3) k_iter13_fast<2, true, false, 0, 0><<<grid, block, 0, s>>>(a);
+        else if (loss && hy == 1) k_iter13_fast<2, true, false, 0, 1><<<grid, block, 0, s>>>(a);
         else if (loss) k_iter13_fast<2, true, false, 0, 2><<<grid, block, 0, s>>>(a);
         else if (hy == 1) k_iter13_fast<2, false, false, 0, 1><<<grid, block, 0, s>>>(a);
         else k_iter13_fast<2, false, false, 0, 2><<<grid, block, 0, s>>>(a);

@@ -499,7 +499,8 @@ def test_level1_fast_path_nnf_and_error(fb, l1_fast):
 
 @pytest.mark.parametrize("loss,H,W,sb,l1,rows", [(1, 96, 112, 1, 0, 1), (2, 96, 112, 1, 0, 1), (0, 64, 80, 1, 0, 1),
                                                  (1, 96, 112, 0, 0, 1), (2, 135, 67, 1, 1, 1), (1, 128, 112, 1, 1, 1),
-                                                 (2, 96, 112, 1, 0, 0), (2, 96, 112, 1, 0, 2), (1, 67, 135, 1, 0, 2)])
+                                                 (2, 96, 112, 1, 0, 0), (2, 96, 112, 1, 0, 2), (1, 67, 135, 1, 0, 2),
+                                                 (2, 96, 112, 1, 0, 3), (0, 64, 80, 1, 0, 3)])
 def test_patch_sum_bound_matches_oracle(fb, loss, H, W, sb, l1, rows):
     """The random search's patch-sum bound (FB_OPT_SUM_BOUND) only skips candidates that provably
     lose the strict select: NNF and E equal the oracle bit for bit with the bound on and off, at level 0 and, with
@@ -520,12 +521,13 @@ def test_patch_sum_bound_matches_oracle(fb, loss, H, W, sb, l1, rows):
         assert_frames(X, Xr)
 
 
-@pytest.mark.parametrize("sb", [0, 1])
-def test_patch_sum_bound_tree_blend(fb, sb):
+@pytest.mark.parametrize("sb,rows", [(0, 1), (1, 1), (1, 3)])
+def test_patch_sum_bound_tree_blend(fb, sb, rows):
     """Fast mode: the tree queries' float-style sources (SF8F blending-table cells) carry FP32 patch sums with an
     absolute margin; the blend equals the oracle bit for bit with the bound on and off."""
     c = fb.Context(0)
     c.set_option(fb.fb.OPT_SUM_BOUND, sb)
+    c.set_option(fb.fb.OPT_TGT_REG_ROWS, rows)
     g, s = moving_texture(9, 72, 96, seed=53)
     cfg = fb.MatchCfg(iters_per_level=3, loss=fb.GUIDE_STYLE, levels=2)
     out, st = c.fb_blend_window(cfg, fb.TREE, dev(g), dev(s), 4)
