@@ -1855,7 +1855,8 @@ cudaError_t launch_iter13_fast(const FieldArgs& a0, int T, int p, int loss, cuda
     const int hy = a.tgt_reg_rows;  // hybrid target (rows in registers: 1, 2; 3 = none; 0 = all)
     if (a.src_fmt == SF10) {  // level 1: SF10 source + TF10 target (GUIDE_STYLE / MEAN_ALIGN, p = 2)
         if (p != 2 || (loss != 1 && loss != 2)) return cudaErrorInvalidValue;
-        if (hy == 1) k_iter13_fast<2, true, false, 0, 1, 1><<<grid, block, 0, s>>>(a);
+        if (hy == 3) k_iter13_fast<2, true, false, 0, 0, 1><<<grid, block, 0, s>>>(a);
+        else if (hy == 1) k_iter13_fast<2, true, false, 0, 1, 1><<<grid, block, 0, s>>>(a);
         else k_iter13_fast<2, true, false, 0, 2, 1><<<grid, block, 0, s>>>(a);
         return cudaGetLastError();
     }
