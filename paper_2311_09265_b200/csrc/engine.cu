@@ -43,10 +43,10 @@ struct fb_ctx_s {
                            // 285 -> 268 balanced, 112 -> 102 fast
     bool sum_bound = true;  // FB_OPT_SUM_BOUND: random-search candidates rejected by the patch-sum bound (level 0,
                             // and level 1 with FB_OPT_L1_FAST) before any patch row is gathered
-    bool l1_fast = false;  // FB_OPT_L1_FAST: level 1 of u8 sources (SF10) through the level-0 kernel structure
-                           // (16-byte TF10 targets, fused fields 1-3 + random search); bit-identical but slower
-                           // (N=48 accurate 683 -> 724 ms: field123.L1 158 ms vs 113 for fields 1-3 of the
-                           // general kernel), so off by default
+    int l1_fast = 0;  // FB_OPT_L1_FAST: level 1 of u8 sources (SF10) through 16-byte TF10 targets and the
+                      // level-0 kernels -- 1: E init + field 0 by the shared-tile kernel, fields 1-3 + random
+                      // search fused; 2: every field by the shared-tile kernel.  Bit-identical; 1 measured slower
+                      // (N=48 accurate: field123.L1 146 ms vs 102 for fields 1-3 of the general kernel)
     std::string err;
     // kernel timing (fb_profile_*)
     bool prof = false;
@@ -528,7 +528,7 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
             for (int j = J - 1; j >= 0; --j) {
                 a.step = 1 << j;
                 const bool last = j == 0;
-                if (last && (fast || l1) && ex.ctx->fuse13) {  // field 0, then fields 1-3 + random search in one launch
+                if (last && (fast || (l1 && ex.ctx->l1_fast == 1)) && ex.ctx->fuse13) {  // field 0, then fields 1-3 + random search in one launch
                     a.Fin = F[cur]; a.Fout = F[cur ^ 1];
                     const int kind0 = (l1 || (ex.ctx->phase0_mid && !pairwise && g.p == 2 &&
                                               (a.src_fmt == fbk::SF8 || a.src_fmt == fbk::SF8F))) ? 2 : kind;
@@ -1181,7 +1181,10 @@ fb_status fb_set_option(fb_ctx ctx, int option, int value)
     case FB_OPT_FUSED_ITER: ctx->fused = value != 0; break;
     case FB_OPT_FUSE13: ctx->fuse13 = value != 0; break;
     case FB_OPT_PHASE0_MID: ctx->phase0_mid = value != 0; break;
-    case FB_OPT_L1_FAST: ctx->l1_fast = value != 0; break;
+    case FB_OPT_L1_FAST:
+        if (value < 0 || value > 2) { ctx->err = "l1_fast must be 0, 1 or 2"; return FB_ERR_INVALID_ARG; }
+        ctx->l1_fast = value;
+        break;
     case FB_OPT_SUM_BOUND: ctx->sum_bound = value != 0; break;
     case FB_OPT_TGT_REG_ROWS:
         if (value < 0 || value > 3) { ctx->err = "tgt_reg_rows must be 0 (all), 1, 2 or 3 (none)"; return FB_ERR_INVALID_ARG; }
