@@ -74,3 +74,25 @@ while R >= 1:
     R >>= 1
 c = tot["cands"]
 print("all radii: " + "  ".join(f"{k} {v/c:.3f}" for k, v in tot.items() if k != "cands"))
+
+# variants of the bound with compact sums (8-byte texels): guide-only, and style sums quantised to 32-unit bins
+tot2 = dict(cands=0, lose=0, full_mean=0, guide_only=0, qstyle=0)
+R = H
+rng = np.random.default_rng(1)
+while R >= 1:
+    off = rng.integers(-R, R + 1, size=(H, H, 2))
+    cr = np.clip(F[..., 0] + off[..., 0], 0, H - 1)
+    cc = np.clip(F[..., 1] + off[..., 1], 0, H - 1)
+    sg, ss = patches(Gs, cr, cc), patches(Ss, cr, cc)
+    full = alpha * ((sg - tg) ** 2).sum((-3, -2, -1)) + ((ss - ta) ** 2).sum((-3, -2, -1))
+    gl = alpha * ((sg.sum((-3, -2)) - tg.sum((-3, -2))) ** 2).sum(-1) / n
+    ssum, tsum = ss.sum((-3, -2)), ta.sum((-3, -2))
+    sl = ((ssum - tsum) ** 2).sum(-1) / n
+    q = np.floor(ssum / 32) * 32
+    dq = np.maximum(np.maximum(q - tsum, tsum - (q + 31)), 0)
+    ql = (dq ** 2).sum(-1) / n
+    for k, v in (("cands", full.size), ("lose", (full >= E).sum()), ("full_mean", (gl + sl >= E).sum()),
+                 ("guide_only", (gl >= E).sum()), ("qstyle", (gl + ql >= E).sum())):
+        tot2[k] += v
+    R >>= 1
+print("compact sums: " + "  ".join(f"{k} {v / tot2['cands']:.3f}" for k, v in tot2.items() if k != "cands"))
