@@ -1484,6 +1484,14 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
     const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
     const int h = a.L.h, w = a.L.w, pitch = a.L.pitch;
     const DTask T = a.tasks[t];
+    // Exact packed sources (SF10 at level 1, SF16 at levels 2-4): the target guide is held in the tile biased by
+    // the magic of the source decode (2^21 / 2^11 for SF10 channels 0, 2 / 1; 2^(23-2k) for SF16), so that the guide
+    // delta of D20 is one FSUB of two biased values -- exact (same binade, Sterbenz) and equal to t - s -- and the
+    // source guide needs no unbiasing FADD.  The bias is exact: level-k values are multiples of 4^-k below 256.
+    constexpr bool GB = SFMT == SF10 || SFMT == SF16;
+    const uint32_t ex = (uint32_t)(75 - a.L.k) << 24;
+    const float gb0 = SFMT == SF10 ? 2097152.0f : __uint_as_float(ex), gb1 = SFMT == SF10 ? 2048.0f : gb0,
+                gb2 = SFMT == SF10 ? 2097152.0f : gb0;
     {
         const float4* Tt = reinterpret_cast<const float4*>(T.tgt);
         for (int k = threadIdx.x; k < SX * SY; k += TILE_X * TILE_Y) {
@@ -1494,6 +1502,7 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
                 v0 = __ldg(&Tt[2 * (pr * pitch + pc)]);
                 v1 = __ldg(&Tt[2 * (pr * pitch + pc) + 1]);
             }
+            if (GB) { v0.x = __fadd_rn(v0.x, gb0); v0.y = __fadd_rn(v0.y, gb1); v0.z = __fadd_rn(v0.z, gb2); }
             t0[yy][xx] = v0;
             t1[yy][xx] = make_float2(v1.x, v1.y);
         }
@@ -1511,13 +1520,13 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
         ts = tile_patch_sums<P>(lx, ly, [&](int yy, int xx, float (&v)[6]) {
             const float4 q0 = t0[yy][xx];
             const float2 q1 = t1[yy][xx];
-            v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w; v[4] = q1.x; v[5] = q1.y;
+            v[0] = __fsub_rn(q0.x, gb0); v[1] = __fsub_rn(q0.y, gb1); v[2] = __fsub_rn(q0.z, gb2);  // exact unbias
+            v[3] = q0.w; v[4] = q1.x; v[5] = q1.y;
         });
     const int c = tx * TILE_X + lx, r = ty * TILE_Y + ly;
     if (r >= h || c >= w) return;
     const float4* S = reinterpret_cast<const float4*>(T.src + a.src_off);
     const uint4* S16 = reinterpret_cast<const uint4*>(T.src + a.src_off);
-    const uint32_t ex = (uint32_t)(75 - a.L.k) << 24;
     float pa[PW ? D : 1][PW ? D : 1][3];  // PAIRWISE reference patch (Eq. 10, D39)
     if (PW) {
         const int2 q = __ldg(&T.pF[r * w + c]);
@@ -1566,14 +1575,14 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
 #pragma unroll
         for (int dc = 0; dc < D; ++dc) {
             float4 s0, s1;
-            if (SFMT == SF10) {
+            if (SFMT == SF10) {  // guide biased (see GB), style exact
                 const uint32_t gw = wd[SFMT == SF10 ? 2 * dc : 0], sw = wd[SFMT == SF10 ? 2 * dc + 1 : 0];
-                s0 = make_float4(f10_0(gw), f10_1(gw), f10_2(gw), TWO ? f10_0(sw) : 0.0f);
+                s0 = make_float4(b10_0(gw), b10_1(gw), b10_2(gw), TWO ? f10_0(sw) : 0.0f);
                 s1 = TWO ? make_float4(f10_1(sw), f10_2(sw), 0.0f, 0.0f) : s0;
             } else if (SFMT == SF16) {
                 const uint4 v = __ldg(&S16[base + dc]);
-                s0 = make_float4(u16f(v.x, 0x7410u, ex), u16f(v.x, 0x7432u, ex), u16f(v.y, 0x7410u, ex),
-                                 TWO ? u16f(v.z, 0x7410u, ex) : 0.0f);
+                s0 = make_float4(__uint_as_float(__byte_perm(v.x, ex, 0x7410u)), __uint_as_float(__byte_perm(v.x, ex, 0x7432u)),
+                                 __uint_as_float(__byte_perm(v.y, ex, 0x7410u)), TWO ? u16f(v.z, 0x7410u, ex) : 0.0f);
                 s1 = TWO ? make_float4(u16f(v.z, 0x7432u, ex), u16f(v.w, 0x7410u, ex), 0.0f, 0.0f) : s0;
             } else {
                 s0 = __ldg(&S[2 * (base + dc)]);
