@@ -1204,40 +1204,53 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? I13_H
     const int i = r * w + c;
     int2 f = make_int2(0, 0);
     float e = 0.0f;
-    // field 1: d = (+1,0), neighbour (r+1, c) of F_in (= the field-0 result), clamped (D11)
+    // Fields 1-3 in one loop with one select site (smaller code: the fused kernel is sensitive to instruction-
+    // cache misses), converged at the top of every iteration:
+    //   fld 0: field 1, d = (+1,0), neighbour (r+1, c) of F_in (= the field-0 result), clamped (D11);
+    //   fld 1: field 2, d = (0,-1), neighbour (r, c-1) of the field-1 result (lane - 1, by shuffle);
+    //   fld 2: field 3, d = (0,+1), neighbour (r, c+1) of the field-2 result (lane + 1); halo lanes skip it.
     if (valid) {
         f = Fi[i];
         e = a.E[t * a.fstride + i];
-        const int2 fn = r + 1 < h ? Fi[i + w] : f;
-        select(f, e, max(fn.x - 1, 0), fn.y);
     }
-    // field 2: d = (0,-1), neighbour (r, c-1) of the field-1 result (lane - 1)
-    {
-        const int2 fl = make_int2(__shfl_up_sync(0xffffffffu, f.x, 1), __shfl_up_sync(0xffffffffu, f.y, 1));
-        if (valid && lane > 0) {
-            const int2 fn = c > 0 ? fl : f;
-            select(f, e, fn.x, min(fn.y + 1, w - 1));
+#pragma unroll 1
+    for (int fld = 0; fld < 3; ++fld) {
+        const int2 nb = make_int2(__shfl_sync(0xffffffffu, f.x, fld == 1 ? lane - 1 : lane + 1),
+                                  __shfl_sync(0xffffffffu, f.y, fld == 1 ? lane - 1 : lane + 1));
+        int2 cand;
+        bool has;
+        if (fld == 0) {
+            has = valid;
+            const int2 fn = valid && r + 1 < h ? Fi[i + w] : f;
+            cand = make_int2(max(fn.x - 1, 0), fn.y);
+        } else if (fld == 1) {
+            has = valid && lane > 0;
+            const int2 fn = c > 0 ? nb : f;
+            cand = make_int2(fn.x, min(fn.y + 1, w - 1));
+        } else {
+            has = valid && lane > 0 && lane < 31;
+            const int2 fn = c + 1 < w ? nb : f;
+            cand = make_int2(fn.x, max(fn.y - 1, 0));
         }
+        if (has) select(f, e, cand.x, cand.y);
     }
-    // field 3: d = (0,+1), neighbour (r, c+1) of the field-2 result (lane + 1), then random search
-    const int2 fr = make_int2(__shfl_down_sync(0xffffffffu, f.x, 1), __shfl_down_sync(0xffffffffu, f.y, 1));
-    // Target patch sums of the bound, while all 32 lanes are converged: column sums over the D patch rows of
-    // the shared tile (tile columns 32.. by lanes 0..2P-1), then the D columns of each lane's patch by shuffles.
     TSums ts{};
-    if (use_csb) {
+    if (use_csb) {  // target patch sums of the bound, warp converged: column sums over the D rows of the shared
+                    // tile (columns 32.. by lanes 0..2P-1), then the D columns of each lane's patch by shuffles
         uint32_t cg[2][2] = {{0u, 0u}, {0u, 0u}};  // [main, extra] {g0 | g1 << 16, g2}
         float ca[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};  // {a0, a1, a2, max_c sum|a_c|}
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
-            if (x == 1 && lane >= 2 * P) break;
             float b0 = 0.f, b1 = 0.f, b2 = 0.f;
 #pragma unroll
             for (int dr = 0; dr < D; ++dr) {
+                if (x == 1 && lane >= 2 * P) break;  // tile columns 32.. only
                 const uint4 v = tT[CSB ? wy + dr : 0][CSB ? lane + 32 * x : 0];
                 if (SF == 1) { cg[x][0] += (v.x & 0x3FFu) | (((v.x >> 10) & 0x3FFu) << 16); cg[x][1] += v.x >> 20; }
                 else { cg[x][0] += (v.x & 0xFFu) | (((v.x >> 8) & 0xFFu) << 16); cg[x][1] += (v.x >> 16) & 0xFFu; }
                 const float t0 = __uint_as_float(v.y), t1 = __uint_as_float(v.z), t2 = __uint_as_float(v.w);
-                ca[x][0] = __fadd_rn(ca[x][0], t0); ca[x][1] = __fadd_rn(ca[x][1], t1); ca[x][2] = __fadd_rn(ca[x][2], t2);
+                ca[x][0] = __fadd_rn(ca[x][0], t0); ca[x][1] = __fadd_rn(ca[x][1], t1);
+                ca[x][2] = __fadd_rn(ca[x][2], t2);
                 b0 = __fadd_ru(b0, fabsf(t0)); b1 = __fadd_ru(b1, fabsf(t1)); b2 = __fadd_ru(b2, fabsf(t2));
             }
             ca[x][3] = fmaxf(b0, fmaxf(b1, b2));
@@ -1259,13 +1272,10 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? I13_H
             m = __fadd_ru(m, own ? p3 : q3);
         }
         constexpr float gsc = SF == 1 ? 0.25f : 1.0f;
-        ts = TSums{(float)(g01 & 0xFFFFu) * gsc, (float)(g01 >> 16) * gsc, (float)g2 * gsc, a0, a1, a2, csb_margin<D>(m)};
+        ts = TSums{(float)(g01 & 0xFFFFu) * gsc, (float)(g01 >> 16) * gsc, (float)g2 * gsc, a0, a1, a2,
+                   csb_margin<D>(m)};
     }
-    if (!valid || lane == 0 || lane == 31) return;
-    {
-        const int2 fn = c + 1 < w ? fr : f;
-        select(f, e, fn.x, max(fn.y - 1, 0));
-    }
+    if (!valid || lane == 0 || lane == 31) return;  // halo lanes only fed fields 1-2
 #pragma unroll
     for (int z = 0; z < 2; ++z)  // tracking fields T_{i-1}, T_{i+1} (D42)
         if (T.trk[z]) {
