@@ -69,8 +69,9 @@ typedef struct {
     uint64_t seed;           /* Philox4x32-10 key (D21)                                             */
     int32_t prop_scales;     /* propagation scales J (jump flood, D41): steps 2^(J-1)..1, each with the
                                 four directions of P:72; 0 or 1 = the paper's unit-step propagation   */
-    int32_t tracking;        /* interpolation: add NNF(S,T_{i-1}), NNF(S,T_{i+1}) as candidate fields
-                                (D42); 0 = off                                            */
+    int32_t tracking;        /* add NNF(S,T_{i-1}), NNF(S,T_{i+1}) as candidate fields: interpolation
+                                (D42) and the direct blend schedule ("optional setting in
+                                blending", D44: NNF(G_j,G_{i+-1}) for NNF(G_j,G_i)); 0 = off   */
 } fb_match_cfg;
 
 typedef struct {
@@ -174,7 +175,9 @@ fb_status fb_remap(fb_ctx ctx, int B, int H, int W, int p, const float* src, con
  * Alg. 3 build (levels <= floor(log2(M+1)), D24) -> Alg. 4 -> Alg. 5 queries on the forward and the
  * reversed table (D26) -> out_i = ((A_f + A_r) - S_i) / |W_i| (Eq. 6).  M = 0 or N = 1 returns the
  * style exactly.  Sharded runs: only targets in [t0, t1) are written (rows t0..t1-1 of out);
- * fb_blend_window is the full range [0, N). */
+ * fb_blend_window is the full range [0, N).  cfg.tracking = 1 (DIRECT only, "optional setting in
+ * blending", D44) couples every pair of the schedule: one batch over all targets; FB_ERR_UNSUPPORTED for the
+ * tree schedule, for a partial range, or beyond 65535 pairs. */
 fb_status fb_blend_window(fb_ctx ctx, const fb_match_cfg* cfg, int schedule, int N, int H, int W, int M,
                           const uint8_t* guide, const uint8_t* style, float* out, fb_stats* stats);
 /* Same, restricted to output targets [t0, t1) of a video whose frames [f0, f0+N) are given: guide/style

@@ -598,27 +598,43 @@ int orc_blend_direct(const orc_cfg* cfg, int N, int H, int W, int M, const uint8
     float* frames = (float*)malloc(sizeof(float) * 3 * npx * 2 * (size_t)N); /* [G_0..G_N-1, S_0..S_N-1] */
     u8_to_float(guide, 3 * npx * N, frames);
     u8_to_float(style, 3 * npx * N, frames + 3 * npx * N);
+    /* Tracking in blending ("optional setting", reading D44): NNF(G_j, G_i) also tries the same source's
+     * NNFs for the neighbouring targets, NNF(G_j, G_{i-1}) and NNF(G_j, G_{i+1}) when those pairs exist, frozen at
+     * the start of each iteration (D42).  Every pair is then coupled to its neighbours, so all targets' pairs
+     * are estimated together and the requested targets are read out of that run. */
+    int nt = cfg->tracking ? N : n_targets;
+    int32_t* tl = (int32_t*)malloc(sizeof(int32_t) * (nt > 0 ? nt : 1));
+    for (int q = 0; q < nt; ++q) tl[q] = cfg->tracking ? q : targets[q];
     int maxT = 0;
-    for (int q = 0; q < n_targets; ++q) maxT += 2 * M;
+    for (int q = 0; q < nt; ++q) maxT += 2 * M;
     orc_task* tasks = (orc_task*)malloc(sizeof(orc_task) * (maxT + 1));
+    int* first = (int*)malloc(sizeof(int) * (nt + 1));
     int T = 0;
-    for (int q = 0; q < n_targets; ++q) {
-        int i = targets[q], lo = i - M < 0 ? 0 : i - M, hi = i + M > N - 1 ? N - 1 : i + M;
+    for (int q = 0; q < nt; ++q) {
+        int i = tl[q], lo = i - M < 0 ? 0 : i - M, hi = i + M > N - 1 ? N - 1 : i + M;
+        first[q] = T;
         for (int j = lo; j <= hi; ++j) {
             if (j == i) continue;
             orc_task tk = { j, i, N + j, cfg->loss == ORC_MEAN_ALIGN ? N + i : -1, q, j, i, ORC_TAG_DIRECT, -1, -1, -1 };
             tasks[T++] = tk;
         }
     }
+    if (cfg->tracking) /* tl = 0..N-1: the task (j, i') sits in target i''s list */
+        for (int a = 0; a < T; ++a)
+            for (int z = 0; z < 2; ++z) {
+                int i2 = tasks[a].tgt_id + (z == 0 ? -1 : 1), j = tasks[a].src_id;
+                if (i2 < 0 || i2 >= N || i2 == j) continue;
+                for (int b = first[i2]; b < (i2 + 1 < nt ? first[i2 + 1] : T); ++b)
+                    if (tasks[b].src_id == j) { if (z == 0) tasks[a].track_prev = b; else tasks[a].track_next = b; }
+            }
     float* X = (float*)malloc(sizeof(float) * 3 * npx * (T > 0 ? T : 1));
     uint64_t evals = 0;
     if (T > 0 && orc_nnf(cfg, T, H, W, frames, tasks, NULL, NULL, X, &evals) != 0) {
-        free(frames); free(tasks); free(X); return -1;
+        free(frames); free(tasks); free(X); free(tl); free(first); return -1;
     }
-    int t = 0;
     for (int q = 0; q < n_targets; ++q) {
         int i = targets[q], lo = i - M < 0 ? 0 : i - M, hi = i + M > N - 1 ? N - 1 : i + M;
-        int t0 = t;
+        int t0 = first[cfg->tracking ? i : q];
         float* o = out + 3 * npx * q;
         for (size_t e = 0; e < 3 * npx; ++e) {
             float a = 0.0f;
@@ -629,11 +645,10 @@ int orc_blend_direct(const orc_cfg* cfg, int N, int H, int W, int M, const uint8
             }
             o[e] = a / (float)(hi - lo + 1);
         }
-        t = t0 + (hi - lo);
     }
     if (pairs_out) *pairs_out = (uint64_t)T;
     if (evals_out) *evals_out = evals;
-    free(frames); free(tasks); free(X);
+    free(frames); free(tasks); free(X); free(tl); free(first);
     return 0;
 }
 

@@ -641,7 +641,13 @@ void blend_direct(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int N_total, 
     const long long n0 = g.npx0();
     std::vector<int> cost;
     for (int i = t0; i < t1; ++i) cost.push_back(std::min(N_total - 1, i + M) - std::max(0, i - M));
-    const auto batches = make_batches(cost, batch_pairs(ex.ctx, g, cfg.loss));
+    // tracking in blending (reading D44) couples every pair of the schedule: one batch
+    long long total = 0;
+    for (int c : cost) total += c;
+    if (cfg.tracking && total > kMaxBatchPairs)
+        throw Fail{FB_ERR_UNSUPPORTED, "tracking in blending needs all pairs of the schedule in one batch"};
+    const auto batches = cfg.tracking ? std::vector<std::pair<int, int>>{{0, t1 - t0}}
+                                      : make_batches(cost, batch_pairs(ex.ctx, g, cfg.loss));
     const size_t mark = ex.ar.off;
     for (auto [b0, b1] : batches) {
         Nvtx nv(ex.dry, "direct batch targets [%d, %d)", t0 + b0, t0 + b1);
@@ -668,6 +674,15 @@ void blend_direct(Exec& ex, const fb_match_cfg& cfg, const Geo& g, int N_total, 
                 tasks.push_back(TaskSpec{FR.slot(j - lo_b), S.frame(j - lo_b), G.frame(i - lo_b),
                                          cfg.loss == FB_LOSS_MEAN_ALIGN ? q - b0 : -1, (uint32_t)j, (uint32_t)i, 0u});
             }
+        }
+        if (cfg.tracking) {  // D44: NNF(G_j -> G_i) also tries NNF(G_j -> G_{i-1}) and NNF(G_j -> G_{i+1})
+            std::map<std::pair<uint32_t, uint32_t>, int> idx;
+            for (int k = 0; k < (int)tasks.size(); ++k) idx[{tasks[k].src_id, tasks[k].tgt_id}] = k;
+            for (TaskSpec& tk : tasks)
+                for (int z = 0; z < 2; ++z) {
+                    const auto it = idx.find({tk.src_id, z == 0 ? tk.tgt_id - 1 : tk.tgt_id + 1});
+                    if (it != idx.end()) tk.track[z] = it->second;
+                }
         }
         BatchOut bo;
         if (!tasks.empty()) bo = run_nnf(ex, cfg, g, FR, tasks, groups, st);
@@ -1302,6 +1317,10 @@ static void blend_range_body(Exec& ex, fb_stats* st, const fb_match_cfg* cfg, in
     if (t0 < 0 || t1 > N_total || t0 >= t1) throw Fail{FB_ERR_INVALID_ARG, "bad target range"};
     if (f0 < 0 || N < 1 || f0 + N > N_total || f0 > std::max(0, t0 - M) || f0 + N < std::min(N_total, t1 + M))
         throw Fail{FB_ERR_INVALID_ARG, "local frames must cover the targets plus a halo of M"};
+    if (cfg->tracking && schedule == FB_SCHED_TREE)
+        throw Fail{FB_ERR_UNSUPPORTED, "tracking in blending is defined for the direct schedule (D44)"};
+    if (cfg->tracking && (t0 > 0 || t1 < N_total))
+        throw Fail{FB_ERR_UNSUPPORTED, "tracking couples every pair of the schedule (D44): use the full call"};
     const Geo g = make_geo(*cfg, H, W);
     if (schedule == FB_SCHED_DIRECT) blend_direct(ex, *cfg, g, N_total, f0, N, M, guide, style, t0, t1, out, st);
     else blend_tree(ex, *cfg, g, N_total, f0, N, M, guide, style, t0, t1, out, st);

@@ -534,3 +534,27 @@ def test_patch_sum_bound_tree_blend(fb, sb, rows):
     ref, pairs, evals = O.blend_tree(ocfg(cfg), g, s, 4)
     assert st["candidate_evals"] == evals
     assert_frames(out, ref)
+
+
+@pytest.mark.parametrize("mode", ["balanced", "accurate"])
+def test_blend_tracking_parity(fb, ctx, mode):
+    """Tracking in blending (P:259 optional setting, D44): every pair NNF(G_j, G_i) also tries NNF(G_j, G_{i+-1});
+    the direct blend equals the oracle bit for bit and evaluates exactly the oracle's candidate count."""
+    g, s = moving_texture(7, 40, 48, seed=57)
+    cfg = fb.MatchCfg(iters_per_level=2, loss=fb.MEAN_ALIGN if mode == "accurate" else fb.GUIDE_STYLE, tracking=1)
+    out, st = ctx.fb_blend_window(cfg, fb.DIRECT, dev(g), dev(s), 2)
+    ref, pairs, evals = O.blend_direct(ocfg(cfg), g, s, 2)
+    assert st["nnf_pairs"] == pairs and st["candidate_evals"] == evals
+    assert_frames(out, ref)
+
+
+def test_blend_tracking_unsupported_forms(fb, ctx):
+    """D44 couples every pair of the schedule: the tree schedule and partial ranges are rejected."""
+    g, s = moving_texture(6, 32, 32, seed=58)
+    cfg = fb.MatchCfg(iters_per_level=1, tracking=1)
+    with pytest.raises(fb.FBError) as e:
+        ctx.fb_blend_window(cfg, fb.TREE, dev(g), dev(s), 2)
+    assert e.value.status == 6
+    with pytest.raises(fb.FBError) as e:
+        ctx.fb_blend_window_range(cfg, fb.DIRECT, 6, 0, dev(g), dev(s), 2, 0, 3)
+    assert e.value.status == 6

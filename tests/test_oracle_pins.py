@@ -843,3 +843,49 @@ def test_tracking_is_jacobi_across_frames():
     Fb, Eb, _, _ = O.nnf(cfg, frames, tasks([3, 2, 1]), want_x=False)
     np.testing.assert_array_equal(Fa, Fb[::-1])
     np.testing.assert_array_equal(Ea, Eb[::-1])
+
+
+def _blend_pairs(N, M):
+    return [(j, i) for i in range(N) for j in range(max(0, i - M), min(N - 1, i + M) + 1) if j != i]
+
+
+def test_blend_tracking_links_and_evals():
+    """Tracking in blending (D44): NNF(G_j, G_i) gets one extra candidate field per existing pair
+    (j, i-1) and (j, i+1) per iteration and level; the pair count is unchanged."""
+    N, M, H = 6, 2, 32
+    g, s = moving_texture(N, H, H, seed=34)
+    base = O.Cfg(iters_per_level=2)
+    _, p0, ev0 = O.blend_direct(base, g, s, M)
+    _, p1, ev1 = O.blend_direct(O.Cfg(iters_per_level=2, tracking=1), g, s, M)
+    pairs = set(_blend_pairs(N, M))
+    links = sum((j, i + d) in pairs for (j, i) in pairs for d in (-1, 1))
+    npx = sum((H >> k) * (H >> k) for k in range(O.level_count(H, H, 2)))
+    assert p0 == p1 == len(pairs)
+    assert ev1 - ev0 == links * npx * 2
+
+
+def test_blend_tracking_recomposed_from_linked_nnf_run():
+    """The tracked blend equals Eq. 2 recomposed from one oracle NNF run over every pair of the schedule
+    with the tracking links written out here (same source, target i-1 / i+1), and a targets subset equals the
+    same rows of the full run (every pair is coupled, so the closure is the whole schedule)."""
+    N, M, H = 5, 2, 24
+    g, s = moving_texture(N, H, H, seed=35)
+    for loss in (O.GUIDE_STYLE, O.MEAN_ALIGN):
+        cfg = O.Cfg(iters_per_level=2, tracking=1, loss=loss)
+        full, _, _ = O.blend_direct(cfg, g, s, M)
+        sub, _, _ = O.blend_direct(cfg, g, s, M, targets=[3, 0])
+        np.testing.assert_array_equal(sub[0], full[3])
+        np.testing.assert_array_equal(sub[1], full[0])
+        pairs = sorted(_blend_pairs(N, M), key=lambda ji: (ji[1], ji[0]))  # the oracle's own order is irrelevant
+        pos = {ji: k for k, ji in enumerate(pairs)}
+        frames = np.concatenate([g, s]).astype(np.float32)
+        tasks = [dict(src_guide=j, tgt_guide=i, src_style=N + j, tgt_style=N + i if loss == O.MEAN_ALIGN else -1,
+                      group=i, src_id=j, tgt_id=i, tag=O.TAG_DIRECT, track_prev=pos.get((j, i - 1), -1),
+                      track_next=pos.get((j, i + 1), -1)) for (j, i) in pairs]
+        _, _, X, _ = O.nnf(cfg, frames, tasks)
+        for i in range(N):
+            lo, hi = max(0, i - M), min(N - 1, i + M)
+            acc = np.zeros((H, H, 3), np.float32)
+            for j in range(lo, hi + 1):
+                acc = acc + (frames[N + i] if j == i else X[pos[(j, i)]])
+            np.testing.assert_array_equal(full[i], acc / np.float32(hi - lo + 1))
