@@ -1305,7 +1305,7 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? I13_H
 // ---- level-0 variant for p = 3, 4: SF8 source, TF16 target tile in shared memory -----------------
 // The target patch of p >= 3 does not fit in registers, so it is staged per tile; the source rows and the
 // exact integer guide term (every partial < 2^24 for p <= 4 at level 0) are those of k_field_fast.
-template <int P, bool TWO, int PHASE, int SFL = 0, int SF = 0>
+template <int P, bool TWO, int PHASE, int SFL = 0, int SF = 0, bool PR = false>
 #ifndef MID_MINB
 #define MID_MINB 8  // p = 2 (phase 0): 8 CTAs/SM at 32 registers beats 5 at 44 (balanced N=48: 68 -> 62 ms)
 #endif
@@ -1315,7 +1315,10 @@ template <int P, bool TWO, int PHASE, int SFL = 0, int SF = 0>
 #ifndef MID10_MINB
 #define MID10_MINB 4  // level-1 SF10 variant (more ALU per tap than the u8 one)
 #endif
-__global__ void __launch_bounds__(TILE_X* TILE_Y, P == 2 ? (SF ? MID10_MINB : MID_MINB) : (P == 3 ? MID3_MINB : 1)) k_field_mid(FieldArgs a)
+#ifndef MIDP_MINB
+#define MIDP_MINB 6  // phase 0 with E init and field 0 scored together (accurate N=48: field0.L0 73.4 -> 67.8 ms)
+#endif
+__global__ void __launch_bounds__(TILE_X* TILE_Y, PR ? MIDP_MINB : (P == 2 ? (SF ? MID10_MINB : MID_MINB) : (P == 3 ? MID3_MINB : 1))) k_field_mid(FieldArgs a)
 {
     constexpr int D = 2 * P + 1, SX = TILE_X + 2 * P, SY = TILE_Y + 2 * P;
     constexpr int NCH = (D + 2) / 2;  // 16-byte chunks covering D texels from an even start
@@ -1450,6 +1453,62 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y, P == 2 ? (SF ? MID10_MINB : MI
     const int2* Fi = a.Fin + t * a.fstride;
     const int i = r * w + c;
     int2 f = Fi[i];
+    // PR (phase 0 of u8 sources, accurate mode): E <- L(F) and the field-0 candidate scored together, row by row,
+    // so each target texel is read from the shared tile once for both (the kernel is bound by the L1/shared data
+    // path).  Each loss keeps its own D20 chain, and the candidate is scored in full instead of with partial-
+    // distance elimination, so the outcome equals E-init followed by the strict select.  Balanced mode keeps the
+    // separate form: its propagation candidates are eliminated early more often (N=48: 61.9 vs 67.2 ms).
+    constexpr bool PAIR0 = PR && PHASE == 0 && SF == 0 && SFL == 0;
+    if (PAIR0 && a.einit) {
+        const int dx = -a.step;  // field 0: d = (-1,0), jump-flood step (D41)
+        const int nr = clampi(r + dx, 0, h - 1);  // D11
+        const int2 fn = Fi[nr * w + c];
+        const int cr = clampi(fn.x - dx, 0, h - 1), cc = clampi(fn.y, 0, w - 1);  // D10
+        const bool two = cr != f.x || cc != f.y;
+        uint32_t dgA = 0u, dgB = 0u;
+        float dsA = 0.0f, dsB = 0.0f;
+#pragma unroll
+        for (int dr = 0; dr < D; ++dr) {
+            uint32_t wa[4 * NCH], wb[4 * NCH];
+            const int ia = (f.x + dr - P + B) * pitch + (f.y - P + B), ib = (cr + dr - P + B) * pitch + (cc - P + B);
+            FB_ASSERT(FB_ROW_OK(ia, a.L, D) && FB_ROW_OK(ib, a.L, D));
+            const uint4* pa = reinterpret_cast<const uint4*>(S + (size_t)(ia & 1) * plane + (ia & ~1));
+            const uint4* pb = reinterpret_cast<const uint4*>(S + (size_t)(ib & 1) * plane + (ib & ~1));
+#pragma unroll
+            for (int k = 0; k < NCH; ++k) {
+                const uint4 v = __ldg(pa + k);
+                wa[4 * k] = v.x; wa[4 * k + 1] = v.y; wa[4 * k + 2] = v.z; wa[4 * k + 3] = v.w;
+                const uint4 u = two ? __ldg(pb + k) : v;
+                wb[4 * k] = u.x; wb[4 * k + 1] = u.y; wb[4 * k + 2] = u.z; wb[4 * k + 3] = u.w;
+            }
+            float ra = 0.0f, rb = 0.0f;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const uint4 tv = tT[ly + dr][lx + j];
+                uint32_t d = __vabsdiffu4(wa[2 * j], tv.x);
+                dgA = __dp4a(d, d, dgA);
+                d = __vabsdiffu4(wb[2 * j], tv.x);
+                dgB = __dp4a(d, d, dgB);
+                if (TWO) {
+                    const uint32_t sa = wa[2 * j + 1], sb = wb[2 * j + 1];
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) {
+                        const float tc = __uint_as_float(ch == 0 ? tv.y : (ch == 1 ? tv.z : tv.w));
+                        float dl = __fsub_rn(tc, u8f(sa, ch)); ra = __fmaf_rn(dl, dl, ra);
+                        dl = __fsub_rn(tc, u8f(sb, ch)); rb = __fmaf_rn(dl, dl, rb);
+                    }
+                }
+            }
+            if (TWO) { dsA = __fadd_rn(dsA, ra); dsB = __fadd_rn(dsB, rb); }
+        }
+        const float eA = TWO ? __fmaf_rn(a.alpha, __uint2float_rn(dgA), dsA) : __uint2float_rn(dgA);
+        const float eB = TWO ? __fmaf_rn(a.alpha, __uint2float_rn(dgB), dsB) : __uint2float_rn(dgB);
+        float e = eA;
+        if (two && eB < eA) { f = make_int2(cr, cc); e = eB; }
+        a.Fout[t * a.fstride + i] = f;
+        a.E[t * a.fstride + i] = e;
+        return;
+    }
     float e = PHASE == 0 && a.einit ? loss(f.x, f.y, __int_as_float(0x7f800000)) : a.E[t * a.fstride + i];
     {
         const int dx = (PHASE == 0 ? -1 : (PHASE == 1 ? 1 : 0)) * a.step;
@@ -1912,11 +1971,16 @@ cudaError_t launch_iter13_fast(const FieldArgs& a0, int T, int p, int loss, cuda
 }
 
 template <int P, bool TWO, int SFL = 0, int SF = 0>
-static void launch_field_mid(const FieldArgs& a, int T, int phase, cudaStream_t s)
+static void launch_field_mid(const FieldArgs& a, int T, int phase, cudaStream_t s, bool pair0 = false)
 {
     const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(TILE_X * TILE_Y);
     switch (phase) {
-    case 0: k_field_mid<P, TWO, 0, SFL, SF><<<grid, block, 0, s>>>(a); break;
+    case 0:
+        if constexpr (SF == 0 && SFL == 0) {
+            if (pair0 && a.einit) { k_field_mid<P, TWO, 0, SFL, SF, true><<<grid, block, 0, s>>>(a); break; }
+        }
+        k_field_mid<P, TWO, 0, SFL, SF><<<grid, block, 0, s>>>(a);
+        break;
     case 1: k_field_mid<P, TWO, 1, SFL, SF><<<grid, block, 0, s>>>(a); break;
     case 2: k_field_mid<P, TWO, 2, SFL, SF><<<grid, block, 0, s>>>(a); break;
     default: k_field_mid<P, TWO, 3, SFL, SF><<<grid, block, 0, s>>>(a); break;
@@ -1943,9 +2007,10 @@ cudaError_t launch_field(const FieldArgs& a0, int T, int p, int loss, int phase,
             return cudaGetLastError();
         }
         if (a.src_fmt != SF8) return cudaErrorInvalidValue;
-        if (p == 2) { if (loss) launch_field_mid<2, true>(a, T, phase, s); else launch_field_mid<2, false>(a, T, phase, s); }
-        else if (p == 3) { if (loss) launch_field_mid<3, true>(a, T, phase, s); else launch_field_mid<3, false>(a, T, phase, s); }
-        else if (p == 4) { if (loss) launch_field_mid<4, true>(a, T, phase, s); else launch_field_mid<4, false>(a, T, phase, s); }
+        const bool pr = loss == 2;  // MEAN_ALIGN: paired phase 0
+        if (p == 2) { if (loss) launch_field_mid<2, true>(a, T, phase, s, pr); else launch_field_mid<2, false>(a, T, phase, s); }
+        else if (p == 3) { if (loss) launch_field_mid<3, true>(a, T, phase, s, pr); else launch_field_mid<3, false>(a, T, phase, s); }
+        else if (p == 4) { if (loss) launch_field_mid<4, true>(a, T, phase, s, pr); else launch_field_mid<4, false>(a, T, phase, s); }
         else return cudaErrorInvalidValue;
         return cudaGetLastError();
     }

@@ -51,6 +51,10 @@ MUTATIONS = [
     ("blending table: wrong BT scale", "Alg. 4, D25", "b[e] = (prev[e] + rt[cid][e] * scale) * 0.5f;",
      "b[e] = (prev[e] + rt[cid][e]) * 0.5f;", None),
     ("Eq. 9: weights swapped", "P:266, D28", "o[e] = fmaf(xl[e], wl, xr[e] * wr);", "o[e] = fmaf(xl[e], wr, xr[e] * wl);", None),
+    ("blend tracking: link to the neighbouring source instead of target", "P:259, D44",
+     "if (tasks[b].src_id == j) { if (z == 0)", "if (tasks[b].src_id == j + (z == 0 ? -1 : 1)) { if (z == 0)", None),
+    ("blend tracking: readout from the requested index instead of the target's", "P:259, D44",
+     "int t0 = first[cfg->tracking ? i : q];", "int t0 = first[q];", None),
 ]
 
 
