@@ -653,8 +653,16 @@ __global__ void k_remap_f3(const float* __restrict__ src, const int2* __restrict
 // checks after rows 1 and 3 (profiles/r01_pde_tuning.txt).
 #define PDE_FAST_S1(P) 1
 #define PDE_FAST_S2(P) (2 * (P) + 1)
-#define PDE_I13_S2(P) ((P) == 2 ? 3 : 2 * (P) + 1)  // fused fields 1-3 with the hybrid target: second check
-                                                     // before the shared-memory rows (N=48: 397 -> 387 ms)
+// Fused fields 1-3: with the patch-sum bound in front, 91-94 % of the candidates it scores pass every partial
+// check, so one check after three rows (p = 2) is best: N=48 field123.L0 318 -> 314 ms accurate, 261 -> 259
+// balanced, 102 -> 100 fast (checks after rows 1 and 3: the round-1 optimum before the bound; 1 only, 2 only,
+// none: 315-318 / 263-267 / 102-104).
+#ifndef PDE_I13_S1
+#define PDE_I13_S1(P) ((P) == 2 ? 3 : 1)
+#endif
+#ifndef PDE_I13_S2
+#define PDE_I13_S2(P) (2 * (P) + 1)
+#endif
 #define PDE_GEN_S1(P) 1
 #define PDE_GEN_S2(P) 3
 __device__ __forceinline__ float partial_loss(float alpha, float dg, float ds, bool two)
@@ -1175,7 +1183,7 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? I13_H
         uint32_t dg = 0u;
         float dgf = 0.0f, ds = 0.0f;
         auto gsum = [&]() { return SF == 1 ? dgf : __uint2float_rn(dg); };
-        constexpr int S1 = PDE_FAST_S1(P), S2 = PDE_I13_S2(P);
+        constexpr int S1 = PDE_I13_S1(P), S2 = PDE_I13_S2(P);
         FB_CNT(cbase + 0);
 #pragma unroll
         for (int dr = 0; dr < S1; ++dr) row(sr, sc, dr, dg, dgf, ds);
