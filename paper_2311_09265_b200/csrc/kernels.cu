@@ -663,8 +663,12 @@ __global__ void k_remap_f3(const float* __restrict__ src, const int2* __restrict
 #ifndef PDE_I13_S2
 #define PDE_I13_S2(P) (2 * (P) + 1)
 #endif
+#ifndef PDE_GEN_S1
 #define PDE_GEN_S1(P) 1
+#endif
+#ifndef PDE_GEN_S2
 #define PDE_GEN_S2(P) 3
+#endif
 __device__ __forceinline__ float partial_loss(float alpha, float dg, float ds, bool two)
 {
     return two ? __fmaf_rn(alpha, dg, ds) : dg;
