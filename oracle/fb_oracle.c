@@ -309,11 +309,13 @@ static void level_field(const orc_level_ctx* L, const orc_cfg* cfg, int field, i
     for (int r = 0; r < h; ++r)
         for (int c = 0; c < w; ++c) {
             size_t i = (size_t)r * w + c;
+            /* D21: one Philox block per two steps (counter step field s >> 1); step s uses words 0, 1 when even,
+             * 2, 3 when odd */
             uint32_t u[4];
-            orc_draw(cfg->seed, (uint32_t)i, 1, (uint32_t)k, (uint32_t)it, (uint32_t)s, (uint32_t)src_id,
+            orc_draw(cfg->seed, (uint32_t)i, 1, (uint32_t)k, (uint32_t)it, (uint32_t)(s >> 1), (uint32_t)src_id,
                      (uint32_t)tag, (uint32_t)tgt_id, u);
-            int ox = (int)mulhi32(u[0], (uint32_t)(2 * R + 1)) - R;
-            int oy = (int)mulhi32(u[1], (uint32_t)(2 * R + 1)) - R;
+            int ox = (int)mulhi32(u[2 * (s & 1)], (uint32_t)(2 * R + 1)) - R;
+            int oy = (int)mulhi32(u[2 * (s & 1) + 1], (uint32_t)(2 * R + 1)) - R;
             int sr = clampi(F[2 * i] + ox, 0, h - 1), sc = clampi(F[2 * i + 1] + oy, 0, w - 1);
             float e = level_loss(L, r, c, sr, sc);
             if (e < E[i]) { F[2 * i] = sr; F[2 * i + 1] = sc; E[i] = e; } /* pointwise: in place is Jacobi */

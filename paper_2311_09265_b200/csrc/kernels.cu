@@ -260,15 +260,22 @@ struct TSums {
     float a0, a1, a2;  // target aux patch sums (FP32)
     float m;           // absolute margin of the aux sums
 };
-// Random-search offset of step s (D13, D21): uniform in [-R, R]^2, R = max(r0 >> s, 1).
-__device__ __forceinline__ int2 rs_offset(const FieldArgs& a, const DTask& T, int i, int s)
+// Random-search draws (D13, D21): one Philox block per two steps -- counter step field s >> 1; step s takes words
+// (x, y) when even, (z, w) when odd -- so a pixel's K steps cost ceil(K/2) blocks.  rs_block is called at every
+// even step (and at s when it starts a loop), rs_offset turns step s's words into a uniform offset in [-R, R]^2,
+// R = max(r0 >> s, 1).
+__device__ __forceinline__ uint4 rs_block(const FieldArgs& a, const DTask& T, int i, int s)
+{
+    return philox4x32_10(
+        make_uint4((uint32_t)i, (1u << 28) | (a.level << 22) | (a.iter << 12) | (uint32_t)(s >> 1), T.c2, T.c3),
+        a.rng.k0, a.rng.k1);
+}
+__device__ __forceinline__ int2 rs_offset(const FieldArgs& a, uint4 u, int s)
 {
     const int R = max(a.rs_r0 >> s, 1);
-    const uint4 u = philox4x32_10(
-        make_uint4((uint32_t)i, (1u << 28) | (a.level << 22) | (a.iter << 12) | (uint32_t)s, T.c2, T.c3), a.rng.k0,
-        a.rng.k1);
     const uint32_t span = 2u * (uint32_t)R + 1u;
-    return make_int2((int)__umulhi(u.x, span) - R, (int)__umulhi(u.y, span) - R);
+    const uint32_t ux = (s & 1) ? u.z : u.x, uy = (s & 1) ? u.w : u.y;
+    return make_int2((int)__umulhi(ux, span) - R, (int)__umulhi(uy, span) - R);
 }
 
 // margin of a two-pass FP32 sum of D^2 aux values whose absolute values sum to <= absum
@@ -821,14 +828,11 @@ __global__ void __launch_bounds__(TILE_X* FAST_TY, 3) k_field_fast(FieldArgs a)
                     if (e2 < e) { f = g; e = e2; }
                 }
             }
+        uint4 ru = make_uint4(0u, 0u, 0u, 0u);
         for (int s = 0; s < a.rs_k; ++s) {
-            const int R = max(a.rs_r0 >> s, 1);
-            const uint4 u = philox4x32_10(
-                make_uint4((uint32_t)i, (1u << 28) | (a.level << 22) | (a.iter << 12) | (uint32_t)s, T.c2, T.c3),
-                a.rng.k0, a.rng.k1);
-            const uint32_t span = 2u * (uint32_t)R + 1u;
-            const int ox = (int)__umulhi(u.x, span) - R, oy = (int)__umulhi(u.y, span) - R;
-            const int sr = clampi(f.x + ox, 0, h - 1), sc = clampi(f.y + oy, 0, w - 1);
+            if (!(s & 1)) ru = rs_block(a, T, i, s);
+            const int2 o = rs_offset(a, ru, s);
+            const int sr = clampi(f.x + o.x, 0, h - 1), sc = clampi(f.y + o.y, 0, w - 1);
             if (sr != f.x || sc != f.y) {
                 const float e2 = loss(sr, sc, e);
                 if (e2 < e) { f = make_int2(sr, sc); e = e2; }
@@ -1003,14 +1007,11 @@ __global__ void __launch_bounds__(32 * (IT_TY + 1), IT_MINB) k_iter_fast(FieldAr
             const int2 g = __ldg(&T.trk[z][i]);
             select(f, e, g.x, g.y);
         }
+    uint4 ru = make_uint4(0u, 0u, 0u, 0u);
     for (int s = 0; s < a.rs_k; ++s) {
-        const int R = max(a.rs_r0 >> s, 1);
-        const uint4 u = philox4x32_10(
-            make_uint4((uint32_t)i, (1u << 28) | (a.level << 22) | (a.iter << 12) | (uint32_t)s, T.c2, T.c3),
-            a.rng.k0, a.rng.k1);
-        const uint32_t span = 2u * (uint32_t)R + 1u;
-        const int ox = (int)__umulhi(u.x, span) - R, oy = (int)__umulhi(u.y, span) - R;
-        select(f, e, clampi(f.x + ox, 0, h - 1), clampi(f.y + oy, 0, w - 1));
+        if (!(s & 1)) ru = rs_block(a, T, i, s);
+        const int2 o = rs_offset(a, ru, s);
+        select(f, e, clampi(f.x + o.x, 0, h - 1), clampi(f.y + o.y, 0, w - 1));
     }
     FB_ASSERT((unsigned)f.x < (unsigned)h && (unsigned)f.y < (unsigned)w);
     a.Fout[t * a.fstride + i] = f;
@@ -1297,8 +1298,10 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? I13_H
     const uint4* SUMS = use_csb ? reinterpret_cast<const uint4*>(T.src + a.sum_off) : nullptr;
     constexpr float ssc = SF == 1 ? 0.25f : 1.0f;  // source sums: n = v (SF8) or n = 4 v (SF10)
     cbase = 8;
+    uint4 ru = make_uint4(0u, 0u, 0u, 0u);
     for (int s = 0; s < a.rs_k; ++s) {
-        const int2 o = rs_offset(a, T, i, s);
+        if (!(s & 1)) ru = rs_block(a, T, i, s);
+        const int2 o = rs_offset(a, ru, s);
         const int sr = clampi(f.x + o.x, 0, h - 1), sc = clampi(f.y + o.y, 0, w - 1);
         if (CSB && use_csb && (sr != f.x || sc != f.y) &&
             (SFL == 1 ? csb_reject_f<D, TWO>(__ldg(SUMS + 2 * (sr * w + sc)), __ldg(SUMS + 2 * (sr * w + sc) + 1), ts,
@@ -1538,8 +1541,10 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y, PR ? MIDP_MINB : (P == 2 ? (SF
             }
         const uint4* SUMS = use_csb ? reinterpret_cast<const uint4*>(T.src + a.sum_off) : nullptr;
         constexpr float ssc = SF == 1 ? 0.25f : 1.0f;  // source sums: n = v (SF8) or n = 4 v (SF10)
+        uint4 ru = make_uint4(0u, 0u, 0u, 0u);
         for (int s = 0; s < a.rs_k; ++s) {
-            const int2 o = rs_offset(a, T, i, s);
+            if (!(s & 1)) ru = rs_block(a, T, i, s);
+            const int2 o = rs_offset(a, ru, s);
             const int sr = clampi(f.x + o.x, 0, h - 1), sc = clampi(f.y + o.y, 0, w - 1);
             if (CSB && use_csb && (sr != f.x || sc != f.y) &&
                 csb_reject<D, TWO>(__ldg(SUMS + sr * w + sc), ts, ssc, a.alpha, e))
@@ -1734,8 +1739,10 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
             }
         const uint4* SUMS = use_csb ? reinterpret_cast<const uint4*>(T.src + a.sum_off) : nullptr;
         const float scale = __uint_as_float((uint32_t)(127 - 2 * a.L.k) << 23);  // 4^-k: unit of the source sums
+        uint4 ru = make_uint4(0u, 0u, 0u, 0u);
         for (int s = 0; s < a.rs_k; ++s) {
-            const int2 o = rs_offset(a, T, i, s);
+            if (!(s & 1)) ru = rs_block(a, T, i, s);
+            const int2 o = rs_offset(a, ru, s);
             const int sr = clampi(f.x + o.x, 0, h - 1), sc = clampi(f.y + o.y, 0, w - 1);
             if (sr != f.x || sc != f.y) {
                 if (CSB && use_csb && csb_reject<D, TWO>(__ldg(SUMS + sr * w + sc), ts, scale, a.alpha, e)) continue;

@@ -51,6 +51,8 @@ MUTATIONS = [
     ("blending table: wrong BT scale", "Alg. 4, D25", "b[e] = (prev[e] + rt[cid][e] * scale) * 0.5f;",
      "b[e] = (prev[e] + rt[cid][e]) * 0.5f;", None),
     ("Eq. 9: weights swapped", "P:266, D28", "o[e] = fmaf(xl[e], wl, xr[e] * wr);", "o[e] = fmaf(xl[e], wr, xr[e] * wl);", None),
+    ("random search: odd steps reuse the even step's words", "D21",
+     "int ox = (int)mulhi32(u[2 * (s & 1)], (uint32_t)(2 * R + 1)) - R;", "int ox = (int)mulhi32(u[0], (uint32_t)(2 * R + 1)) - R;", None),
     ("blend tracking: link to the neighbouring source instead of target", "P:259, D44",
      "if (tasks[b].src_id == j) { if (z == 0)", "if (tasks[b].src_id == j + (z == 0 ? -1 : 1)) { if (z == 0)", None),
     ("blend tracking: readout from the requested index instead of the target's", "P:259, D44",
