@@ -96,3 +96,28 @@ while R >= 1:
         tot2[k] += v
     R >>= 1
 print("compact sums: " + "  ".join(f"{k} {v / tot2['cands']:.3f}" for k, v in tot2.items() if k != "cands"))
+
+# partial rows + Cauchy-Schwarz on the remaining rows, for candidates that survive the patch-mean bound
+tot3 = dict(surv=0, r0=0, r1=0, r2=0, pde0=0, pde2=0)
+R = H
+rng = np.random.default_rng(2)
+while R >= 1:
+    off = rng.integers(-R, R + 1, size=(H, H, 2))
+    cr = np.clip(F[..., 0] + off[..., 0], 0, H - 1)
+    cc = np.clip(F[..., 1] + off[..., 1], 0, H - 1)
+    sg, ss = patches(Gs, cr, cc), patches(Ss, cr, cc)
+    dg, ds = alpha * (sg - tg) ** 2, (ss - ta) ** 2
+    mean = (alpha * ((sg.sum((-3, -2)) - tg.sum((-3, -2))) ** 2).sum(-1)
+            + ((ss.sum((-3, -2)) - ta.sum((-3, -2))) ** 2).sum(-1)) / n
+    surv = mean < E
+    tot3["surv"] += surv.sum()
+    for r_, key in ((0, "r0"), (1, "r1"), (2, "r2")):
+        part = dg[..., : r_ + 1, :, :].sum((-3, -2, -1)) + ds[..., : r_ + 1, :, :].sum((-3, -2, -1))
+        m = (D - r_ - 1) * D
+        rest = (alpha * ((sg[..., r_ + 1:, :, :].sum((-3, -2)) - tg[..., r_ + 1:, :, :].sum((-3, -2))) ** 2).sum(-1)
+                + ((ss[..., r_ + 1:, :, :].sum((-3, -2)) - ta[..., r_ + 1:, :, :].sum((-3, -2))) ** 2).sum(-1)) / m
+        tot3[key] += (surv & (part + rest >= E)).sum()
+        if r_ in (0, 2):
+            tot3["pde" + str(r_)] += (surv & (part >= E)).sum()
+    R >>= 1
+print("among mean-bound survivors: " + "  ".join(f"{k} {v / tot3['surv']:.3f}" for k, v in tot3.items() if k != "surv"))
