@@ -114,10 +114,12 @@ uint64_t fb_launch_count(fb_ctx ctx);
  *   FB_OPT_PHASE0_MID   1  0 = level-0 E init + field 0 with the register-target kernel
  *   FB_OPT_TGT_REG_ROWS 3  target patch rows held in registers by the fused level-0 kernel (0 = all, 1, 2,
  *                          3 = none: every row from the shared tile)
- *   FB_OPT_L1_FAST      0  1 = level 1 (u8 sources, p = 2) through 16-byte TF10 targets and the fused
- *                          fields-1-3 kernel instead of the general kernel (bit-identical, measured slower)
+ *   FB_OPT_L1_FAST      0  level 1 (u8 sources, p = 2) through 16-byte TF10 targets and the level-0 kernels
+ *                          instead of the general kernel: 1 = fields 1-3 fused, 2 = per-field shared-tile
+ *                          launches (bit-identical, both measured slower)
  *   FB_OPT_SUM_BOUND    1  0 = no patch-sum lower bound in the random search (every candidate gathers its
- *                          first patch row; the bound only skips candidates that provably lose)
+ *                          patch rows; the bound only skips candidates that provably lose, DESIGN.md §6;
+ *                          used at every level with exact packed sources and for float-style table cells)
  * Errors: FB_ERR_INVALID_ARG (unknown option or value). */
 typedef enum { FB_OPT_FUSED_ITER = 0, FB_OPT_FUSE13 = 1, FB_OPT_PHASE0_MID = 2, FB_OPT_TGT_REG_ROWS = 3,
                FB_OPT_L1_FAST = 4, FB_OPT_SUM_BOUND = 5 } fb_option;
