@@ -137,9 +137,10 @@ __global__ void k_pack_src(const PackSrc* __restrict__ jobs, int fmt, PLvl L)
             if (in) {
                 const uint8_t* g = J.g8 + 3LL * (r * L.w + c);
                 v.x = g[0] | (g[1] << 8) | (g[2] << 16);
+                v.y = 1u << 24;  // byte 3: the in-image count the slot remaps accumulate (0 in the border)
                 if (J.s8) {
                     const uint8_t* s = J.s8 + 3LL * (r * L.w + c);
-                    v.y = s[0] | (s[1] << 8) | (s[2] << 16);
+                    v.y |= s[0] | (s[1] << 8) | (s[2] << 16);
                 }
             }
             reinterpret_cast<uint2*>(J.out)[(size_t)cpy * n + i] = v;
@@ -481,15 +482,17 @@ __device__ __forceinline__ float3 remap_px_slot(const char* __restrict__ slot, i
             const int tc = c + dc;
             const int2 f = __ldg(&F[trc * w + clampi(tc, 0, w - 1)]);
             const int sr = f.x - dr, sc = f.y - dc;
-            const bool v = rin && (unsigned)tc < (unsigned)w && (unsigned)sr < (unsigned)h && (unsigned)sc < (unsigned)w;
             const int idx = (sr + kBorder) * pitch + sc + kBorder;
             FB_ASSERT(sr >= -kBorder && sc >= -kBorder && sr < h + kBorder && sc < w + kBorder);
-            if (SFMT == SF8) {
+            if (SFMT == SF8) {  // the source-side validity is the texel's count byte (1 inside, 0 in the border)
                 uint32_t sv = __ldg(reinterpret_cast<const uint32_t*>(slot) + 2 * idx + 1);
-                sv = v ? sv : 0u;
+                sv = rin && (unsigned)tc < (unsigned)w ? sv : 0u;
                 a0 += __byte_perm(sv, 0u, 0x4240u);  // r | b << 16
-                a1 += __byte_perm(sv, 0u, 0x4441u);  // g
-            } else if (SFMT == SF10) {
+                a1 += __byte_perm(sv, 0u, 0x4341u);  // g | count << 16
+                continue;
+            }
+            const bool v = rin && (unsigned)tc < (unsigned)w && (unsigned)sr < (unsigned)h && (unsigned)sc < (unsigned)w;
+            if (SFMT == SF10) {
                 uint32_t sv = __ldg(reinterpret_cast<const uint32_t*>(slot) + 2 * idx + 1);
                 sv = v ? sv : 0u;
                 a0 += sv & 0x3FFu;
@@ -507,7 +510,8 @@ __device__ __forceinline__ float3 remap_px_slot(const char* __restrict__ slot, i
     }
     float x, y, z;
     if (SFMT == SF8) {
-        x = (float)(a0 & 0xffffu); y = (float)a1; z = (float)(a0 >> 16);
+        x = (float)(a0 & 0xffffu); y = (float)(a1 & 0xffffu); z = (float)(a0 >> 16);
+        n = (int)(a1 >> 16);
     } else {
         const float sc = __int_as_float((127 - 2 * k) << 23);  // 4^-k, exact
         x = __fmul_rn((float)a0, sc); y = __fmul_rn((float)a1, sc); z = __fmul_rn((float)a2, sc);

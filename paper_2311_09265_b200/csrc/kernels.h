@@ -8,7 +8,7 @@
 //  * float4 pyramids [slot][level-major texels] (RGB + 0) for remap inputs and packing;
 //  * packed PatchMatch operands with a zero border of kBorder texels on every side (so patch taps never
 //    need bounds checks: out-of-image taps read the border's zeros, reading D9) and an even pitch:
-//      source  SF8  (level 0, uint8 style): uint2 {G rgb u8, S rgb u8}                        8 B
+//      source  SF8  (level 0, uint8 style): uint2 {G rgb u8, S rgb u8 | 1 << 24 inside the image}  8 B
 //              SF10 (level 1, uint8 style): uint2 {G, S} of 10-bit fields n = 4 v (r | g << 10 | b << 20),
 //                   exact because level-1 values are multiples of 1/4 (D6); two copies like SF8        8 B
 //              SF16 (levels 2..4, uint8 style): uint4 of u16 n = v * 4^k {G.r,G.g | G.b,0 |
