@@ -323,6 +323,20 @@ def roofline(prof, wl, cfg, steps):
                                     "source": tr[dom].get("source")}
         except (OSError, ValueError):
             pass
+    # the other profiled classes: the same hardware view (ncu L1 wavefronts per work unit x 128 B x this run's
+    # units / this run's time), so every captured kernel's utilisation of its bound resource is in the line
+    if os.path.exists(traffic_file):
+        try:
+            tr = json.load(open(traffic_file))
+            classes = {}
+            for k, v in tr.items():
+                if k in prof and "l1_wavefronts_per_work" in v and prof[k]["ms"] > 0 and prof[k]["work"] > 0:
+                    gbs = v["l1_wavefronts_per_work"] * 128.0 * prof[k]["work"] / (prof[k]["ms"] / 1e3) / 1e9
+                    classes[k] = {"hw_l1_gbs": gbs, "hw_l1_frac": gbs / peak, "share_of_kernel_time": prof[k]["ms"] / total_ms,
+                                  "ncu_util": v.get("ncu_util"), "source": v.get("source")}
+            roof["classes"] = classes
+        except (OSError, ValueError):
+            pass
     fp32_peak = SMS * FP32_LANES_PER_SM * 2 * SM_MAX_MHZ * 1e6 / 1e12
     alu = {"kernel": f"pm_{dom}", "bound": "alu", "achieved": d["work"] * fpe / sec / 1e12, "peak": fp32_peak,
            "unit": "TFLOP/s", "frac": d["work"] * fpe / sec / 1e12 / fp32_peak, "flops_per_eval": fpe,
