@@ -1028,7 +1028,10 @@ __global__ void __launch_bounds__(32 * (IT_TY + 1), IT_MINB) k_iter_fast(FieldAr
 // and field 3 (right neighbour's field-2 result by shuffle) and the random search.  Lanes 0 and 31 of
 // each warp are halo columns that recompute the fields their interior neighbours read, so the interior
 // pixels see exactly the Jacobi inputs of the per-field launches.  No shared memory, no barrier.
-static constexpr int I13_TY = 4;
+#ifndef FB_I13_TY
+#define FB_I13_TY 4
+#endif
+static constexpr int I13_TY = FB_I13_TY;
 
 // NR < D (hybrid target): only the first NR rows of each lane's target patch live in registers -- row 0 is
 // read by every candidate, rows >= 1 only by candidates that survive row 0 -- and the rest is read from a
