@@ -558,3 +558,18 @@ def test_blend_tracking_unsupported_forms(fb, ctx):
     with pytest.raises(fb.FBError) as e:
         ctx.fb_blend_window_range(cfg, fb.DIRECT, 6, 0, dev(g), dev(s), 2, 0, 3)
     assert e.value.status == 6
+
+
+@pytest.mark.parametrize("mode", ["accurate", "fast"])
+def test_max_size_identical_frames_identity(fb, mode):
+    """Largest frames in the tests (UHD 2160x3840, 7 pyramid levels): with identity init on identical frames every
+    NNF stays the identity (E = 0 is never beaten, D16), so the blend returns the style exactly (P6 at full scale;
+    exercises the 64-bit offsets, slot pitches and patch-sum planes at the largest sizes)."""
+    g1 = textured_frame(2160, 3840, seed=61)
+    g = np.stack([g1, g1, g1])
+    s = np.stack([g1[..., ::-1], g1[..., ::-1], g1[..., ::-1]]).copy()
+    loss = fb.MEAN_ALIGN if mode == "accurate" else fb.GUIDE_STYLE
+    cfg = fb.MatchCfg(iters_per_level=1, loss=loss, init=fb.INIT_IDENTITY)
+    out, st = fb.Context(0).fb_blend_window(cfg, fb.TREE if mode == "fast" else fb.DIRECT, dev(g), dev(s), 1)
+    assert st["nnf_pairs"] > 0
+    assert torch.equal(out, dev(s).float())
