@@ -43,6 +43,7 @@ struct fb_ctx_s {
                            // 285 -> 268 balanced, 112 -> 102 fast
     bool sum_bound = true;  // FB_OPT_SUM_BOUND: random-search candidates rejected by the patch-sum bound (level 0,
                             // and level 1 with FB_OPT_L1_FAST) before any patch row is gathered
+    bool p3_fused = true;  // FB_OPT_P3_FUSED: level-0 fields 1-3 + random search in one launch at p = 3 as well
     int l1_fast = 0;  // FB_OPT_L1_FAST: level 1 of u8 sources (SF10) through 16-byte TF10 targets and the
                       // level-0 kernels -- 1: E init + field 0 by the shared-tile kernel, fields 1-3 + random
                       // search fused; 2: every field by the shared-tile kernel.  Bit-identical; 1 measured slower
@@ -528,7 +529,9 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
             for (int j = J - 1; j >= 0; --j) {
                 a.step = 1 << j;
                 const bool last = j == 0;
-                if (last && (fast || (l1 && ex.ctx->l1_fast == 1)) && ex.ctx->fuse13) {  // field 0, then fields 1-3 + random search in one launch
+                // p = 3 at level 0 (u8 sources): fields 1-3 + random search fused as well (FB_OPT_P3_FUSED)
+                const bool p3f = ex.ctx->p3_fused && tf16 && g.p == 3 && !pairwise && slots.fmt0 == fbk::SF8;
+                if (last && (fast || p3f || (l1 && ex.ctx->l1_fast == 1)) && ex.ctx->fuse13) {  // field 0, then fields 1-3 + random search in one launch
                     a.Fin = F[cur]; a.Fout = F[cur ^ 1];
                     const int kind0 = (l1 || (ex.ctx->phase0_mid && !pairwise && g.p == 2 &&
                                               (a.src_fmt == fbk::SF8 || a.src_fmt == fbk::SF8F))) ? 2 : kind;
@@ -1201,6 +1204,7 @@ fb_status fb_set_option(fb_ctx ctx, int option, int value)
         ctx->l1_fast = value;
         break;
     case FB_OPT_SUM_BOUND: ctx->sum_bound = value != 0; break;
+    case FB_OPT_P3_FUSED: ctx->p3_fused = value != 0; break;
     case FB_OPT_TGT_REG_ROWS:
         if (value < 0 || value > 3) { ctx->err = "tgt_reg_rows must be 0 (all), 1, 2 or 3 (none)"; return FB_ERR_INVALID_ARG; }
         ctx->tgt_reg_rows = value;

@@ -1049,7 +1049,10 @@ template <int P, bool TWO, bool PW = false, int SFL = 0, int NR = 2 * P + 1, int
 #ifndef I13_HY0_MINB
 #define I13_HY0_MINB 8  // no target row in registers (every row from the shared tile)
 #endif
-__global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? I13_HY0_MINB : (SFL ? I13_SFL_MINB : (NR == 1 ? I13_HY1_MINB : I13_HY_MINB))) : 3) k_iter13_fast(FieldArgs a)
+#ifndef I13_P3_MINB
+#define I13_P3_MINB 10  // p = 3 (7-texel rows): config-5 shard field123.L0 6 / 8 / 10 CTAs: 339 / 330 / 324 ms (separate launches 333)
+#endif
+__global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? (P == 3 ? I13_P3_MINB : I13_HY0_MINB) : (SFL ? I13_SFL_MINB : (NR == 1 ? I13_HY1_MINB : I13_HY_MINB))) : 3) k_iter13_fast(FieldArgs a)
 {
     constexpr int D = 2 * P + 1;
     constexpr bool HY = NR < D;
@@ -1972,6 +1975,11 @@ cudaError_t launch_iter13_fast(const FieldArgs& a0, int T, int p, int loss, cuda
         else if (p == 2 && hy == 2) k_iter13_fast<2, true, false, 1, 2><<<grid, block, 0, s>>>(a);
         else if (p == 2) k_iter13_fast<2, true, false, 1><<<grid, block, 0, s>>>(a);
         else return cudaErrorInvalidValue;
+        return cudaGetLastError();
+    }
+    if (p == 3 && loss != 3) {  // level 0 at p = 3 (config 5): every target row from the shared tile
+        if (loss) k_iter13_fast<3, true, false, 0, 0><<<grid, block, 0, s>>>(a);
+        else k_iter13_fast<3, false, false, 0, 0><<<grid, block, 0, s>>>(a);
         return cudaGetLastError();
     }
     if (p == 2 && loss != 3 && hy >= 1) {

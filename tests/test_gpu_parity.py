@@ -573,3 +573,17 @@ def test_max_size_identical_frames_identity(fb, mode):
     out, st = fb.Context(0).fb_blend_window(cfg, fb.TREE if mode == "fast" else fb.DIRECT, dev(g), dev(s), 1)
     assert st["nnf_pairs"] > 0
     assert torch.equal(out, dev(s).float())
+
+
+@pytest.mark.parametrize("mode,p3f", [("balanced", 1), ("accurate", 1), ("balanced", 0)])
+def test_p3_fused_fields_match_oracle(fb, mode, p3f):
+    """p = 3 (config 5's patch 7) at level 0: fields 1-3 and the random search in one launch (FB_OPT_P3_FUSED) or as
+    separate launches, both equal to the oracle bit for bit on a ragged size."""
+    c = fb.Context(0)
+    c.set_option(fb.fb.OPT_P3_FUSED, p3f)
+    g, s = moving_texture(5, 70, 101, seed=63)
+    cfg = fb.MatchCfg(patch_radius=3, iters_per_level=2, loss=fb.MEAN_ALIGN if mode == "accurate" else fb.GUIDE_STYLE)
+    out, st = c.fb_blend_window(cfg, fb.DIRECT, dev(g), dev(s), 2)
+    ref, pairs, evals = O.blend_direct(ocfg(cfg), g, s, 2)
+    assert st["candidate_evals"] == evals
+    assert_frames(out, ref)
