@@ -587,3 +587,18 @@ def test_p3_fused_fields_match_oracle(fb, mode, p3f):
     ref, pairs, evals = O.blend_direct(ocfg(cfg), g, s, 2)
     assert st["candidate_evals"] == evals
     assert_frames(out, ref)
+
+
+@pytest.mark.parametrize("H,W,loss", [(5, 5, 2), (5, 203, 1), (203, 5, 2), (6, 33, 1), (31, 7, 0)])
+def test_extreme_shapes_match_oracle(fb, ctx, H, W, loss):
+    """Smallest and most elongated frames for p = 2 (one pyramid level, a single ragged tile in one dimension):
+    NNF, E and remap equal the oracle bit for bit."""
+    cfg, (sg, tg, ss, ts, keys), frames, tasks = _nnf_case(fb, loss, H, W, seed=67, n=3)
+    group = [0] * len(keys) if loss == fb.MEAN_ALIGN else None
+    F, E, X, st = ctx.fb_nnf_estimate(cfg, dev(sg), dev(tg), None if loss == 0 else dev(ss),
+                                      dev(ts) if loss == 2 else None, group=group, pair_keys=keys)
+    Fr, Er, Xr, ev = O.nnf(ocfg(cfg), frames, tasks, want_x=loss != 0)
+    assert st["candidate_evals"] == ev
+    assert_nnf(F, E, Fr, Er)
+    if loss != 0:
+        assert_frames(X, Xr)
