@@ -59,6 +59,49 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
 
+// ---- bulk-copy (TMA engine) staging of target tiles: one thread issues one cp.async.bulk per tile row (a
+// contiguous run of 16-byte texels in the padded target plane), completing on an mbarrier the CTA waits on.
+#ifndef FB_TILE_TMA
+#define FB_TILE_TMA 1
+#endif
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// Stage rows [pr0, pr0 + NY) x columns [pc0, pc0 + NX) of a padded uint4 plane (row pitch `pitch` texels, `rows`
+// rows) into tile[NY][NX]: rows / columns beyond the plane are left unwritten -- no valid pixel's patch reaches them
+// (the plane's zero border is wider than every patch radius).  Call from all threads; returns with the tile ready.
+template <int NY, int NX>
+__device__ __forceinline__ void stage_tile_tma(uint4 (&tile)[NY][NX], const uint4* plane, int pitch, int rows, int pr0,
+                                               int pc0, uint64_t* bar)
+{
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        const int ny = min(NY, rows - pr0), nx = min(NX, pitch - pc0);
+        mbar_expect_tx(bar, (uint32_t)(ny * nx * 16));
+        for (int y = 0; y < ny; ++y) bulk_g2s(&tile[y][0], plane + (size_t)(pr0 + y) * pitch + pc0, (uint32_t)nx * 16u, bar);
+    }
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    mbar_wait(bar, 0);
+}
+
 // u8 channel `ch` of a packed rgb word as an exact float: 0x4B0000xx is 2^23 + xx.
 __device__ __forceinline__ float u8f(uint32_t word, int ch)
 {
@@ -1075,12 +1118,17 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? (P ==
     __shared__ uint4 tT[TTY][TTX];
     if (HY) {  // the CTA's target tile (rows r0-P.., cols c0-P..), zero outside the padded plane
         const int pr0 = ty * I13_TY - P + B, pc0 = tx * IT_TX - 1 - P + B;
+#if FB_TILE_TMA
+        __shared__ uint64_t tbar;
+        stage_tile_tma<TTY, TTX>(tT, Tt, pitch, a.L.rows, pr0, pc0, &tbar);
+#else
         for (int k = threadIdx.x; k < TTY * TTX; k += 32 * I13_TY) {
             const int yy = k / TTX, xx = k - yy * TTX;
             const int pr = pr0 + yy, pc = pc0 + xx;
             tT[yy][xx] = (pr < a.L.rows && pc < pitch) ? __ldg(&Tt[pr * pitch + pc]) : make_uint4(0u, 0u, 0u, 0u);
         }
         __syncthreads();
+#endif
     }
     constexpr bool CSB = (SFL == 0 || SFL == 1) && !PW && HY;  // patch-sum bound of the random search (csb_reject)
     const bool use_csb = CSB && a.sum_off >= 0;
@@ -1355,13 +1403,18 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y, PR ? MIDP_MINB : (P == 2 ? (SF
     const DTask T = a.tasks[t];
     {
         const uint4* Tt = reinterpret_cast<const uint4*>(T.tgt);
+#if FB_TILE_TMA
+        __shared__ uint64_t tbar;
+        stage_tile_tma<SY, SX>(tT, Tt, pitch, a.L.rows, ty * TILE_Y - P + B, tx * TILE_X - P + B, &tbar);
+#else
         for (int k = threadIdx.x; k < SX * SY; k += TILE_X * TILE_Y) {
             const int yy = k / SX, xx = k - yy * SX;
             const int pr = ty * TILE_Y + yy - P + B, pc = tx * TILE_X + xx - P + B;
             tT[yy][xx] = (pr < a.L.rows && pc < pitch) ? __ldg(&Tt[pr * pitch + pc]) : make_uint4(0u, 0u, 0u, 0u);
         }
+        __syncthreads();
+#endif
     }
-    __syncthreads();
     const int lx = threadIdx.x & (TILE_X - 1), ly = threadIdx.x / TILE_X;
     const int c = tx * TILE_X + lx, r = ty * TILE_Y + ly;
     // patch-sum bound of the random search (csb_reject): target sums while the warp is converged
