@@ -1704,13 +1704,24 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
                 }
             }
     }
-    auto row = [&](int sr, int sc, int dr, float& dg, float& ds) {
-        const int base = (sr + dr - P + B) * pitch + (sc - P + B);
-        FB_ASSERT((unsigned)sr < (unsigned)h && (unsigned)sc < (unsigned)w && FB_ROW_OK(base, a.L, D));
-        float rg = 0.0f, rs = 0.0f;
-        // SF10: the row's texel pairs from the copy in which it starts 16-byte aligned (as SF8)
-        constexpr int NCH = (D + 2) / 2;
-        uint32_t wd[SFMT == SF10 ? 4 * NCH : 1];
+    // source texel dc of a patch row starting at padded texel `base` (SF10: from the row's preloaded words wd)
+    auto texel = [&](const uint32_t* wd, int base, int dc, float4& s0, float4& s1) {
+        if (SFMT == SF10) {  // guide biased (see GB), style exact
+            const uint32_t gw = wd[SFMT == SF10 ? 2 * dc : 0], sw = wd[SFMT == SF10 ? 2 * dc + 1 : 0];
+            s0 = make_float4(b10_0(gw), b10_1(gw), b10_2(gw), TWO ? f10_0(sw) : 0.0f);
+            s1 = TWO ? make_float4(f10_1(sw), f10_2(sw), 0.0f, 0.0f) : s0;
+        } else if (SFMT == SF16) {
+            const uint4 v = __ldg(&S16[base + dc]);
+            s0 = make_float4(__uint_as_float(__byte_perm(v.x, ex, 0x7410u)), __uint_as_float(__byte_perm(v.x, ex, 0x7432u)),
+                             __uint_as_float(__byte_perm(v.y, ex, 0x7410u)), TWO ? u16f(v.z, 0x7410u, ex) : 0.0f);
+            s1 = TWO ? make_float4(u16f(v.z, 0x7432u, ex), u16f(v.w, 0x7410u, ex), 0.0f, 0.0f) : s0;
+        } else {
+            s0 = __ldg(&S[2 * (base + dc)]);
+            s1 = TWO ? __ldg(&S[2 * (base + dc) + 1]) : s0;
+        }
+    };
+    constexpr int NCH = (D + 2) / 2;
+    auto preload = [&](int base, uint32_t (&wd)[SFMT == SF10 ? 4 * NCH : 1]) {  // SF10: the row's aligned copy
         if (SFMT == SF10) {
             const uint4* cp = reinterpret_cast<const uint4*>(
                 reinterpret_cast<const uint2*>(T.src + a.src_off) + (size_t)(base & 1) * (a.L.rows * pitch) + (base & ~1));
@@ -1721,22 +1732,18 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
                 wd[SFMT == SF10 ? 4 * k + 2 : 0] = v.z; wd[SFMT == SF10 ? 4 * k + 3 : 0] = v.w;
             }
         }
+    };
+    auto row = [&](int sr, int sc, int dr, float& dg, float& ds) {
+        const int base = (sr + dr - P + B) * pitch + (sc - P + B);
+        FB_ASSERT((unsigned)sr < (unsigned)h && (unsigned)sc < (unsigned)w && FB_ROW_OK(base, a.L, D));
+        float rg = 0.0f, rs = 0.0f;
+        // SF10: the row's texel pairs from the copy in which it starts 16-byte aligned (as SF8)
+        uint32_t wd[SFMT == SF10 ? 4 * NCH : 1];
+        preload(base, wd);
 #pragma unroll
         for (int dc = 0; dc < D; ++dc) {
             float4 s0, s1;
-            if (SFMT == SF10) {  // guide biased (see GB), style exact
-                const uint32_t gw = wd[SFMT == SF10 ? 2 * dc : 0], sw = wd[SFMT == SF10 ? 2 * dc + 1 : 0];
-                s0 = make_float4(b10_0(gw), b10_1(gw), b10_2(gw), TWO ? f10_0(sw) : 0.0f);
-                s1 = TWO ? make_float4(f10_1(sw), f10_2(sw), 0.0f, 0.0f) : s0;
-            } else if (SFMT == SF16) {
-                const uint4 v = __ldg(&S16[base + dc]);
-                s0 = make_float4(__uint_as_float(__byte_perm(v.x, ex, 0x7410u)), __uint_as_float(__byte_perm(v.x, ex, 0x7432u)),
-                                 __uint_as_float(__byte_perm(v.y, ex, 0x7410u)), TWO ? u16f(v.z, 0x7410u, ex) : 0.0f);
-                s1 = TWO ? make_float4(u16f(v.z, 0x7432u, ex), u16f(v.w, 0x7410u, ex), 0.0f, 0.0f) : s0;
-            } else {
-                s0 = __ldg(&S[2 * (base + dc)]);
-                s1 = TWO ? __ldg(&S[2 * (base + dc) + 1]) : s0;
-            }
+            texel(wd, base, dc, s0, s1);
             const float4 q0 = t0[ly + dr][lx + dc];
             float dl;
             dl = __fsub_rn(q0.x, s0.x); rg = __fmaf_rn(dl, dl, rg);
@@ -1778,6 +1785,55 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y) k_field_gen(FieldArgs a)
     const int2* Fi = a.Fin + t * a.fstride;
     const int i = r * w + c;
     int2 f = Fi[i];
+    // Accurate mode (a.pair0): E <- L(F) and the field-0 candidate scored together row by row, each target texel
+    // read from the tile once for both (as k_field_mid's PR form; exact: the candidate is scored in full and
+    // selected strictly).
+    if (PHASE == 0 && TWO && !PW && a.einit && a.pair0) {
+        const int dx = -a.step;  // field 0: d = (-1,0), jump-flood step (D41)
+        const int2 fn = Fi[clampi(r + dx, 0, h - 1) * w + c];
+        const int cr = clampi(fn.x - dx, 0, h - 1), cc = clampi(fn.y, 0, w - 1);  // D11, D10
+        const bool two = cr != f.x || cc != f.y;
+        float dgA = 0.0f, dsA = 0.0f, dgB = 0.0f, dsB = 0.0f;
+#pragma unroll
+        for (int dr = 0; dr < D; ++dr) {
+            const int ba = (f.x + dr - P + B) * pitch + (f.y - P + B), bb = (cr + dr - P + B) * pitch + (cc - P + B);
+            uint32_t wa[SFMT == SF10 ? 4 * NCH : 1], wb[SFMT == SF10 ? 4 * NCH : 1];
+            preload(ba, wa);
+            if (two) preload(bb, wb);
+            float rga = 0.0f, rsa = 0.0f, rgb = 0.0f, rsb = 0.0f;
+#pragma unroll
+            for (int dc = 0; dc < D; ++dc) {
+                const float4 q0 = t0[ly + dr][lx + dc];
+                const float2 q1 = t1[ly + dr][lx + dc];
+                float4 s0, s1;
+                texel(wa, ba, dc, s0, s1);
+                float dl;
+                dl = __fsub_rn(q0.x, s0.x); rga = __fmaf_rn(dl, dl, rga);
+                dl = __fsub_rn(q0.y, s0.y); rga = __fmaf_rn(dl, dl, rga);
+                dl = __fsub_rn(q0.z, s0.z); rga = __fmaf_rn(dl, dl, rga);
+                dl = __fsub_rn(q0.w, s0.w); rsa = __fmaf_rn(dl, dl, rsa);
+                dl = __fsub_rn(q1.x, s1.x); rsa = __fmaf_rn(dl, dl, rsa);
+                dl = __fsub_rn(q1.y, s1.y); rsa = __fmaf_rn(dl, dl, rsa);
+                if (two) {
+                    texel(wb, bb, dc, s0, s1);
+                    dl = __fsub_rn(q0.x, s0.x); rgb = __fmaf_rn(dl, dl, rgb);
+                    dl = __fsub_rn(q0.y, s0.y); rgb = __fmaf_rn(dl, dl, rgb);
+                    dl = __fsub_rn(q0.z, s0.z); rgb = __fmaf_rn(dl, dl, rgb);
+                    dl = __fsub_rn(q0.w, s0.w); rsb = __fmaf_rn(dl, dl, rsb);
+                    dl = __fsub_rn(q1.x, s1.x); rsb = __fmaf_rn(dl, dl, rsb);
+                    dl = __fsub_rn(q1.y, s1.y); rsb = __fmaf_rn(dl, dl, rsb);
+                }
+            }
+            dgA = __fadd_rn(dgA, rga); dsA = __fadd_rn(dsA, rsa);
+            dgB = __fadd_rn(dgB, rgb); dsB = __fadd_rn(dsB, rsb);
+        }
+        float e = __fmaf_rn(a.alpha, dgA, dsA);
+        const float eB = __fmaf_rn(a.alpha, dgB, dsB);
+        if (two && eB < e) { f = make_int2(cr, cc); e = eB; }
+        a.Fout[t * a.fstride + i] = f;
+        a.E[t * a.fstride + i] = e;
+        return;
+    }
     float e = PHASE == 0 && a.einit ? loss(f.x, f.y, __int_as_float(0x7f800000)) : a.E[t * a.fstride + i];
     {
         const int dx = (PHASE == 0 ? -1 : (PHASE == 1 ? 1 : 0)) * a.step;  // jump-flood step (D41)
@@ -2081,6 +2137,7 @@ cudaError_t launch_field(const FieldArgs& a0, int T, int p, int loss, int phase,
     a.tiles_x = (a.L.w + TILE_X - 1) / TILE_X;
     a.tiles_per_task = a.tiles_x * ((a.L.h + (fast ? FAST_TY : TILE_Y) - 1) / (fast ? FAST_TY : TILE_Y));
     const bool pw = loss == 3;
+    a.pair0 = loss == 2 && kind == 0 && phase == 0;  // accurate mode: paired E init + field 0 in the general kernel
     if (kind == 2) {  // level 0: SF8 (or, p = 2, SF8F) source, TF16 target tile; level 1: SF10 + TF10 (p = 2)
         if (pw) return cudaErrorInvalidValue;
         if (a.src_fmt == SF10) {

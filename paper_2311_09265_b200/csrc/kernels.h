@@ -99,6 +99,7 @@ struct FieldArgs {
     int do_rs;             // phase 3 runs the random search (last field of the iteration)
     float* Eout;           // fused fields 1-3: final E (nullable); E itself is read-only there
     int tgt_reg_rows;      // fused fields 1-3 (p = 2): target patch rows held in registers (0 = all)
+    int pair0;             // general kernel phase 0 with E init: score E and the field-0 candidate together
     long long sum_off;     // byte offset of this level's patch-sum plane inside each source slot, or -1 (none):
                            // the random search then rejects candidates by the patch-sum bound
 };
