@@ -1,12 +1,13 @@
 // kernels.cu — sm_100a kernels of the FastBlend hot path (arXiv 2311.09265).
 //
 // No tensor cores: the method has no dense contraction (patch distances are gathers of data-dependent
-// patches).  The bound resource is the L1/LSU gather path (ncu: 79-88 % of peak L1 wavefronts on the
-// dominant kernels, profiles/r01_v10_*, r01_v8_*); the design minimises load instructions and sectors per
-// candidate evaluation: 8-byte packed exact texels at levels 0-1 (u8, 10-bit), a zero
-// border instead of per-tap bounds checks, the target patch rows every candidate reads held in registers
-// across a pixel's candidates, an exact integer guide term (dp4a) where the contract proves it equal to
-// the FP32 sum, exact integer remap sums, and occupancy bounds tuned per kernel.
+// patches).  The bound resources are the L1/shared data path and the issue rate (ncu: 81-89 % of peak L1
+// wavefronts and 65-85 % issue on the top kernels, profiles/r02_v6_*, r02_v5_*); the design minimises the work
+// and the load instructions per candidate evaluation: exact elimination (a Cauchy-Schwarz
+// patch-sum bound before any patch row is read, partial distances after three rows), 8-byte packed exact
+// texels at levels 0-1 (u8, 10-bit), a zero border instead of per-tap bounds checks, target tiles staged by
+// the TMA bulk-copy engine, an exact integer guide term (dp4a) where the contract proves it equal to the FP32
+// sum, exact integer remap sums, and occupancy bounds tuned per kernel.
 //
 // Every floating-point operation that decides a result is written with an explicit IEEE intrinsic
 // (__fadd_rn, __fsub_rn, __fmaf_rn, __fdiv_rn) in the order DESIGN.md §3 fixes (D20), so the kernels
