@@ -2087,6 +2087,11 @@ cudaError_t launch_iter13_fast(const FieldArgs& a0, int T, int p, int loss, cuda
         else return cudaErrorInvalidValue;
         return cudaGetLastError();
     }
+    if (p == 1 && loss != 3 && hy == 3) {  // p = 1: every target row from the shared tile (patch-sum bound on)
+        if (loss) k_iter13_fast<1, true, false, 0, 0><<<grid, block, 0, s>>>(a);
+        else k_iter13_fast<1, false, false, 0, 0><<<grid, block, 0, s>>>(a);
+        return cudaGetLastError();
+    }
     if (p == 3 && loss != 3) {  // level 0 at p = 3 (config 5): every target row from the shared tile
         if (loss) k_iter13_fast<3, true, false, 0, 0><<<grid, block, 0, s>>>(a);
         else k_iter13_fast<3, false, false, 0, 0><<<grid, block, 0, s>>>(a);
