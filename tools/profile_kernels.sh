@@ -24,7 +24,7 @@ cap gen1L1 "k_field_gen<\\(int\\)2, \\(bool\\)1, \\(int\\)1, \\(int\\)4" 1
 cap gen2L1 "k_field_gen<\\(int\\)2, \\(bool\\)1, \\(int\\)2, \\(int\\)4" 1
 cap gen3L1 "k_field_gen<\\(int\\)2, \\(bool\\)1, \\(int\\)3, \\(int\\)4" 1
 cap field123L0 "k_iter13_fast" 1
-cap tbarL1 "k_combine<\\(int\\)2, \\(int\\)3>" 1
+cap tbarL1 "k_combine<\\(int\\)2, \\(int\\)3>" 15  # level 1 (coarse-to-fine: levels 4, 3, 2 first)
 cap combine "k_combine<\\(int\\)2, \\(int\\)1>" 0
-cap gen3L2 "k_field_gen<\\(int\\)2, \\(bool\\)1, \\(int\\)3, \\(int\\)2" 1
+cap gen3L2 "k_field_gen<\\(int\\)2, \\(bool\\)1, \\(int\\)3, \\(int\\)2" 10  # level 2 (after levels 4, 3)
 ls -la gpurun_out
