@@ -44,6 +44,8 @@ struct fb_ctx_s {
     bool sum_bound = true;  // FB_OPT_SUM_BOUND: random-search candidates rejected by the patch-sum bound (level 0,
                             // and level 1 with FB_OPT_L1_FAST) before any patch row is gathered
     bool p3_fused = true;  // FB_OPT_P3_FUSED: level-0 fields 1-3 + random search in one launch at p = 3 as well
+    bool tail_bound = true;  // FB_OPT_TAIL_BOUND: the level-0 fused random search adds the partial + remainder
+                             // bound (tail-row sums plane next to the patch sums, p = 2, SF8 sources)
     int l1_fast = 0;  // FB_OPT_L1_FAST: level 1 of u8 sources (SF10) through 16-byte TF10 targets and the
                       // level-0 kernels -- 1: E init + field 0 by the shared-tile kernel, fields 1-3 + random
                       // search fused; 2: every field by the shared-tile kernel.  Bit-identical; 1 measured slower
@@ -307,8 +309,9 @@ struct Slots {
     size_t stride = 0;  // bytes per slot
     size_t off[24] = {};
     long long sum_off[24];  // patch-sum plane of level k inside a slot (kernels.h SumJob), or -1
+    long long tail_off[24];  // tail-row sums plane of level k (SumJob::tail), or -1
     int fmt0 = fbk::SF8;
-    Slots() { std::fill(sum_off, sum_off + 24, -1LL); }
+    Slots() { std::fill(sum_off, sum_off + 24, -1LL); std::fill(tail_off, tail_off + 24, -1LL); }
     const char* slot(long long i) const { return base + (size_t)i * stride; }
 };
 
@@ -331,6 +334,10 @@ Slots pack_sources(Exec& ex, const Geo& g, int fmt0, const std::vector<SlotSpec>
                           (f != fbk::SF10 || !ex.ctx->l1_fast || D * D * 1020 < 65536);
         S.sum_off[k] = sums ? (long long)off : -1;
         if (sums) off = (off + (size_t)g.PL[k].h * g.PL[k].w * sizeof(uint4) * (f == fbk::SF8F ? 2 : 1) + 255) & ~size_t(255);
+        // tail-row sums for the fused level-0 kernel's partial + remainder bound (p = 2, u8 sources)
+        const bool tail = sums && ex.ctx->tail_bound && f == fbk::SF8 && k == 0 && g.p == 2;
+        S.tail_off[k] = tail ? (long long)off : -1;
+        if (tail) off = (off + (size_t)g.PL[k].h * g.PL[k].w * sizeof(uint4) + 255) & ~size_t(255);
     }
     S.stride = off;
     const int n = (int)specs.size();
@@ -351,7 +358,10 @@ Slots pack_sources(Exec& ex, const Geo& g, int fmt0, const std::vector<SlotSpec>
             std::vector<fbk::SumJob> sj(n);
             for (int i = 0; i < n; ++i)
                 sj[i] = fbk::SumJob{S.base + (size_t)i * S.stride + S.off[k],
-                                    reinterpret_cast<uint4*>(S.base + (size_t)i * S.stride + S.sum_off[k])};
+                                    reinterpret_cast<uint4*>(S.base + (size_t)i * S.stride + S.sum_off[k]),
+                                    S.tail_off[k] >= 0
+                                        ? reinterpret_cast<uint4*>(S.base + (size_t)i * S.stride + S.tail_off[k])
+                                        : nullptr};
             const fbk::SumJob* dsj = ex.upload(sj);
             ex.launch("patch_sums", [&] { return fbk::launch_patch_sums(dsj, n, fmt, g.PL[k], g.p, ex.ctx->stream); },
                       (uint64_t)n * g.PL[k].h * g.PL[k].w);
@@ -511,6 +521,7 @@ BatchOut run_nnf(Exec& ex, const fb_match_cfg& cfg, const Geo& g, const Slots& s
             a.src_fmt = src_fmt(slots.fmt0, k);
             a.tgt_reg_rows = ex.ctx->tgt_reg_rows;
             a.sum_off = slots.sum_off[k];
+            a.tail_off = slots.tail_off[k];
             char names[4][32];
             for (int ph = 0; ph < 4; ++ph) snprintf(names[ph], sizeof names[ph], "field%d.L%d", ph, k);
             const int J = std::max(1, cfg.prop_scales);  // jump-flood scales (D41)
@@ -1205,6 +1216,7 @@ fb_status fb_set_option(fb_ctx ctx, int option, int value)
         break;
     case FB_OPT_SUM_BOUND: ctx->sum_bound = value != 0; break;
     case FB_OPT_P3_FUSED: ctx->p3_fused = value != 0; break;
+    case FB_OPT_TAIL_BOUND: ctx->tail_bound = value != 0; break;
     case FB_OPT_TGT_REG_ROWS:
         if (value < 0 || value > 3) { ctx->err = "tgt_reg_rows must be 0 (all), 1, 2 or 3 (none)"; return FB_ERR_INVALID_ARG; }
         ctx->tgt_reg_rows = value;

@@ -238,7 +238,7 @@ __global__ void k_pack_src(const PackSrc* __restrict__ jobs, int fmt, PLvl L)
 // source blocks: integer sums over the (2p+1)^2 patch (zero border = zero padding, D9), exact; the caller checks
 // that every sum fits its 21-bit field.  The patch rows are re-read per output texel (L1 hits).
 template <int P>
-__global__ void k_patch_sums(const SumJob* __restrict__ jobs, int fmt, PLvl L)
+__global__ void k_patch_sums(const SumJob* __restrict__ jobs, int fmt, PLvl L, int tail_r0)
 {
     constexpr int D = 2 * P + 1;
     const SumJob J = jobs[blockIdx.y];
@@ -265,7 +265,9 @@ __global__ void k_patch_sums(const SumJob* __restrict__ jobs, int fmt, PLvl L)
             continue;
         }
         uint32_t g0 = 0, g1 = 0, g2 = 0, s0 = 0, s1 = 0, s2 = 0;
+        uint32_t tl[3] = {0u, 0u, 0u};  // SF8 tail rows: {G.r | G.g << 16, G.b | S.r << 16, S.g | S.b << 16}
         for (int dr = 0; dr < D; ++dr) {
+            if (dr == tail_r0) { tl[0] = g0 | (g1 << 16); tl[1] = g2 | (s0 << 16); tl[2] = s1 | (s2 << 16); }
             const size_t row0 = (size_t)(r + dr - P + B) * L.pitch + (c - P + B);
 #pragma unroll
             for (int dc = 0; dc < D; ++dc) {
@@ -288,6 +290,8 @@ __global__ void k_patch_sums(const SumJob* __restrict__ jobs, int fmt, PLvl L)
         const unsigned long long lo = g0 | ((unsigned long long)g1 << 21) | ((unsigned long long)g2 << 42);
         const unsigned long long hi = s0 | ((unsigned long long)s1 << 21) | ((unsigned long long)s2 << 42);
         J.sums[i] = make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32));
+        if (J.tail)  // SF8 (sums < 2^16): the tail rows = the whole patch minus the rows before tail_r0
+            J.tail[i] = make_uint4((g0 | (g1 << 16)) - tl[0], (g2 | (s0 << 16)) - tl[1], (s1 | (s2 << 16)) - tl[2], 0u);
     }
 }
 
@@ -364,6 +368,27 @@ __device__ __forceinline__ bool csb_reject_f(uint4 qa, uint4 qb, const TSums& t,
         lb = __fmaf_rd(alpha, lb, __fmul_rd(__fmaf_rd(l2, l2, __fmaf_rd(l1, l1, __fmul_rd(l0, l0))), inv));
     }
     return __fmul_rd(lb, 1.0f - 0x1p-16f) >= e;
+}
+// Partial + remainder bound of the fused level-0 kernel: after the partial-distance check at row S1
+// fails, the FP32 partial P (rows < S1) plus Cauchy-Schwarz on the NT tail taps' sums (SumJob::tail q, target tail
+// sums tg01 = G.r | G.g << 16, tg2 = G.b (exact), a0..a2 (FP32, absolute error <= m: the whole patch's csb_margin
+// bounds the tail's few roundings)) is a lower bound of the candidate's FP32 loss up to 46 u: P over-states the
+// exact partial by <= 23 u, the full loss under-states the exact loss by <= 23 u (see the patch-sum bound above).
+// So rd((P + LB) (1 - 2^-16)) >= E implies the FP32 loss is >= E and the candidate cannot win (D16).
+template <int NT>
+__device__ __forceinline__ bool tail_reject(uint4 q, uint32_t tg01, uint32_t tg2, float a0, float a1, float a2,
+                                            float m, float alpha, float part, float e)
+{
+    const uint32_t d01 = __vabsdiffu2(tg01, q.x), d2 = __vabsdiffu2(tg2, q.y) & 0xFFFFu;
+    const uint32_t d0 = d01 & 0xFFFFu, d1 = d01 >> 16;
+    const uint32_t gg = d0 * d0 + d1 * d1 + d2 * d2;  // exact: < 3 * 2^32 / 2^8 for tail sums < 2^12
+    constexpr float kS = 1.0f - 0x1p-22f;
+    const float l0 = fmaxf(__fsub_rd(__fmul_rd(fabsf(__fsub_rn(a0, (float)(q.y >> 16))), kS), m), 0.0f);
+    const float l1 = fmaxf(__fsub_rd(__fmul_rd(fabsf(__fsub_rn(a1, (float)(q.z & 0xFFFFu))), kS), m), 0.0f);
+    const float l2 = fmaxf(__fsub_rd(__fmul_rd(fabsf(__fsub_rn(a2, (float)(q.z >> 16))), kS), m), 0.0f);
+    const float ls = __fmaf_rd(l2, l2, __fmaf_rd(l1, l1, __fmul_rd(l0, l0)));
+    const float lb = __fmul_rd(__fmaf_rd(alpha, __uint2float_rd(gg), ls), __frcp_rd((float)NT));
+    return __fmul_rd(__fadd_rd(part, lb), 1.0f - 0x1p-16f) >= e;
 }
 // Target patch sums of the bound for lane (lx, ly) of a warp-per-tile-row layout (tile column lx + j, row ly + dr):
 // column sums over the D rows (tile columns 32.. by lanes 0..2P-1), then the D columns by shuffles.  All 32 lanes
@@ -717,6 +742,9 @@ __global__ void k_remap_f3(const float* __restrict__ src, const int2* __restrict
 #endif
 #ifndef PDE_I13_S2
 #define PDE_I13_S2(P) (2 * (P) + 1)
+#endif
+#ifndef FB_TAIL_BOUND
+#define FB_TAIL_BOUND 1  // compile the partial + remainder bound (tail_reject) into the fused level-0 kernel
 #endif
 #ifndef PDE_GEN_S1
 #define PDE_GEN_S1(P) 1
@@ -1243,15 +1271,29 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? (P ==
     // the candidate cannot win the strict select (D16); its remaining rows are never loaded.  Results
     // are unchanged: selected candidates are always evaluated in full, in the D20 order.
     int cbase = 0;  // FB_COUNTERS: 0 propagation, 8 random search
-    auto loss = [&](int sr, int sc, float bound) -> float {
+    // partial + remainder bound (tail_reject) of the random search: the target's tail-row sums, set with the
+    // patch-sum bound's target sums
+    constexpr int S1 = PDE_I13_S1(P);
+    constexpr bool TB = FB_TAIL_BOUND && CSB && SF == 0 && SFL == 0 && TWO && P == 2 && S1 < D;
+    const bool use_tail = TB && use_csb && a.tail_off >= 0;
+    const uint4* TAIL = use_tail ? reinterpret_cast<const uint4*>(T.src + a.tail_off) : nullptr;
+    uint32_t tt01 = 0u, tt2 = 0u;
+    float tta0 = 0.0f, tta1 = 0.0f, tta2 = 0.0f, ttm = 0.0f;
+    auto loss = [&](int sr, int sc, float bound, bool tail) -> float {
         uint32_t dg = 0u;
         float dgf = 0.0f, ds = 0.0f;
         auto gsum = [&]() { return SF == 1 ? dgf : __uint2float_rn(dg); };
-        constexpr int S1 = PDE_I13_S1(P), S2 = PDE_I13_S2(P);
+        constexpr int S2 = PDE_I13_S2(P);
         FB_CNT(cbase + 0);
+        const uint4 q = TB && tail ? __ldg(TAIL + sr * w + sc) : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
         for (int dr = 0; dr < S1; ++dr) row(sr, sc, dr, dg, dgf, ds);
-        if (partial_loss(a.alpha, gsum(), ds, TWO) >= bound) { FB_CNT(cbase + 1); return __int_as_float(0x7f800000); }
+        const float part = partial_loss(a.alpha, gsum(), ds, TWO);
+        if (part >= bound) { FB_CNT(cbase + 1); return __int_as_float(0x7f800000); }
+        if (TB && tail && tail_reject<(D - S1) * D>(q, tt01, tt2, tta0, tta1, tta2, ttm, a.alpha, part, bound)) {
+            FB_CNT(21);
+            return __int_as_float(0x7f800000);
+        }
         if (S2 < D) {
 #pragma unroll
             for (int dr = S1; dr < S2; ++dr) row(sr, sc, dr, dg, dgf, ds);
@@ -1265,10 +1307,10 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? (P ==
     };
     // A candidate equal to the incumbent has exactly the incumbent's loss (same aux within the
     // iteration), so it cannot win the strict select (D16): skipping it changes nothing.
-    auto select = [&](int2& f, float& e, int sr, int sc) {
+    auto select = [&](int2& f, float& e, int sr, int sc, bool tail) {
         if (sr == f.x && sc == f.y) { FB_CNT(cbase + 5); return; }
         if (sr != f.x || sc != f.y) {  // an incumbent-equal candidate cannot win (see select)
-            const float e2 = loss(sr, sc, e);
+            const float e2 = loss(sr, sc, e, tail);
             if (e2 < e) { f = make_int2(sr, sc); e = e2; FB_CNT(cbase + 4); }
         }
     };
@@ -1304,13 +1346,15 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? (P ==
             const int2 fn = c + 1 < w ? nb : f;
             cand = make_int2(fn.x, max(fn.y - 1, 0));
         }
-        if (has) select(f, e, cand.x, cand.y);
+        if (has) select(f, e, cand.x, cand.y, false);
     }
     TSums ts{};
     if (use_csb) {  // target patch sums of the bound, warp converged: column sums over the D rows of the shared
                     // tile (columns 32.. by lanes 0..2P-1), then the D columns of each lane's patch by shuffles
         uint32_t cg[2][2] = {{0u, 0u}, {0u, 0u}};  // [main, extra] {g0 | g1 << 16, g2}
         float ca[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};  // {a0, a1, a2, max_c sum|a_c|}
+        uint32_t cgt[2][2] = {{0u, 0u}, {0u, 0u}};  // the same over the tail rows [S1, D) (tail_reject)
+        float cat[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
             float b0 = 0.f, b1 = 0.f, b2 = 0.f;
@@ -1324,11 +1368,17 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? (P ==
                 ca[x][0] = __fadd_rn(ca[x][0], t0); ca[x][1] = __fadd_rn(ca[x][1], t1);
                 ca[x][2] = __fadd_rn(ca[x][2], t2);
                 b0 = __fadd_ru(b0, fabsf(t0)); b1 = __fadd_ru(b1, fabsf(t1)); b2 = __fadd_ru(b2, fabsf(t2));
+                if (TB && dr >= S1) {
+                    cgt[x][0] += (v.x & 0xFFu) | (((v.x >> 8) & 0xFFu) << 16); cgt[x][1] += (v.x >> 16) & 0xFFu;
+                    cat[x][0] = __fadd_rn(cat[x][0], t0); cat[x][1] = __fadd_rn(cat[x][1], t1);
+                    cat[x][2] = __fadd_rn(cat[x][2], t2);
+                }
             }
             ca[x][3] = fmaxf(b0, fmaxf(b1, b2));
         }
         uint32_t g01 = cg[0][0], g2 = cg[0][1];  // 16-bit lanes: every sum <= D^2 * 1020 < 2^16
         float a0 = ca[0][0], a1 = ca[0][1], a2 = ca[0][2], m = ca[0][3];
+        if (TB) { tt01 = cgt[0][0]; tt2 = cgt[0][1]; tta0 = cat[0][0]; tta1 = cat[0][1]; tta2 = cat[0][2]; }
 #pragma unroll
         for (int j = 1; j < D; ++j) {
             const bool own = lane + j < 32;
@@ -1342,17 +1392,28 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? (P ==
             g01 += own ? x0 : y0; g2 += own ? x1 : y1;
             a0 = __fadd_rn(a0, own ? p0 : q0); a1 = __fadd_rn(a1, own ? p1 : q1); a2 = __fadd_rn(a2, own ? p2 : q2);
             m = __fadd_ru(m, own ? p3 : q3);
+            if (TB) {
+                const uint32_t u0 = __shfl_down_sync(0xffffffffu, cgt[0][0], j), v0 = __shfl_sync(0xffffffffu, cgt[1][0], src);
+                const uint32_t u1 = __shfl_down_sync(0xffffffffu, cgt[0][1], j), v1 = __shfl_sync(0xffffffffu, cgt[1][1], src);
+                const float r0 = __shfl_down_sync(0xffffffffu, cat[0][0], j), s0 = __shfl_sync(0xffffffffu, cat[1][0], src);
+                const float r1 = __shfl_down_sync(0xffffffffu, cat[0][1], j), s1 = __shfl_sync(0xffffffffu, cat[1][1], src);
+                const float r2 = __shfl_down_sync(0xffffffffu, cat[0][2], j), s2 = __shfl_sync(0xffffffffu, cat[1][2], src);
+                tt01 += own ? u0 : v0; tt2 += own ? u1 : v1;
+                tta0 = __fadd_rn(tta0, own ? r0 : s0); tta1 = __fadd_rn(tta1, own ? r1 : s1);
+                tta2 = __fadd_rn(tta2, own ? r2 : s2);
+            }
         }
         constexpr float gsc = SF == 1 ? 0.25f : 1.0f;
         ts = TSums{(float)(g01 & 0xFFFFu) * gsc, (float)(g01 >> 16) * gsc, (float)g2 * gsc, a0, a1, a2,
                    csb_margin<D>(m)};
+        ttm = ts.m;
     }
     if (!valid || lane == 0 || lane == 31) return;  // halo lanes only fed fields 1-2
 #pragma unroll
     for (int z = 0; z < 2; ++z)  // tracking fields T_{i-1}, T_{i+1} (D42)
         if (T.trk[z]) {
             const int2 g = __ldg(&T.trk[z][i]);
-            select(f, e, g.x, g.y);
+            select(f, e, g.x, g.y, false);
         }
     const uint4* SUMS = use_csb ? reinterpret_cast<const uint4*>(T.src + a.sum_off) : nullptr;
     constexpr float ssc = SF == 1 ? 0.25f : 1.0f;  // source sums: n = v (SF8) or n = 4 v (SF10)
@@ -1369,7 +1430,7 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? (P ==
             FB_CNT(14);
             continue;
         }
-        select(f, e, sr, sc);
+        select(f, e, sr, sc, use_tail);
     }
     FB_ASSERT((unsigned)f.x < (unsigned)h && (unsigned)f.y < (unsigned)w);
     a.Fout[t * a.fstride + i] = f;
@@ -1962,10 +2023,11 @@ cudaError_t launch_patch_sums(const SumJob* jobs, int n, int fmt, PLvl L, int p,
     if (fmt != SF8 && fmt != SF10 && fmt != SF16 && fmt != SF8F) return cudaErrorInvalidValue;
     cudaError_t e = cudaSuccess;
     FB_DISPATCH_P(p, (e = for_y_chunks(n, [&](long long y0, int m) {
-        k_patch_sums<PP><<<grid1d((long long)L.h * L.w, m), 256, 0, s>>>(jobs + y0, fmt, L);
+        k_patch_sums<PP><<<grid1d((long long)L.h * L.w, m), 256, 0, s>>>(jobs + y0, fmt, L, tail_row0(p));
     })));
     return e;
 }
+int tail_row0(int p) { return PDE_I13_S1(p); }
 
 template <int P>
 static cudaError_t launch_aux_remap_t(const DTask* tasks, int T, const int2* F, long long fstride, Lvl L, PLvl PL,

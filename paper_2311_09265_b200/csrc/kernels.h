@@ -102,15 +102,20 @@ struct FieldArgs {
     int pair0;             // general kernel phase 0 with E init: score E and the field-0 candidate together
     long long sum_off;     // byte offset of this level's patch-sum plane inside each source slot, or -1 (none):
                            // the random search then rejects candidates by the patch-sum bound
+    long long tail_off;    // byte offset of the tail-row sums plane (SumJob::tail), or -1: the fused level-0
+                           // kernel's random search then adds the partial + remainder bound
 };
 
-// Patch sums of a packed source level block (SF8 at level 0, SF10 at level 1): for every texel (r, c) of the
-// level, the sums over its (2p+1)^2 patch (zero padding, D9) of the integer fields n of each guide and style
-// channel, as uint4 {sG.r | sG.g << 16, sG.b | sS.r << 16, sS.g | sS.b << 16, 0} at [r * w + c]; every sum
-// is below 2^16 (checked by the caller: (2p+1)^2 * max n < 2^16).
+// Patch sums of a packed source level block (SF8 at level 0, SF10 at level 1, SF16 above, SF8F): for every texel
+// (r, c) of the level, the sums over its (2p+1)^2 patch (zero padding, D9) of the integer fields n of each guide
+// and style channel, as uint4 {lo, hi} of 21-bit fields (lo = sG.r | sG.g << 21 | sG.b << 42, hi the same of sS)
+// at [r * w + c]; every sum is below 2^21 (checked by the caller).  SF8F: two uint4 per texel (see k_patch_sums).
+// `tail` (SF8 only, nullable): the sums over the patch's last rows [tail_r0, 2p+1) -- the rows the fused level-0
+// kernel scores after its partial-distance check -- as uint4 {G.r | G.g << 16, G.b | S.r << 16, S.g | S.b << 16, 0}.
 struct SumJob {
     const char* blk;  // packed level block (copy 0)
     uint4* sums;      // [h * w]
+    uint4* tail;      // [h * w] or NULL
 };
 
 // Packing jobs: one per (slot, level) for sources, one per task/group for BASE targets.
@@ -128,6 +133,8 @@ cudaError_t launch_u8_to_pyr0(const uint8_t* frames, float4* pyr, int B, int H, 
 cudaError_t launch_box(float4* pyr, int B, long long pyr_stride, Lvl prev, Lvl cur, cudaStream_t s);
 cudaError_t launch_pack_src(const PackSrc* jobs, int n, int fmt, PLvl L, cudaStream_t s);
 cudaError_t launch_patch_sums(const SumJob* jobs, int n, int fmt, PLvl L, int p, cudaStream_t s);
+// first tail row of SumJob::tail for patch radius p (the fused level-0 kernel's partial-distance check row)
+int tail_row0(int p);
 cudaError_t launch_pack_tgt_guide(const DTask* tasks, int T, Lvl L, PLvl P, int tfmt, cudaStream_t s);
 cudaError_t launch_init(const DTask* tasks, int T, int2* F, long long fstride, Lvl L, int identity, Rng rng,
                         uint32_t level, cudaStream_t s);

@@ -21,6 +21,7 @@ DIRECT, TREE = 0, 1
 INIT_RANDOM, INIT_IDENTITY = 0, 1
 OP_NNF, OP_BLEND_DIRECT, OP_BLEND_TREE, OP_INTERPOLATE = 0, 1, 2, 3
 OPT_FUSED_ITER, OPT_FUSE13, OPT_PHASE0_MID, OPT_TGT_REG_ROWS, OPT_L1_FAST, OPT_SUM_BOUND, OPT_P3_FUSED = 0, 1, 2, 3, 4, 5, 6
+OPT_TAIL_BOUND = 7
 TAG_DIRECT, TAG_TREE_BUILD_F, TAG_TREE_QUERY_F, TAG_TREE_BUILD_R, TAG_TREE_QUERY_R, TAG_INTERP, TAG_API = range(7)
 
 STATUS = {0: "FB_OK", 1: "FB_ERR_INVALID_ARG", 2: "FB_ERR_SHAPE", 3: "FB_ERR_CUDA", 4: "FB_ERR_NCCL",

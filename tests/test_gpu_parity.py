@@ -521,6 +521,25 @@ def test_patch_sum_bound_matches_oracle(fb, loss, H, W, sb, l1, rows):
         assert_frames(X, Xr)
 
 
+@pytest.mark.parametrize("loss,H,W,tail", [(2, 96, 112, 1), (1, 135, 67, 1), (2, 67, 135, 0), (1, 96, 112, 0),
+                                            (2, 160, 192, 1)])
+def test_tail_bound_matches_oracle(fb, loss, H, W, tail):
+    """The fused level-0 random search's partial + remainder bound (FB_OPT_TAIL_BOUND: FP32 partial
+    of the first three patch rows plus Cauchy-Schwarz on the last two rows' sums) only skips candidates that
+    provably lose: NNF, E and the candidate count equal the oracle's bit for bit with the bound on and off, odd
+    sizes putting tail rows on the zero-padded border."""
+    c = fb.Context(0)
+    c.set_option(fb.fb.OPT_TAIL_BOUND, tail)
+    cfg, (sg, tg, ss, ts, keys), frames, tasks = _nnf_case(fb, loss, H, W, seed=61, n=3, levels=3)
+    group = [0] * len(keys) if loss == fb.MEAN_ALIGN else None
+    F, E, X, st = c.fb_nnf_estimate(cfg, dev(sg), dev(tg), dev(ss), dev(ts) if loss == 2 else None, group=group,
+                                    pair_keys=keys)
+    Fr, Er, Xr, ev = O.nnf(ocfg(cfg), frames, tasks, want_x=True)
+    assert st["candidate_evals"] == ev
+    assert_nnf(F, E, Fr, Er)
+    assert_frames(X, Xr)
+
+
 @pytest.mark.parametrize("sb,rows", [(0, 1), (1, 1), (1, 3)])
 def test_patch_sum_bound_tree_blend(fb, sb, rows):
     """Fast mode: the tree queries' float-style sources (SF8F blending-table cells) carry FP32 patch sums with an

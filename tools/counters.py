@@ -30,3 +30,5 @@ for name, b in (("propagation", 0), ("random search", 8)):
           f"full {full / max(ev, 1):.3f}, wins {win / max(ev, 1):.4f}, incumbent-equal skipped {same:.4g}")
 print(f"random search rejected by the patch-sum bound: {c[14]:.4g} "
       f"({c[14] / max(c[14] + c[8], 1):.3f} of candidates that differ from the incumbent)")
+print(f"random search rejected by the partial + remainder bound after row 3: {c[21]:.4g} "
+      f"({c[21] / max(c[8], 1):.3f} of its loss calls)")
