@@ -121,9 +121,9 @@ uint64_t fb_launch_count(fb_ctx ctx);
  *                          patch rows; the bound only skips candidates that provably lose, DESIGN.md §6;
  *                          used at every level with exact packed sources and for float-style table cells)
  *   FB_OPT_P3_FUSED     1  0 = at p = 3, level-0 fields 1-3 and the random search as separate launches
- *   FB_OPT_TAIL_BOUND   1  0 = no partial + remainder bound in the level-0 fused random search (p = 2, exact u8
- *                          sources: the FP32 partial of the first rows plus Cauchy-Schwarz on the remaining rows'
- *                          sums; only skips candidates that provably lose)
+ *   FB_OPT_TAIL_BOUND   0  1 = the level-0 fused random search adds the partial + remainder bound (p = 2, exact
+ *                          u8 sources: the FP32 partial of the first rows plus Cauchy-Schwarz on the remaining
+ *                          rows' sums; only skips candidates that provably lose; measured slower)
  * Errors: FB_ERR_INVALID_ARG (unknown option or value). */
 typedef enum { FB_OPT_FUSED_ITER = 0, FB_OPT_FUSE13 = 1, FB_OPT_PHASE0_MID = 2, FB_OPT_TGT_REG_ROWS = 3,
                FB_OPT_L1_FAST = 4, FB_OPT_SUM_BOUND = 5, FB_OPT_P3_FUSED = 6,

@@ -44,8 +44,9 @@ struct fb_ctx_s {
     bool sum_bound = true;  // FB_OPT_SUM_BOUND: random-search candidates rejected by the patch-sum bound (level 0,
                             // and level 1 with FB_OPT_L1_FAST) before any patch row is gathered
     bool p3_fused = true;  // FB_OPT_P3_FUSED: level-0 fields 1-3 + random search in one launch at p = 3 as well
-    bool tail_bound = true;  // FB_OPT_TAIL_BOUND: the level-0 fused random search adds the partial + remainder
-                             // bound (tail-row sums plane next to the patch sums, p = 2, SF8 sources)
+    bool tail_bound = false;  // FB_OPT_TAIL_BOUND: the level-0 fused random search adds the partial + remainder
+                              // bound (tail-row sums plane next to the patch sums, p = 2, SF8 sources); its
+                              // registers keep the kernel at 8 CTAs/SM, which loses to 10 without it
     int l1_fast = 0;  // FB_OPT_L1_FAST: level 1 of u8 sources (SF10) through 16-byte TF10 targets and the
                       // level-0 kernels -- 1: E init + field 0 by the shared-tile kernel, fields 1-3 + random
                       // search fused; 2: every field by the shared-tile kernel.  Bit-identical; 1 measured slower

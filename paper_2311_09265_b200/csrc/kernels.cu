@@ -743,9 +743,6 @@ __global__ void k_remap_f3(const float* __restrict__ src, const int2* __restrict
 #ifndef PDE_I13_S2
 #define PDE_I13_S2(P) (2 * (P) + 1)
 #endif
-#ifndef FB_TAIL_BOUND
-#define FB_TAIL_BOUND 1  // compile the partial + remainder bound (tail_reject) into the fused level-0 kernel
-#endif
 #ifndef PDE_GEN_S1
 #define PDE_GEN_S1(P) 1
 #endif
@@ -1108,7 +1105,7 @@ static constexpr int I13_TY = FB_I13_TY;
 // NR < D (hybrid target): only the first NR rows of each lane's target patch live in registers -- row 0 is
 // read by every candidate, rows >= 1 only by candidates that survive row 0 -- and the rest is read from a
 // shared-memory copy of the CTA's target tile.  Registers drop from 168 to <= 128: 4 CTAs/SM instead of 3.
-template <int P, bool TWO, bool PW = false, int SFL = 0, int NR = 2 * P + 1, int SF = 0>
+template <int P, bool TWO, bool PW = false, int SFL = 0, int NR = 2 * P + 1, int SF = 0, bool TL = false>
 #ifndef I13_HY_MINB
 #define I13_HY_MINB 5  // 96 registers, no spills: 5 CTAs/SM (N=48: 388 -> 357 ms; 6 and 7 spill and lose)
 #endif
@@ -1119,12 +1116,16 @@ template <int P, bool TWO, bool PW = false, int SFL = 0, int NR = 2 * P + 1, int
 #define I13_HY1_MINB 6  // one target row in registers
 #endif
 #ifndef I13_HY0_MINB
-#define I13_HY0_MINB 8  // no target row in registers (every row from the shared tile)
+#define I13_HY0_MINB 10  // no target row in registers, u8 sources: 48 registers (N=48 accurate 308 -> 302 ms against 8
+                         // CTAs at 64, 9: 305, 12: 315; balanced 247 -> 241 ms)
+#endif
+#ifndef I13_HY0X_MINB
+#define I13_HY0X_MINB 8  // the same with SF8F cells (fast mode: 10 CTAs 97.4 vs 96.0 ms), SF10, the tail bound, p = 1
 #endif
 #ifndef I13_P3_MINB
 #define I13_P3_MINB 10  // p = 3 (7-texel rows): config-5 shard field123.L0 6 / 8 / 10 CTAs: 339 / 330 / 324 ms (separate launches 333)
 #endif
-__global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? (P == 3 ? I13_P3_MINB : I13_HY0_MINB) : (SFL ? I13_SFL_MINB : (NR == 1 ? I13_HY1_MINB : I13_HY_MINB))) : 3) k_iter13_fast(FieldArgs a)
+__global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? (P == 3 ? I13_P3_MINB : (P == 2 && !SFL && !SF && !TL ? I13_HY0_MINB : I13_HY0X_MINB)) : (SFL ? I13_SFL_MINB : (NR == 1 ? I13_HY1_MINB : I13_HY_MINB))) : 3) k_iter13_fast(FieldArgs a)
 {
     constexpr int D = 2 * P + 1;
     constexpr bool HY = NR < D;
@@ -1274,7 +1275,7 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? (P ==
     // partial + remainder bound (tail_reject) of the random search: the target's tail-row sums, set with the
     // patch-sum bound's target sums
     constexpr int S1 = PDE_I13_S1(P);
-    constexpr bool TB = FB_TAIL_BOUND && CSB && SF == 0 && SFL == 0 && TWO && P == 2 && S1 < D;
+    constexpr bool TB = TL && CSB && SF == 0 && SFL == 0 && TWO && P == 2 && S1 < D;
     const bool use_tail = TB && use_csb && a.tail_off >= 0;
     const uint4* TAIL = use_tail ? reinterpret_cast<const uint4*>(T.src + a.tail_off) : nullptr;
     uint32_t tt01 = 0u, tt2 = 0u;
@@ -2160,7 +2161,8 @@ cudaError_t launch_iter13_fast(const FieldArgs& a0, int T, int p, int loss, cuda
         return cudaGetLastError();
     }
     if (p == 2 && loss != 3 && hy >= 1) {
-        if (loss && hy == 3) k_iter13_fast<2, true, false, 0, 0><<<grid, block, 0, s>>>(a);
+        if (loss && hy == 3 && a.tail_off >= 0) k_iter13_fast<2, true, false, 0, 0, 0, true><<<grid, block, 0, s>>>(a);
+        else if (loss && hy == 3) k_iter13_fast<2, true, false, 0, 0><<<grid, block, 0, s>>>(a);
         else if (loss && hy == 1) k_iter13_fast<2, true, false, 0, 1><<<grid, block, 0, s>>>(a);
         else if (loss) k_iter13_fast<2, true, false, 0, 2><<<grid, block, 0, s>>>(a);
         else if (hy == 1) k_iter13_fast<2, false, false, 0, 1><<<grid, block, 0, s>>>(a);
