@@ -12,6 +12,9 @@
 // Every floating-point operation that decides a result is written with an explicit IEEE intrinsic
 // (__fadd_rn, __fsub_rn, __fmaf_rn, __fdiv_rn) in the order DESIGN.md §3 fixes (D20), so the kernels
 // are bit-identical to the contract regardless of scheduling or thread mapping.
+#include <algorithm>
+#include <mutex>
+#include <unordered_map>
 #include "kernels.h"
 
 #include <algorithm>
@@ -2018,6 +2021,43 @@ cudaError_t launch_upsample(const int2* Fc, int2* Ff, int T, long long fstride, 
     default: return cudaErrorInvalidValue;          \
     }
 
+// Shared-memory carve-out of the gather kernels: the smallest that still holds the occupancy the registers
+// allow (cudaOccupancyMaxActiveBlocksPerMultiprocessor) x (static shared memory + the 1 KB the driver reserves per
+// CTA), so the rest of the SM's 256 KB stays L1 cache for the patch gathers.  The driver's default picks a larger
+// carve-out (132 KB for the fused level-0 kernel, which needs 58): N=48 field123.L0 302 -> 299.5 ms; the maximum
+// carve-out (100 %) costs 11 %.  Set once per kernel; -DFB_CARVEOUT=<percent> forces one value (A/B builds).
+#ifndef FB_CARVEOUT
+#define FB_CARVEOUT -2  // -2: computed per kernel, -1: driver default
+#endif
+static void carve(const void* fn, int threads)
+{
+#if FB_CARVEOUT == -1
+    (void)fn; (void)threads;
+#else
+    static std::mutex mu;
+    static std::unordered_map<const void*, int> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count(fn)) return;
+    int pct = FB_CARVEOUT;
+    if (pct < 0) {
+        cudaFuncAttributes fa{};
+        int dev = 0, smem_max = 0, n = 0;
+        if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess || cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, 0) != cudaSuccess || smem_max <= 0) {
+            (void)cudaGetLastError();
+            done[fn] = -1;
+            return;
+        }
+        const long long need = (long long)n * ((long long)fa.sharedSizeBytes + 1024);
+        pct = (int)std::min<long long>(100, (need * 100 + smem_max - 1) / smem_max);
+    }
+    (void)cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    (void)cudaGetLastError();
+    done[fn] = pct;
+#endif
+}
+
 cudaError_t launch_patch_sums(const SumJob* jobs, int n, int fmt, PLvl L, int p, cudaStream_t s)
 {
     if (n <= 0) return cudaSuccess;
@@ -2038,10 +2078,10 @@ static cudaError_t launch_aux_remap_t(const DTask* tasks, int T, const int2* F, 
         const dim3 g = grid1d((long long)PL.rows * PL.pitch, n);
         const DTask* tk = tasks + y0;
         const int2* Fy = F + y0 * fstride;
-        if (sfmt == SF8) k_aux_remap<P, SF8><<<g, 256, 0, s>>>(tk, Fy, fstride, L, PL, tfmt, src_off);
-        else if (sfmt == SF10) k_aux_remap<P, SF10><<<g, 256, 0, s>>>(tk, Fy, fstride, L, PL, tfmt, src_off);
-        else if (sfmt == SF16) k_aux_remap<P, SF16><<<g, 256, 0, s>>>(tk, Fy, fstride, L, PL, tfmt, src_off);
-        else k_aux_remap<P, -1><<<g, 256, 0, s>>>(tk, Fy, fstride, L, PL, tfmt, src_off);
+        if (sfmt == SF8) { carve((const void*)k_aux_remap<P, SF8>, (int)(256)); k_aux_remap<P, SF8><<<g, 256, 0, s>>>(tk, Fy, fstride, L, PL, tfmt, src_off); }
+        else if (sfmt == SF10) { carve((const void*)k_aux_remap<P, SF10>, (int)(256)); k_aux_remap<P, SF10><<<g, 256, 0, s>>>(tk, Fy, fstride, L, PL, tfmt, src_off); }
+        else if (sfmt == SF16) { carve((const void*)k_aux_remap<P, SF16>, (int)(256)); k_aux_remap<P, SF16><<<g, 256, 0, s>>>(tk, Fy, fstride, L, PL, tfmt, src_off); }
+        else { carve((const void*)k_aux_remap<P, -1>, (int)(256)); k_aux_remap<P, -1><<<g, 256, 0, s>>>(tk, Fy, fstride, L, PL, tfmt, src_off); }
     });
 }
 
@@ -2061,11 +2101,11 @@ static cudaError_t launch_combine_t(const DOut* outs, int n_outs, const DMember*
         const dim3 g = grid1d(fmt >= 2 ? (long long)PL.rows * PL.pitch : (long long)h * w, n);
         const DOut* o = outs + y0;
         switch (fmt) {
-        case 0: k_combine<P, 0><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); break;
-        case 1: k_combine<P, 1><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); break;
-        case 2: k_combine<P, 2><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); break;
-        case 4: k_combine<P, 4><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); break;
-        default: k_combine<P, 3><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); break;
+        case 0: { carve((const void*)k_combine<P, 0>, (int)(256)); k_combine<P, 0><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); } break;
+        case 1: { carve((const void*)k_combine<P, 1>, (int)(256)); k_combine<P, 1><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); } break;
+        case 2: { carve((const void*)k_combine<P, 2>, (int)(256)); k_combine<P, 2><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); } break;
+        case 4: { carve((const void*)k_combine<P, 4>, (int)(256)); k_combine<P, 4><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); } break;
+        default: { carve((const void*)k_combine<P, 3>, (int)(256)); k_combine<P, 3><<<g, 256, 0, s>>>(o, mem, F, fstride, h, w, PL); } break;
         }
     });
 }
@@ -2095,10 +2135,10 @@ static void launch_field_gen(const FieldArgs& a, int T, int phase, cudaStream_t 
 {
     const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(TILE_X * TILE_Y);
     switch (phase) {
-    case 0: k_field_gen<P, TWO, 0, SFMT, PW><<<grid, block, 0, s>>>(a); break;
-    case 1: k_field_gen<P, TWO, 1, SFMT, PW><<<grid, block, 0, s>>>(a); break;
-    case 2: k_field_gen<P, TWO, 2, SFMT, PW><<<grid, block, 0, s>>>(a); break;
-    default: k_field_gen<P, TWO, 3, SFMT, PW><<<grid, block, 0, s>>>(a); break;
+    case 0: { carve((const void*)k_field_gen<P, TWO, 0, SFMT, PW>, (int)(block.x * block.y * block.z)); k_field_gen<P, TWO, 0, SFMT, PW><<<grid, block, 0, s>>>(a); } break;
+    case 1: { carve((const void*)k_field_gen<P, TWO, 1, SFMT, PW>, (int)(block.x * block.y * block.z)); k_field_gen<P, TWO, 1, SFMT, PW><<<grid, block, 0, s>>>(a); } break;
+    case 2: { carve((const void*)k_field_gen<P, TWO, 2, SFMT, PW>, (int)(block.x * block.y * block.z)); k_field_gen<P, TWO, 2, SFMT, PW><<<grid, block, 0, s>>>(a); } break;
+    default: { carve((const void*)k_field_gen<P, TWO, 3, SFMT, PW>, (int)(block.x * block.y * block.z)); k_field_gen<P, TWO, 3, SFMT, PW><<<grid, block, 0, s>>>(a); } break;
     }
 }
 
@@ -2107,10 +2147,10 @@ static void launch_field_fast(const FieldArgs& a, int T, int phase, cudaStream_t
 {
     const dim3 grid((unsigned)((long long)T * a.tiles_per_task)), block(TILE_X * FAST_TY);
     switch (phase) {
-    case 0: k_field_fast<P, TWO, 0, PW, SFL><<<grid, block, 0, s>>>(a); break;
-    case 1: k_field_fast<P, TWO, 1, PW, SFL><<<grid, block, 0, s>>>(a); break;
-    case 2: k_field_fast<P, TWO, 2, PW, SFL><<<grid, block, 0, s>>>(a); break;
-    default: k_field_fast<P, TWO, 3, PW, SFL><<<grid, block, 0, s>>>(a); break;
+    case 0: { carve((const void*)k_field_fast<P, TWO, 0, PW, SFL>, (int)(block.x * block.y * block.z)); k_field_fast<P, TWO, 0, PW, SFL><<<grid, block, 0, s>>>(a); } break;
+    case 1: { carve((const void*)k_field_fast<P, TWO, 1, PW, SFL>, (int)(block.x * block.y * block.z)); k_field_fast<P, TWO, 1, PW, SFL><<<grid, block, 0, s>>>(a); } break;
+    case 2: { carve((const void*)k_field_fast<P, TWO, 2, PW, SFL>, (int)(block.x * block.y * block.z)); k_field_fast<P, TWO, 2, PW, SFL><<<grid, block, 0, s>>>(a); } break;
+    default: { carve((const void*)k_field_fast<P, TWO, 3, PW, SFL>, (int)(block.x * block.y * block.z)); k_field_fast<P, TWO, 3, PW, SFL><<<grid, block, 0, s>>>(a); } break;
     }
 }
 
@@ -2135,48 +2175,48 @@ cudaError_t launch_iter13_fast(const FieldArgs& a0, int T, int p, int loss, cuda
     const int hy = a.tgt_reg_rows;  // hybrid target (rows in registers: 1, 2; 3 = none; 0 = all)
     if (a.src_fmt == SF10) {  // level 1: SF10 source + TF10 target (GUIDE_STYLE / MEAN_ALIGN, p = 2)
         if (p != 2 || (loss != 1 && loss != 2)) return cudaErrorInvalidValue;
-        if (hy == 3) k_iter13_fast<2, true, false, 0, 0, 1><<<grid, block, 0, s>>>(a);
-        else if (hy == 1) k_iter13_fast<2, true, false, 0, 1, 1><<<grid, block, 0, s>>>(a);
-        else k_iter13_fast<2, true, false, 0, 2, 1><<<grid, block, 0, s>>>(a);
+        if (hy == 3) { carve((const void*)k_iter13_fast<2, true, false, 0, 0, 1>, (int)(block.x * block.y * block.z)); k_iter13_fast<2, true, false, 0, 0, 1><<<grid, block, 0, s>>>(a); }
+        else if (hy == 1) { carve((const void*)k_iter13_fast<2, true, false, 0, 1, 1>, (int)(block.x * block.y * block.z)); k_iter13_fast<2, true, false, 0, 1, 1><<<grid, block, 0, s>>>(a); }
+        else { carve((const void*)k_iter13_fast<2, true, false, 0, 2, 1>, (int)(block.x * block.y * block.z)); k_iter13_fast<2, true, false, 0, 2, 1><<<grid, block, 0, s>>>(a); }
         return cudaGetLastError();
     }
     if (a.src_fmt == SF8F) {
         if (loss != 1 && loss != 2) return cudaErrorInvalidValue;
-        if (p == 1) k_iter13_fast<1, true, false, 1><<<grid, block, 0, s>>>(a);
-        else if (p == 2 && hy == 3) k_iter13_fast<2, true, false, 1, 0><<<grid, block, 0, s>>>(a);
-        else if (p == 2 && hy == 1) k_iter13_fast<2, true, false, 1, 1><<<grid, block, 0, s>>>(a);
-        else if (p == 2 && hy == 2) k_iter13_fast<2, true, false, 1, 2><<<grid, block, 0, s>>>(a);
-        else if (p == 2) k_iter13_fast<2, true, false, 1><<<grid, block, 0, s>>>(a);
+        if (p == 1) { carve((const void*)k_iter13_fast<1, true, false, 1>, (int)(block.x * block.y * block.z)); k_iter13_fast<1, true, false, 1><<<grid, block, 0, s>>>(a); }
+        else if (p == 2 && hy == 3) { carve((const void*)k_iter13_fast<2, true, false, 1, 0>, (int)(block.x * block.y * block.z)); k_iter13_fast<2, true, false, 1, 0><<<grid, block, 0, s>>>(a); }
+        else if (p == 2 && hy == 1) { carve((const void*)k_iter13_fast<2, true, false, 1, 1>, (int)(block.x * block.y * block.z)); k_iter13_fast<2, true, false, 1, 1><<<grid, block, 0, s>>>(a); }
+        else if (p == 2 && hy == 2) { carve((const void*)k_iter13_fast<2, true, false, 1, 2>, (int)(block.x * block.y * block.z)); k_iter13_fast<2, true, false, 1, 2><<<grid, block, 0, s>>>(a); }
+        else if (p == 2) { carve((const void*)k_iter13_fast<2, true, false, 1>, (int)(block.x * block.y * block.z)); k_iter13_fast<2, true, false, 1><<<grid, block, 0, s>>>(a); }
         else return cudaErrorInvalidValue;
         return cudaGetLastError();
     }
     if (p == 1 && loss != 3 && hy == 3) {  // p = 1: every target row from the shared tile (patch-sum bound on)
-        if (loss) k_iter13_fast<1, true, false, 0, 0><<<grid, block, 0, s>>>(a);
-        else k_iter13_fast<1, false, false, 0, 0><<<grid, block, 0, s>>>(a);
+        if (loss) { carve((const void*)k_iter13_fast<1, true, false, 0, 0>, (int)(block.x * block.y * block.z)); k_iter13_fast<1, true, false, 0, 0><<<grid, block, 0, s>>>(a); }
+        else { carve((const void*)k_iter13_fast<1, false, false, 0, 0>, (int)(block.x * block.y * block.z)); k_iter13_fast<1, false, false, 0, 0><<<grid, block, 0, s>>>(a); }
         return cudaGetLastError();
     }
     if (p == 3 && loss != 3) {  // level 0 at p = 3 (config 5): every target row from the shared tile
-        if (loss) k_iter13_fast<3, true, false, 0, 0><<<grid, block, 0, s>>>(a);
-        else k_iter13_fast<3, false, false, 0, 0><<<grid, block, 0, s>>>(a);
+        if (loss) { carve((const void*)k_iter13_fast<3, true, false, 0, 0>, (int)(block.x * block.y * block.z)); k_iter13_fast<3, true, false, 0, 0><<<grid, block, 0, s>>>(a); }
+        else { carve((const void*)k_iter13_fast<3, false, false, 0, 0>, (int)(block.x * block.y * block.z)); k_iter13_fast<3, false, false, 0, 0><<<grid, block, 0, s>>>(a); }
         return cudaGetLastError();
     }
     if (p == 2 && loss != 3 && hy >= 1) {
-        if (loss && hy == 3 && a.tail_off >= 0) k_iter13_fast<2, true, false, 0, 0, 0, true><<<grid, block, 0, s>>>(a);
-        else if (loss && hy == 3) k_iter13_fast<2, true, false, 0, 0><<<grid, block, 0, s>>>(a);
-        else if (loss && hy == 1) k_iter13_fast<2, true, false, 0, 1><<<grid, block, 0, s>>>(a);
-        else if (loss) k_iter13_fast<2, true, false, 0, 2><<<grid, block, 0, s>>>(a);
-        else if (hy == 1) k_iter13_fast<2, false, false, 0, 1><<<grid, block, 0, s>>>(a);
-        else k_iter13_fast<2, false, false, 0, 2><<<grid, block, 0, s>>>(a);
+        if (loss && hy == 3 && a.tail_off >= 0) { carve((const void*)k_iter13_fast<2, true, false, 0, 0, 0, true>, (int)(block.x * block.y * block.z)); k_iter13_fast<2, true, false, 0, 0, 0, true><<<grid, block, 0, s>>>(a); }
+        else if (loss && hy == 3) { carve((const void*)k_iter13_fast<2, true, false, 0, 0>, (int)(block.x * block.y * block.z)); k_iter13_fast<2, true, false, 0, 0><<<grid, block, 0, s>>>(a); }
+        else if (loss && hy == 1) { carve((const void*)k_iter13_fast<2, true, false, 0, 1>, (int)(block.x * block.y * block.z)); k_iter13_fast<2, true, false, 0, 1><<<grid, block, 0, s>>>(a); }
+        else if (loss) { carve((const void*)k_iter13_fast<2, true, false, 0, 2>, (int)(block.x * block.y * block.z)); k_iter13_fast<2, true, false, 0, 2><<<grid, block, 0, s>>>(a); }
+        else if (hy == 1) { carve((const void*)k_iter13_fast<2, false, false, 0, 1>, (int)(block.x * block.y * block.z)); k_iter13_fast<2, false, false, 0, 1><<<grid, block, 0, s>>>(a); }
+        else { carve((const void*)k_iter13_fast<2, false, false, 0, 2>, (int)(block.x * block.y * block.z)); k_iter13_fast<2, false, false, 0, 2><<<grid, block, 0, s>>>(a); }
         return cudaGetLastError();
     }
     if (p == 1) {
-        if (loss == 3) k_iter13_fast<1, true, true><<<grid, block, 0, s>>>(a);
-        else if (loss) k_iter13_fast<1, true><<<grid, block, 0, s>>>(a);
-        else k_iter13_fast<1, false><<<grid, block, 0, s>>>(a);
+        if (loss == 3) { carve((const void*)k_iter13_fast<1, true, true>, (int)(block.x * block.y * block.z)); k_iter13_fast<1, true, true><<<grid, block, 0, s>>>(a); }
+        else if (loss) { carve((const void*)k_iter13_fast<1, true>, (int)(block.x * block.y * block.z)); k_iter13_fast<1, true><<<grid, block, 0, s>>>(a); }
+        else { carve((const void*)k_iter13_fast<1, false>, (int)(block.x * block.y * block.z)); k_iter13_fast<1, false><<<grid, block, 0, s>>>(a); }
     } else if (p == 2) {
-        if (loss == 3) k_iter13_fast<2, true, true><<<grid, block, 0, s>>>(a);
-        else if (loss) k_iter13_fast<2, true><<<grid, block, 0, s>>>(a);
-        else k_iter13_fast<2, false><<<grid, block, 0, s>>>(a);
+        if (loss == 3) { carve((const void*)k_iter13_fast<2, true, true>, (int)(block.x * block.y * block.z)); k_iter13_fast<2, true, true><<<grid, block, 0, s>>>(a); }
+        else if (loss) { carve((const void*)k_iter13_fast<2, true>, (int)(block.x * block.y * block.z)); k_iter13_fast<2, true><<<grid, block, 0, s>>>(a); }
+        else { carve((const void*)k_iter13_fast<2, false>, (int)(block.x * block.y * block.z)); k_iter13_fast<2, false><<<grid, block, 0, s>>>(a); }
     } else {
         return cudaErrorInvalidValue;
     }
@@ -2190,13 +2230,13 @@ static void launch_field_mid(const FieldArgs& a, int T, int phase, cudaStream_t 
     switch (phase) {
     case 0:
         if constexpr (SF == 0 && SFL == 0) {
-            if (pair0 && a.einit) { k_field_mid<P, TWO, 0, SFL, SF, true><<<grid, block, 0, s>>>(a); break; }
+            if (pair0 && a.einit) { { carve((const void*)k_field_mid<P, TWO, 0, SFL, SF, true>, (int)(block.x * block.y * block.z)); k_field_mid<P, TWO, 0, SFL, SF, true><<<grid, block, 0, s>>>(a); } break; }
         }
-        k_field_mid<P, TWO, 0, SFL, SF><<<grid, block, 0, s>>>(a);
+        { carve((const void*)k_field_mid<P, TWO, 0, SFL, SF>, (int)(block.x * block.y * block.z)); k_field_mid<P, TWO, 0, SFL, SF><<<grid, block, 0, s>>>(a); }
         break;
-    case 1: k_field_mid<P, TWO, 1, SFL, SF><<<grid, block, 0, s>>>(a); break;
-    case 2: k_field_mid<P, TWO, 2, SFL, SF><<<grid, block, 0, s>>>(a); break;
-    default: k_field_mid<P, TWO, 3, SFL, SF><<<grid, block, 0, s>>>(a); break;
+    case 1: { carve((const void*)k_field_mid<P, TWO, 1, SFL, SF>, (int)(block.x * block.y * block.z)); k_field_mid<P, TWO, 1, SFL, SF><<<grid, block, 0, s>>>(a); } break;
+    case 2: { carve((const void*)k_field_mid<P, TWO, 2, SFL, SF>, (int)(block.x * block.y * block.z)); k_field_mid<P, TWO, 2, SFL, SF><<<grid, block, 0, s>>>(a); } break;
+    default: { carve((const void*)k_field_mid<P, TWO, 3, SFL, SF>, (int)(block.x * block.y * block.z)); k_field_mid<P, TWO, 3, SFL, SF><<<grid, block, 0, s>>>(a); } break;
     }
 }
 
