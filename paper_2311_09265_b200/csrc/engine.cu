@@ -326,7 +326,7 @@ Slots pack_sources(Exec& ex, const Geo& g, int fmt0, const std::vector<SlotSpec>
     for (int k = 0; k < g.Lv; ++k) {
         S.off[k] = off;
         const int f = src_fmt(fmt0, k);
-        const size_t copies = (f == fbk::SF8 || f == fbk::SF10) ? fbk::kSF8Copies : 1;
+        const size_t copies = f == fbk::SF8 ? fbk::kSF8Copies : (f == fbk::SF10 ? 2 : 1);
         off = (off + copies * g.PL[k].rows * g.PL[k].pitch * src_bytes(f) + 255) & ~size_t(255);
         // patch sums for the random-search bound (exact packed sources: SF8 at level 0, SF10, SF16); every sum
         // must fit its 21-bit field (and, through the fused kernel at level 1, its 16-bit target sums)

@@ -173,7 +173,7 @@ __global__ void k_pack_src(const PackSrc* __restrict__ jobs, int fmt, PLvl L)
 {
     const PackSrc J = jobs[blockIdx.y];
     const int n = L.rows * L.pitch;
-    const int copies = (fmt == SF8 || fmt == SF10) ? kSF8Copies : 1;
+    const int copies = fmt == SF8 ? kSF8Copies : (fmt == SF10 ? 2 : 1);
     for (int ii = blockIdx.x * blockDim.x + threadIdx.x; ii < n * copies; ii += gridDim.x * blockDim.x) {
         const int cpy = ii / n, i = ii - cpy * n;  // copy cpy holds texel (pr, pc + cpy) at (pr, pc)
         const int pr = i / L.pitch, pc = i - pr * L.pitch;
@@ -1445,6 +1445,15 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? (P ==
 // The target patch of p >= 3 does not fit in registers, so it is staged per tile; the source rows and the
 // exact integer guide term (every partial < 2^24 for p <= 4 at level 0) are those of k_field_fast.
 template <int P, bool TWO, int PHASE, int SFL = 0, int SF = 0, bool PR = false>
+// Source rows of the shared-memory-target kernel: 0 = from the aligned copy of the two SF8 copies (parity-free),
+// 1 = from copy 0 with parity selects except in the paired accurate phase 0 (default), 2 = copy 0 everywhere.  Its
+// candidates are coherent across lanes (the current F, the row-above neighbour's F), so reading one copy lets
+// adjacent lanes share lines: N=48 balanced field0.L0 58.7 -> 54.1 ms, fast 22.3 -> 21.5, config-5 shard
+// 107.3 -> 98.9 ms; the paired phase 0 loses with copy 0 (66.5 -> 74.0 ms: two rows of selects per tap), and so
+// does the fused fields-1-3 kernel (issue-bound on its selects).
+#ifndef FB_MID_COPY0
+#define FB_MID_COPY0 1
+#endif
 #ifndef MID_MINB
 #define MID_MINB 8  // p = 2 (phase 0): 8 CTAs/SM at 32 registers beats 5 at 44 (balanced N=48: 68 -> 62 ms)
 #endif
@@ -1546,9 +1555,11 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y, PR ? MIDP_MINB : (P == 2 ? (SF
             if (TWO) ds = __fadd_rn(ds, rs);
             return;
         }
+        constexpr bool C2 = kSF8Copies == 2 && (FB_MID_COPY0 == 0 || (FB_MID_COPY0 == 1 && PR));  // aligned copy, else
+                                                                                                 // copy 0 + selects
         const uint4* cp = reinterpret_cast<const uint4*>(
-            S + (kSF8Copies == 2 ? (size_t)(idx & 1) * plane + (idx & ~1) : (size_t)(idx & ~1)));
-        const int o = kSF8Copies == 2 ? 0 : (idx & 1);
+            S + (C2 ? (size_t)(idx & 1) * plane + (idx & ~1) : (size_t)(idx & ~1)));
+        const int o = C2 ? 0 : (idx & 1);
         uint32_t wd[4 * NCH];
 #pragma unroll
         for (int k = 0; k < NCH; ++k) {
@@ -1616,8 +1627,10 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y, PR ? MIDP_MINB : (P == 2 ? (SF
             uint32_t wa[4 * NCH], wb[4 * NCH];
             const int ia = (f.x + dr - P + B) * pitch + (f.y - P + B), ib = (cr + dr - P + B) * pitch + (cc - P + B);
             FB_ASSERT(FB_ROW_OK(ia, a.L, D) && FB_ROW_OK(ib, a.L, D));
-            const uint4* pa = reinterpret_cast<const uint4*>(S + (size_t)(ia & 1) * plane + (ia & ~1));
-            const uint4* pb = reinterpret_cast<const uint4*>(S + (size_t)(ib & 1) * plane + (ib & ~1));
+            constexpr bool C2P = kSF8Copies == 2 && FB_MID_COPY0 < 2;  // aligned copy, else copy 0 + selects
+            const uint4* pa = reinterpret_cast<const uint4*>(S + (C2P ? (size_t)(ia & 1) * plane : 0) + (ia & ~1));
+            const uint4* pb = reinterpret_cast<const uint4*>(S + (C2P ? (size_t)(ib & 1) * plane : 0) + (ib & ~1));
+            const int oa = C2P ? 0 : (ia & 1), ob = C2P ? 0 : (ib & 1);
 #pragma unroll
             for (int k = 0; k < NCH; ++k) {
                 const uint4 v = __ldg(pa + k);
@@ -1629,12 +1642,12 @@ __global__ void __launch_bounds__(TILE_X* TILE_Y, PR ? MIDP_MINB : (P == 2 ? (SF
 #pragma unroll
             for (int j = 0; j < D; ++j) {
                 const uint4 tv = tT[ly + dr][lx + j];
-                uint32_t d = __vabsdiffu4(wa[2 * j], tv.x);
+                uint32_t d = __vabsdiffu4(oa ? wa[2 * j + 2] : wa[2 * j], tv.x);
                 dgA = __dp4a(d, d, dgA);
-                d = __vabsdiffu4(wb[2 * j], tv.x);
+                d = __vabsdiffu4(ob ? wb[2 * j + 2] : wb[2 * j], tv.x);
                 dgB = __dp4a(d, d, dgB);
                 if (TWO) {
-                    const uint32_t sa = wa[2 * j + 1], sb = wb[2 * j + 1];
+                    const uint32_t sa = oa ? wa[2 * j + 3] : wa[2 * j + 1], sb = ob ? wb[2 * j + 3] : wb[2 * j + 1];
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) {
                         const float tc = __uint_as_float(ch == 0 ? tv.y : (ch == 1 ? tv.z : tv.w));
@@ -1983,7 +1996,7 @@ cudaError_t launch_box(float4* pyr, int Bn, long long pyr_stride, Lvl prev, Lvl 
 cudaError_t launch_pack_src(const PackSrc* jobs, int n, int fmt, PLvl L, cudaStream_t s)
 {
     if (n <= 0) return cudaSuccess;
-    const int copies = (fmt == SF8 || fmt == SF10) ? kSF8Copies : 1;
+    const int copies = fmt == SF8 ? kSF8Copies : (fmt == SF10 ? 2 : 1);
     return for_y_chunks(n, [&](long long y0, int m) {
         k_pack_src<<<grid1d((long long)L.rows * L.pitch * copies, m), 256, 0, s>>>(jobs + y0, fmt, L);
     });
