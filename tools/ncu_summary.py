@@ -47,7 +47,13 @@ def full(rep, out, evals=None):
                 wf = _num(d["l1tex__data_pipe_lsu_wavefronts.sum"][1])
             else:
                 key = [k for k in d if k.endswith("l1tex__data_pipe_lsu_wavefronts.avg")][0]
-                wf = _num(d[key][1]) * 148
+                if d[key][1] != "no data":
+                    wf = _num(d[key][1]) * 148
+                else:  # only the utilisation was captured: 1 wavefront per SM per cycle at 100 %
+                    pct = _num(d["l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"][1]) / 100
+                    t_ms = _num(d["gpu__time_duration.sum"][1])
+                    ghz = _num(d["sm__cycles_elapsed.avg.per_second"][1])
+                    wf = pct * t_ms * 1e-3 * ghz * 1e9 * 148
             lines.append(f"  l1tex__data_pipe_lsu_wavefronts (sum over 148 SMs) {wf:.4g}")
             rd = _num(d["dram__bytes_read.sum"][1]) * SCALE.get(d["dram__bytes_read.sum"][0], 1.0)
             wr = _num(d["dram__bytes_write.sum"][1]) * SCALE.get(d["dram__bytes_write.sum"][0], 1.0)
