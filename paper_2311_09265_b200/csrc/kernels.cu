@@ -68,6 +68,10 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v,
 #ifndef FB_TILE_TMA
 #define FB_TILE_TMA 1
 #endif
+// Random search of the fused level-0 kernel with the next step's patch-sum texel loaded one step ahead (exact)
+#ifndef FB_RS_PREFETCH
+#define FB_RS_PREFETCH 0
+#endif
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
 {
@@ -1423,6 +1427,40 @@ __global__ void __launch_bounds__(32 * I13_TY, NR < 2 * P + 1 ? (NR == 0 ? (P ==
     constexpr float ssc = SF == 1 ? 0.25f : 1.0f;  // source sums: n = v (SF8) or n = 4 v (SF10)
     cbase = 8;
     uint4 ru = make_uint4(0u, 0u, 0u, 0u);
+#if FB_RS_PREFETCH
+    // Software-pipelined bound (exact): step s+1's candidate and its patch-sum texel are loaded before step s is
+    // decided, from the incumbent as it stands; most steps are rejected by the bound and leave f unchanged, so
+    // the load is the one step s+1 needs; when step s moves f the candidate is recomputed and reloaded.
+    if (SFL == 0 && CSB && use_csb && a.rs_k > 0) {
+        ru = rs_block(a, T, i, 0);
+        int2 o = rs_offset(a, ru, 0);
+        int sr = clampi(f.x + o.x, 0, h - 1), sc = clampi(f.y + o.y, 0, w - 1);
+        uint4 sm = __ldg(SUMS + sr * w + sc);
+        for (int s = 0; s < a.rs_k; ++s) {
+            uint4 run = ru, smn = make_uint4(0u, 0u, 0u, 0u);
+            int2 on = make_int2(0, 0);
+            int srn = 0, scn = 0;
+            const bool more = s + 1 < a.rs_k;
+            if (more) {
+                if (!((s + 1) & 1)) run = rs_block(a, T, i, s + 1);
+                on = rs_offset(a, run, s + 1);
+                srn = clampi(f.x + on.x, 0, h - 1); scn = clampi(f.y + on.y, 0, w - 1);
+                smn = __ldg(SUMS + srn * w + scn);
+            }
+            if ((sr != f.x || sc != f.y) && csb_reject<D, TWO>(sm, ts, ssc, a.alpha, e)) {
+                FB_CNT(14);
+            } else {
+                const int2 f0 = f;
+                select(f, e, sr, sc, use_tail);
+                if (more && (f.x != f0.x || f.y != f0.y)) {
+                    srn = clampi(f.x + on.x, 0, h - 1); scn = clampi(f.y + on.y, 0, w - 1);
+                    smn = __ldg(SUMS + srn * w + scn);
+                }
+            }
+            ru = run; sr = srn; sc = scn; sm = smn;
+        }
+    } else
+#endif
     for (int s = 0; s < a.rs_k; ++s) {
         if (!(s & 1)) ru = rs_block(a, T, i, s);
         const int2 o = rs_offset(a, ru, s);
